@@ -1,0 +1,172 @@
+/*
+ * spgemm.h -- C ABI of the B200-native hash SpGEMM hot path.
+ *
+ * Method: Gustavson's row-wise SpGEMM C = A*B on CSR (§2,
+ * Fig:code_spgemm) with a hash-table accumulator in two phases,
+ * symbolic then numeric (Fig:hash_spgemm), optional per-row
+ * ascending column sort of C.  "P:n" = line n of PAPER.md.
+ *
+ * Conventions (all entry points):
+ *   - Matrix pointers inside spg_csr are DEVICE pointers on the current CUDA
+ *     device.  The caller owns every buffer and the stream; the library never
+ *     frees caller memory.  Inputs are never written.
+ *   - Scalars returned through int64_t* out-parameters are HOST pointers.
+ *   - `stream` is a cudaStream_t passed as void*.  Every call enqueues its
+ *     work on `stream` (it may fork to internal streams and joins back before
+ *     returning or before the stream's next work); NULL = legacy default stream.
+ *   - Every call returns spg_status; nothing aborts.  spg_last_error(ctx)
+ *     gives a message for the last failing call on that ctx.
+ *   - One spg_ctx per concurrent caller (a ctx holds the plan between the two
+ *     phases and a grow-only workspace).  A ctx is bound to the device that
+ *     was current at spg_ctx_create.
+ *   - Types: row_ptr int64, col_idx int32 in [0, ncols) with ncols <= 2^31-1
+ *     (0xFFFFFFFF is the hash table's empty key, "initialized by storing
+ *     -1"), values fp64.
+ *   - No CPU fallback: without a usable CUDA device every call that computes
+ *     returns SPG_ERR_CUDA.
+ */
+#ifndef SPGEMM_H_
+#define SPGEMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPG_OK = 0,
+    SPG_ERR_INVALID_ARG = 1,  /* NULL pointer, negative size, bad flag          */
+    SPG_ERR_DIM_MISMATCH = 2, /* A.ncols != B.nrows (A m x n, B n x k)    */
+    SPG_ERR_INDEX_RANGE = 3,  /* column outside [0, ncols) (spg_validate only)   */
+    SPG_ERR_OVERFLOW = 4,     /* a B row longer than 2^26, ncols > 2^31-1, ...   */
+    SPG_ERR_WORKSPACE = 5,    /* workspace allocation failed                     */
+    SPG_ERR_STATE = 6,        /* spg_numeric without a matching spg_symbolic     */
+    SPG_ERR_CUDA = 7          /* a CUDA runtime error (message in last_error)    */
+} spg_status;
+
+/* A CSR matrix (§2: rpts[n+1], cols[nnz], vals[nnz]).
+ * row_ptr[0] MAY be nonzero: a row-range view of a larger matrix is passed as
+ * (row_ptr + r0, nrows = r1 - r0) with the SAME col_idx/val base pointers;
+ * entries of row i are col_idx[row_ptr[i] .. row_ptr[i+1]-1].  Columns within
+ * a row must be unique; their order is arbitrary ("Any" input order,
+ * Tab:summary P:155). */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    const int64_t *row_ptr; /* device, [nrows + 1], nondecreasing              */
+    const int32_t *col_idx; /* device, indexed by row_ptr                       */
+    const double *val;      /* device, indexed by row_ptr; may be NULL for
+                               spg_symbolic / spg_validate                      */
+} spg_csr;
+
+/* Optional workspace allocator (e.g. the PyTorch caching allocator).  Called
+ * only when the ctx workspace must grow; `stream` is the cudaStream_t of the
+ * call.  If both are NULL the library uses cudaMalloc/cudaFree. */
+typedef void *(*spg_alloc_fn)(size_t bytes, void *stream, void *user);
+typedef void (*spg_free_fn)(void *ptr, void *stream, void *user);
+
+typedef struct spg_ctx spg_ctx;
+
+/* Host-visible summary of the last spg_symbolic (for tests and benches). */
+typedef struct {
+    int64_t nrows;          /* rows of A (= rows of C)                          */
+    int64_t flop_total;     /* sum_i flop_i                  */
+    int64_t nnz_total;      /* nnz(C) = C_row_ptr[nrows]                        */
+    int64_t max_row_flop;   /* max_i flop_i                                     */
+    int64_t max_row_nnz;    /* max_i nnz(c_i*)                                  */
+    int64_t sym_bin_rows[12]; /* rows per symbolic bin    */
+    int64_t num_bin_rows[12]; /* rows per numeric bin                           */
+} spg_info;
+
+spg_status spg_ctx_create(spg_ctx **ctx, spg_alloc_fn alloc, spg_free_fn free_fn,
+                          void *user);
+spg_status spg_ctx_destroy(spg_ctx *ctx);
+const char *spg_last_error(const spg_ctx *ctx);
+/* Number of kernels this ctx has launched so far (evidence for benches). */
+int64_t spg_launch_count(const spg_ctx *ctx);
+
+/* Per-launch timing (measurement aid; off by default).  With enable != 0
+ * every kernel launch of this ctx is bracketed by two CUDA events recorded
+ * on the stream that kernel runs on (internal streams included), so a bench
+ * can attribute device time to kernels without a profiler.  Records persist
+ * until spg_profile_reset.  spg_profile_count synchronizes on the recorded
+ * events and returns their number; spg_profile_record returns the kernel
+ * name (static string owned by the library) and duration in ms. */
+spg_status spg_profile_enable(spg_ctx *ctx, int enable);
+spg_status spg_profile_reset(spg_ctx *ctx);
+int64_t spg_profile_count(spg_ctx *ctx);
+spg_status spg_profile_record(spg_ctx *ctx, int64_t idx, const char **name, float *ms);
+
+/* Phase 1 -- symbolic (Fig:hash_spgemm l.1-14 and "Symbolic(rpts_C, A, B)",
+ * P:292-310; hashing P:283, "In symbolic phase, it is enough to insert keys",
+ * P:285).  Steps, all on the GPU: per-row flop (Fig:load_balance l.1-6),
+ * row binning by hash table size (lowest 2^n > min(N_col, flop)),
+ * per-bin hash symbolic kernels that count nnz(c_i*), exclusive scan into
+ * C_row_ptr.
+ *   A, B        : device CSR, A.ncols == B.nrows; values unused.
+ *   C_row_ptr   : device, caller-allocated int64[A.nrows + 1]; written with
+ *                 C's row pointer, C_row_ptr[0] = 0 (C-local even for a
+ *                 row-range view of A).
+ *   nnz_C       : host out, nnz(C) = C_row_ptr[A.nrows].
+ *   flop_total  : host out (may be NULL), sum of per-row flop.
+ * Blocks the calling thread for two small device->host reads (bin counts,
+ * then nnz and numeric bin counts).  Keeps the plan (flop, bins) in ctx for
+ * spg_numeric. */
+spg_status spg_symbolic(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
+                        int64_t *C_row_ptr, int64_t *nnz_C, int64_t *flop_total,
+                        void *stream);
+
+/* Phase 2 -- numeric ("Numeric(C, A, B)"; "In numeric phase ... we need
+ * to store the resulting value data"; optional ascending sort).
+ * Must follow spg_symbolic on the same ctx with the same A, B and C_row_ptr.
+ *   C_col_idx, C_val : device, caller-allocated with nnz_C entries.
+ *   sorted           : 0 = columns of each C row in unspecified order;
+ *                      1 = strictly increasing columns in every row.
+ * Asynchronous on `stream`.  Values are fp64 sums of fp64 products (order of
+ * accumulation unspecified). */
+spg_status spg_numeric(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
+                       const int64_t *C_row_ptr, int32_t *C_col_idx, double *C_val,
+                       int sorted, void *stream);
+
+/* Summary of the last spg_symbolic on this ctx (host struct). */
+spg_status spg_get_info(const spg_ctx *ctx, spg_info *info);
+
+/* Debug export of the last symbolic plan (device outputs, int64[A.nrows]):
+ *   flop_out : per-row flop (Fig:load_balance l.1-6), may be NULL
+ *   tsize_out: per-row symbolic hash table size of Fig:hash_spgemm
+ *              (lowest 2^n > min(N_col, flop_i)), may be NULL.
+ * Asynchronous on `stream`. */
+spg_status spg_plan_export(spg_ctx *ctx, int64_t *flop_out, int64_t *tsize_out,
+                           void *stream);
+
+/* RowsToThreads on the GPU (Fig:load_balance): per-row flop of
+ * A*B, prefix sum, offset[t] = lowbnd(flop_ps, floor(total*t/nparts)) for
+ * t = 1..nparts-1 (lowbnd = first id with flop_ps[id] >= value),
+ * offset[0] = 0, offset[nparts] = A.nrows.
+ *   offsets    : HOST out, int64[nparts + 1].
+ *   flop_total : HOST out (may be NULL).
+ * Blocks for the small device->host read. */
+spg_status spg_rows_to_parts(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
+                             int64_t nparts, int64_t *offsets, int64_t *flop_total,
+                             void *stream);
+
+/* Masked sum for triangle counting (Sec 5.6; BASELINE config 5):
+ * sum over stored C(i,j) with (i,j) in pattern(G) of (int64)C(i,j).
+ * C rows may be in any order; G rows MUST be sorted ascending; C.nrows ==
+ * G.nrows rows are matched by index, C a row block starting at row
+ * g_row_begin of G.  Result to HOST *sum (blocks for 8 bytes). */
+spg_status spg_mask_sum(spg_ctx *ctx, const spg_csr *C, const spg_csr *G,
+                        int64_t g_row_begin, int64_t *sum, void *stream);
+
+/* Validation of the CSR invariants (untimed): row_ptr nondecreasing, columns
+ * in [0, ncols); with check_sorted != 0 also strictly increasing columns per
+ * row (which implies uniqueness).  Returns SPG_OK or SPG_ERR_INDEX_RANGE /
+ * SPG_ERR_INVALID_ARG.  Blocks. */
+spg_status spg_validate(spg_ctx *ctx, const spg_csr *M, int check_sorted, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPGEMM_H_ */

@@ -1,0 +1,203 @@
+"""Torch-facing API over the C ABI.  PyTorch supplies device memory, streams
+and process groups; every step of the SpGEMM runs in libspgemm.so kernels.
+
+    C = spgemm(A, B, sorted=True)          # Gustavson hash SpGEMM, two phases
+    offs = rows_to_parts(A, B, nparts)      # RowsToThreads on the GPU (a8)
+    t = triangle_count(L, U, G)             # L*U, mask by G, sum/2 (a9)
+"""
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+@dataclass
+class DeviceCSR:
+    """CSR on a CUDA device: row_ptr int64[nrows+1] (row_ptr[0] may be > 0 for
+    a row-range view), col int32, val float64 (may be None)."""
+    nrows: int
+    ncols: int
+    row_ptr: torch.Tensor
+    col: torch.Tensor
+    val: torch.Tensor | None
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1].item() - self.row_ptr[0].item())
+
+    def rows(self, r0: int, r1: int) -> "DeviceCSR":
+        """Zero-copy row-range view [r0, r1)."""
+        return DeviceCSR(r1 - r0, self.ncols, self.row_ptr[r0:r1 + 1], self.col, self.val)
+
+    def c(self) -> _lib.spg_csr:
+        assert self.row_ptr.dtype == torch.int64 and self.row_ptr.is_contiguous()
+        assert self.col.dtype == torch.int32 and self.col.is_contiguous()
+        if self.val is not None:
+            assert self.val.dtype == torch.float64 and self.val.is_contiguous()
+        return _lib.spg_csr(self.nrows, self.ncols, self.row_ptr.data_ptr(),
+                            self.col.data_ptr() if self.col.numel() else 0,
+                            self.val.data_ptr() if (self.val is not None and self.val.numel()) else 0)
+
+    @staticmethod
+    def from_host(M, device="cuda", non_blocking: bool = False) -> "DeviceCSR":
+        """Copy a host CSR (synth.CSR-like: nrows, ncols, row_ptr, col, val)."""
+        dev = torch.device(device)
+        return DeviceCSR(int(M.nrows), int(M.ncols),
+                         torch.as_tensor(np.ascontiguousarray(M.row_ptr, np.int64)).to(dev, non_blocking=non_blocking),
+                         torch.as_tensor(np.ascontiguousarray(M.col, np.int32)).to(dev, non_blocking=non_blocking),
+                         torch.as_tensor(np.ascontiguousarray(M.val, np.float64)).to(dev, non_blocking=non_blocking))
+
+    def to_host(self):
+        rp = self.row_ptr.cpu().numpy()
+        rp = rp - rp[0]
+        s = int(self.row_ptr[0].item())
+        col = self.col[s:s + int(rp[-1])].cpu().numpy()
+        val = self.val[s:s + int(rp[-1])].cpu().numpy() if self.val is not None else None
+        return rp, col, val
+
+
+class Context:
+    """One spg_ctx (plan + grow-only workspace) bound to a CUDA device."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        with torch.cuda.device(self.device):
+            self.handle = _lib.spg_ctx_create()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.spg_ctx_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    @property
+    def launches(self) -> int:
+        return _lib.spg_launch_count(self.handle)
+
+    def info(self) -> dict:
+        return _lib.spg_get_info(self.handle)
+
+
+_tls = threading.local()
+
+
+def default_context(device=None) -> Context:
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    if dev not in cache:
+        cache[dev] = Context(dev)
+    return cache[dev]
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def spg_symbolic(A: DeviceCSR, B: DeviceCSR, ctx: Context | None = None):
+    """Phase 1: returns (C_row_ptr tensor, nnz(C), flop)."""
+    ctx = ctx or default_context()
+    rp = torch.empty(A.nrows + 1, dtype=torch.int64, device=A.row_ptr.device)
+    nnz, flop = _lib.spg_symbolic(ctx.handle, A.c(), B.c(), rp.data_ptr(), _stream())
+    return rp, nnz, flop
+
+
+def spg_numeric(A: DeviceCSR, B: DeviceCSR, C_row_ptr: torch.Tensor, nnz: int,
+                sorted: bool = True, ctx: Context | None = None,
+                out: tuple | None = None) -> DeviceCSR:
+    """Phase 2: allocates C.col/C.val (torch caching allocator) unless `out`
+    gives them, and fills them."""
+    ctx = ctx or default_context()
+    dev = A.row_ptr.device
+    if out is None:
+        col = torch.empty(nnz, dtype=torch.int32, device=dev)
+        val = torch.empty(nnz, dtype=torch.float64, device=dev)
+    else:
+        col, val = out
+    _lib.spg_numeric(ctx.handle, A.c(), B.c(), C_row_ptr.data_ptr(),
+                     col.data_ptr() if nnz else 0, val.data_ptr() if nnz else 0, sorted, _stream())
+    return DeviceCSR(A.nrows, B.ncols, C_row_ptr, col, val)
+
+
+def spgemm(A: DeviceCSR, B: DeviceCSR, sorted: bool = True,
+           ctx: Context | None = None) -> DeviceCSR:
+    """C = A*B (Gustavson, hash accumulator, two phases)."""
+    if A.ncols != B.nrows:
+        raise ValueError(f"dimension mismatch: A is {A.nrows}x{A.ncols}, B is {B.nrows}x{B.ncols}")
+    ctx = ctx or default_context()
+    rp, nnz, _ = spg_symbolic(A, B, ctx)
+    return spg_numeric(A, B, rp, nnz, sorted, ctx)
+
+
+def plan_export(ctx: Context | None = None, m: int | None = None):
+    """(flop[m], paper table size[m]) of the last symbolic on ctx."""
+    ctx = ctx or default_context()
+    m = ctx.info()["nrows"] if m is None else m
+    f = torch.empty(m, dtype=torch.int64, device=ctx.device)
+    t = torch.empty(m, dtype=torch.int64, device=ctx.device)
+    if m:
+        _lib.spg_plan_export(ctx.handle, f.data_ptr(), t.data_ptr(), _stream())
+    return f, t
+
+
+def rows_to_parts(A: DeviceCSR, B: DeviceCSR, nparts: int, ctx: Context | None = None):
+    """offset[0..nparts] of Fig:load_balance computed on the GPU; and total flop."""
+    ctx = ctx or default_context()
+    return _lib.spg_rows_to_parts(ctx.handle, A.c(), B.c(), nparts, _stream())
+
+
+def mask_sum(C: DeviceCSR, G: DeviceCSR, g_row_begin: int = 0, ctx: Context | None = None) -> int:
+    ctx = ctx or default_context()
+    return _lib.spg_mask_sum(ctx.handle, C.c(), G.c(), g_row_begin, _stream())
+
+
+def validate(M: DeviceCSR, check_sorted: bool = False, ctx: Context | None = None) -> None:
+    ctx = ctx or default_context()
+    _lib.spg_validate(ctx.handle, M.c(), check_sorted, _stream())
+
+
+def row_blocks_by_bytes(A: DeviceCSR, B: DeviceCSR, budget_entries: int,
+                        ctx: Context | None = None) -> list[int]:
+    """Row offsets of blocks whose C holds at most ~budget_entries entries,
+    bounded through flop (nnz(c_i) <= flop_i): RowsToThreads with enough parts."""
+    ctx = ctx or default_context()
+    _, tot = rows_to_parts(A, B, 1, ctx)
+    nparts = max(1, -(-tot // max(1, budget_entries)))
+    offs, _ = rows_to_parts(A, B, nparts, ctx)
+    out = [offs[0]]
+    for o in offs[1:]:
+        if o != out[-1]:
+            out.append(o)
+    if out[-1] != A.nrows:
+        out.append(A.nrows)
+    return out
+
+
+def triangle_count(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, sorted: bool = False,
+                   block_entries: int | None = None, ctx: Context | None = None) -> int:
+    """Triangles = sum(C o G)/2, C = L*U (Sec 5.6, BASELINE config 5).
+    C is produced and consumed in row blocks (row-range views of L) so it never
+    has to fit whole in HBM."""
+    ctx = ctx or default_context()
+    if block_entries is None:
+        free, _ = torch.cuda.mem_get_info(L.row_ptr.device)
+        block_entries = max(1 << 20, int(free * 0.6) // 12)
+    offs = row_blocks_by_bytes(L, U, block_entries, ctx)
+    total = 0
+    for r0, r1 in zip(offs[:-1], offs[1:]):
+        C = spgemm(L.rows(r0, r1), U, sorted, ctx)
+        total += mask_sum(C, G, r0, ctx)
+        del C
+    if total % 2:
+        raise RuntimeError("sum(C o G) is odd: G is not symmetric")
+    return total // 2

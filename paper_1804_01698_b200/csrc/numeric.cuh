@@ -1,0 +1,369 @@
+// numeric.cuh -- steps a6 (numeric hash accumulation) and a7 (optional sort).
+// "In numeric phase, however, we need to store the resulting value data.
+// Once the computation on the hash table finishes, the results are sorted by
+// column indices in ascending order (if necessary), and stored to memory as
+// output.".  Table size T = lowest 2^n >= 2 nnz(c_i) (reading R6).
+#pragma once
+#include "spg_internal.cuh"
+#include "symbolic.cuh"
+
+namespace spg {
+
+// Probe for key c, inserting it if absent; returns its slot.
+__device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int logT) {
+  const uint32_t mask = (1u << logT) - 1u;
+  uint32_t h = hash_slot(c, logT);
+  while (true) {
+    const uint32_t k = ((volatile uint32_t *)keys)[h];
+    if (k == c) return h;
+    if (k == kEmpty) {
+      const uint32_t old = atomicCAS(keys + h, kEmpty, c);
+      if (old == kEmpty || old == c) return h;
+    }
+    h = (h + 1u) & mask;
+  }
+}
+
+// Enumerate products of A row [as, ae) (chunks c0, c0+cstride, ... of 32
+// a_ik) and call f(active, col, a_ik * b_kj) once per lane per round; all 32
+// lanes call f (inactive lanes with active = false) so f may use warp
+// collectives.
+template <typename F>
+__device__ __forceinline__ void for_row_products(const DevCSR &A, const DevCSR &B, int64_t as,
+                                                 int64_t ae, int64_t c0, int64_t cstride,
+                                                 F &&f) {
+  const int lane = lane_id();
+  for (int64_t cb = as + c0 * 32; cb < ae; cb += cstride * 32) {
+    const int64_t e = cb + lane;
+    int len = 0;
+    int64_t bs = 0;
+    double a = 0.0;
+    if (e < ae) {
+      const int k = __ldg(A.col + e);
+      a = __ldg(A.val + e);
+      bs = __ldg(B.rp + k);
+      len = (int)(__ldg(B.rp + k + 1) - bs);
+    }
+    const int incl = warp_incl_scan(len);
+    const int excl = incl - len;
+    const int total = __shfl_sync(kFull, incl, 31);
+    for (int p0 = 0; p0 < total; p0 += 32) {
+      const int p = p0 + lane;
+      const int own = owner_lane(incl, p);
+      const int64_t obs = shfl_i64(bs, own);
+      const int oex = __shfl_sync(kFull, excl, own);
+      const double oa = shfl_f64(a, own);
+      uint32_t c = 0;
+      double v = 0.0;
+      const bool act = p < total;
+      if (act) {
+        const int64_t q = obs + (p - oex);
+        c = (uint32_t)__ldg(B.col + q);
+        v = oa * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+      }
+      f(act, c, v);
+    }
+  }
+}
+
+// Warp-cooperative bitonic sort of P (power of two) (key, val) pairs in smem.
+__device__ __forceinline__ void warp_bitonic(uint32_t *keys, double *vals, int P) {
+  const int lane = lane_id();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < (P >> 1); t += 32) {
+        const int i0 = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int i1 = i0 + j;
+        const bool up = (i0 & k) == 0;
+        const uint32_t a = keys[i0], b = keys[i1];
+        if ((a > b) == up) {
+          keys[i0] = b; keys[i1] = a;
+          const double va = vals[i0];
+          vals[i0] = vals[i1]; vals[i1] = va;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ void block_bitonic(uint32_t *keys, double *vals, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+        const int i0 = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int i1 = i0 + j;
+        const bool up = (i0 & k) == 0;
+        const uint32_t a = keys[i0], b = keys[i1];
+        if ((a > b) == up) {
+          keys[i0] = b; keys[i1] = a;
+          const double va = vals[i0];
+          vals[i0] = vals[i1]; vals[i1] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// W tier: one warp per row, warp-private keys[TMAX] + vals[TMAX] in smem.
+// Distinct keys of one round go to distinct slots, so the value add is a
+// plain read-modify-write; lanes that share a key in a round (found with
+// __match_any_sync) use the atomic add.  Rounds are separated by __syncwarp.
+// ---------------------------------------------------------------------------
+template <int TMAX, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restrict__ rows,
+                                                         int64_t nrows, DevCSR A, DevCSR B,
+                                                         const int64_t *__restrict__ c_rp,
+                                                         int32_t *__restrict__ c_col,
+                                                         double *__restrict__ c_val,
+                                                         int sorted) {
+  extern __shared__ double s_dyn_f64[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *vals = s_dyn_f64 + w * TMAX;
+  uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + w * TMAX;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t r = int64_t(blockIdx.x) * WARPS + w; r < nrows; r += int64_t(gridDim.x) * WARPS) {
+    const int i = rows[r];
+    const int64_t rp0 = c_rp[i];
+    const int nnz = (int)(c_rp[i + 1] - rp0);
+    const int logT = num_log2(nnz);
+    const int T = 1 << logT;
+    for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
+    __syncwarp();
+    for_row_products(A, B, A.rp[i], A.rp[i + 1], 0, 1, [&](bool act, uint32_t c, double v) {
+      uint32_t slot = 0;
+      if (act) slot = num_probe(keys, c, logT);
+      const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
+      if (act) {
+        if (__popc(grp) == 1) vals[slot] += v;   // c_ij <- c_ij + value (l.8)
+        else atomicAdd(vals + slot, v);
+      }
+      __syncwarp();
+    });
+    if (!sorted) {
+      int base = 0;
+      for (int s0 = 0; s0 < T; s0 += 32) {
+        const uint32_t k = keys[s0 + lane];
+        const bool occ = k != kEmpty;
+        const unsigned bal = __ballot_sync(kFull, occ);
+        if (occ) {
+          const int64_t o = rp0 + base + __popc(bal & lt_mask);
+          c_col[o] = (int32_t)k;
+          c_val[o] = vals[s0 + lane];
+        }
+        base += __popc(bal);
+      }
+    } else {
+      // compact occupied slots to the front (destination <= source), in order
+      int base = 0;
+      for (int s0 = 0; s0 < T; s0 += 32) {
+        const uint32_t k = keys[s0 + lane];
+        const double v = vals[s0 + lane];
+        const bool occ = k != kEmpty;
+        const unsigned bal = __ballot_sync(kFull, occ);
+        __syncwarp();
+        if (occ) {
+          const int d = base + __popc(bal & lt_mask);
+          keys[d] = k;
+          vals[d] = v;
+        }
+        base += __popc(bal);
+        __syncwarp();
+      }
+      int P = 1;
+      while (P < nnz) P <<= 1;
+      for (int s = nnz + lane; s < P; s += 32) keys[s] = kEmpty;
+      __syncwarp();
+      warp_bitonic(keys, vals, P);
+      for (int s = lane; s < nnz; s += 32) {
+        c_col[rp0 + s] = (int32_t)keys[s];
+        c_val[rp0 + s] = vals[s];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Block-wide unordered compaction of occupied slots of a table into C row.
+__device__ __forceinline__ void block_emit_unsorted(const uint32_t *keys, const double *vals,
+                                                    int64_t T, int64_t rp0, int32_t *c_col,
+                                                    double *c_val, int *s_cnt) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t s0 = int64_t(threadIdx.x & ~31); s0 < T; s0 += blockDim.x) {
+    const int64_t s = s0 + lane;
+    const uint32_t k = s < T ? keys[s] : kEmpty;
+    const bool occ = k != kEmpty;
+    const unsigned bal = __ballot_sync(kFull, occ);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(s_cnt, __popc(bal));
+    base = __shfl_sync(kFull, base, 0);
+    if (occ) {
+      const int64_t o = rp0 + base + __popc(bal & lt_mask);
+      c_col[o] = (int32_t)k;
+      c_val[o] = vals[s];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B tier: one block per row, keys/vals of T slots in dynamic smem, shared by
+// the block (atomic CAS for keys, atomic fp64 add for values).  Sorted output:
+// emit unordered into C, reload the row into smem, bitonic sort, store.
+// ---------------------------------------------------------------------------
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict__ rows,
+                                                       int64_t nrows, DevCSR A, DevCSR B,
+                                                       const int64_t *__restrict__ c_rp,
+                                                       int32_t *__restrict__ c_col,
+                                                       double *__restrict__ c_val, int sorted,
+                                                       int tmax) {
+  extern __shared__ double s_dyn_f64[];
+  __shared__ int s_cnt;
+  constexpr int NW = THREADS / 32;
+  const int w = threadIdx.x >> 5;
+  double *vals = s_dyn_f64;
+  uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + tmax);
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int i = rows[r];
+    const int64_t rp0 = c_rp[i];
+    const int nnz = (int)(c_rp[i + 1] - rp0);
+    const int logT = num_log2(nnz);
+    const int T = 1 << logT;
+    for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for_row_products(A, B, A.rp[i], A.rp[i + 1], w, NW, [&](bool act, uint32_t c, double v) {
+      if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
+    });
+    __syncthreads();
+    block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
+    if (sorted) {
+      __syncthreads();
+      int P = 1;
+      while (P < nnz) P <<= 1;
+      for (int s = threadIdx.x; s < P; s += THREADS) {
+        if (s < nnz) { keys[s] = (uint32_t)c_col[rp0 + s]; vals[s] = c_val[rp0 + s]; }
+        else keys[s] = kEmpty;
+      }
+      __syncthreads();
+      block_bitonic(keys, vals, P);
+      for (int s = threadIdx.x; s < nnz; s += THREADS) {
+        c_col[rp0 + s] = (int32_t)keys[s];
+        c_val[rp0 + s] = vals[s];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// G tier: one block per row, keys/vals in a per-block global slab (L2
+// atomics: CAS for keys, native fp64 RED for values).  Sorted output by a
+// bitmap rank over column chunks of kRankBits: set a bit per present column,
+// prefix-popcount, each key's output position is its rank.
+// ---------------------------------------------------------------------------
+constexpr int kRankBits = 1 << 20;               // columns per rank chunk
+constexpr int kRankWords = kRankBits / 32;       // 32768 words = 128 KB
+constexpr int kRankGroup = 64;                   // words per u16 prefix group
+constexpr int kRankGroups = kRankWords / kRankGroup;
+constexpr size_t kRankSmem = size_t(kRankWords) * 4 + size_t(kRankWords) * 2 +
+                             size_t(kRankGroups) * 4;
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restrict__ rows,
+                                                        int64_t nrows, DevCSR A, DevCSR B,
+                                                        const int64_t *__restrict__ c_rp,
+                                                        int32_t *__restrict__ c_col,
+                                                        double *__restrict__ c_val, int sorted,
+                                                        uint32_t *__restrict__ slab_keys,
+                                                        double *__restrict__ slab_vals,
+                                                        int64_t slabT) {
+  extern __shared__ uint32_t s_dyn_u32[];
+  __shared__ int s_cnt;
+  __shared__ long long s_chunk_base;
+  constexpr int NW = THREADS / 32;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *keys = slab_keys + int64_t(blockIdx.x) * slabT;
+  double *vals = slab_vals + int64_t(blockIdx.x) * slabT;
+  uint32_t *bm = s_dyn_u32;                                          // [kRankWords]
+  uint16_t *wpre = reinterpret_cast<uint16_t *>(bm + kRankWords);    // [kRankWords]
+  int *gpre = reinterpret_cast<int *>(wpre + kRankWords);           // [kRankGroups]
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int i = rows[r];
+    const int64_t rp0 = c_rp[i];
+    const int64_t nnz = c_rp[i + 1] - rp0;
+    const int logT = num_log2(nnz);
+    const int64_t T = int64_t(1) << logT;
+    for (int64_t s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
+    if (threadIdx.x == 0) { s_cnt = 0; s_chunk_base = 0; }
+    __syncthreads();
+    for_row_products(A, B, A.rp[i], A.rp[i + 1], w, NW, [&](bool act, uint32_t c, double v) {
+      if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
+    });
+    __syncthreads();
+    if (!sorted) {
+      block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
+    } else {
+      for (int64_t cbase = 0; cbase < B.ncols; cbase += kRankBits) {
+        const int64_t nbits = (B.ncols - cbase) < kRankBits ? (B.ncols - cbase) : kRankBits;
+        const int nwords = (int)((nbits + 31) >> 5);
+        for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;
+        __syncthreads();
+        for (int64_t s = threadIdx.x; s < T; s += THREADS) {
+          const uint32_t k = keys[s];
+          if (k != kEmpty && int64_t(k) >= cbase && int64_t(k) - cbase < nbits) {
+            const uint32_t off = (uint32_t)(int64_t(k) - cbase);
+            atomicOr(bm + (off >> 5), 1u << (off & 31u));
+          }
+        }
+        __syncthreads();
+        // per-group prefix: warp handles groups g = w, w + NW, ...; 2 words/lane
+        const int ngroups = (nwords + kRankGroup - 1) / kRankGroup;
+        for (int g = w; g < ngroups; g += NW) {
+          const int w0 = g * kRankGroup + 2 * lane;
+          const int c0 = w0 < nwords ? __popc(bm[w0]) : 0;
+          const int c1 = w0 + 1 < nwords ? __popc(bm[w0 + 1]) : 0;
+          const int incl = warp_incl_scan(c0 + c1);
+          const int ex = incl - c0 - c1;
+          if (w0 < nwords) wpre[w0] = (uint16_t)ex;
+          if (w0 + 1 < nwords) wpre[w0 + 1] = (uint16_t)(ex + c0);
+          if (lane == 31) gpre[g] = incl;
+        }
+        __syncthreads();
+        if (w == 0) {  // exclusive scan of group totals
+          int carry = 0;
+          for (int g0 = 0; g0 < ngroups; g0 += 32) {
+            const int g = g0 + lane;
+            const int v = g < ngroups ? gpre[g] : 0;
+            const int incl = warp_incl_scan(v);
+            if (g < ngroups) gpre[g] = carry + incl - v;
+            carry += __shfl_sync(kFull, incl, 31);
+          }
+          if (lane == 0) s_cnt = carry;  // set bits in this chunk
+        }
+        __syncthreads();
+        const long long cb = s_chunk_base;
+        for (int64_t s = threadIdx.x; s < T; s += THREADS) {
+          const uint32_t k = keys[s];
+          if (k != kEmpty && int64_t(k) >= cbase && int64_t(k) - cbase < nbits) {
+            const uint32_t off = (uint32_t)(int64_t(k) - cbase);
+            const uint32_t wd = off >> 5;
+            const int pos = gpre[wd / kRankGroup] + wpre[wd] +
+                            __popc(bm[wd] & ((1u << (off & 31u)) - 1u));
+            c_col[rp0 + cb + pos] = (int32_t)k;
+            c_val[rp0 + cb + pos] = vals[s];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_chunk_base += s_cnt;
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace spg

@@ -1,0 +1,292 @@
+// plan.cuh -- steps a1 (flop), a2 (bins), a4 (scan), a8 (partition), a9 (mask
+// sum) and validation.  Included once by spgemm.cu.
+#pragma once
+#include "spg_internal.cuh"
+
+namespace spg {
+
+// ---------------------------------------------------------------------------
+// a1 + a2 counts.  flop[i] = sum_{j in A_i} nnz(B_{col_j})
+// (Fig:load_balance l.1-6; "non-trivial scalar multiplications",
+// P:137).  G lanes cooperate on one row (G in {4,8,16,32}); also counts rows
+// per symbolic bin, the total / max flop and the longest B row touched.
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(256) k_flop_bin(DevCSR A, const int64_t *__restrict__ b_rp,
+                                                  int64_t ncols, int64_t *__restrict__ flop,
+                                                  PlanInfo *info, int count_bins) {
+  __shared__ unsigned s_bins[kMaxBins];
+  __shared__ unsigned long long s_sum, s_max, s_maxb;
+  if (threadIdx.x < kMaxBins) s_bins[threadIdx.x] = 0;
+  if (threadIdx.x == 0) { s_sum = 0; s_max = 0; s_maxb = 0; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  constexpr int kRowsPerWarp = 32 / G;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long my_sum = 0, my_max = 0, my_maxb = 0;
+  for (int64_t base = warp * kRowsPerWarp; base < A.nrows; base += nwarps * kRowsPerWarp) {
+    const int64_t i = base + lane / G;
+    if (i < A.nrows) {  // uniform inside the G-lane group
+      const int64_t s = A.rp[i], e = A.rp[i + 1];
+      int64_t f = 0, mb = 0;
+      for (int64_t j = s + gl; j < e; j += G) {
+        const int k = __ldg(A.col + j);
+        const int64_t len = __ldg(b_rp + k + 1) - __ldg(b_rp + k);
+        f += len;
+        mb = len > mb ? len : mb;
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) f += __shfl_xor_sync(gmask, f, o, G);
+      my_maxb = (unsigned long long)mb > my_maxb ? (unsigned long long)mb : my_maxb;
+      if (gl == 0) {
+        flop[i] = f;
+        my_sum += (unsigned long long)f;
+        my_max = (unsigned long long)f > my_max ? (unsigned long long)f : my_max;
+        if (count_bins) atomicAdd(&s_bins[sym_bin(f, ncols)], 1u);
+      }
+    }
+  }
+  my_sum = warp_sum(my_sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long t = __shfl_xor_sync(kFull, my_max, o);
+    my_max = t > my_max ? t : my_max;
+    t = __shfl_xor_sync(kFull, my_maxb, o);
+    my_maxb = t > my_maxb ? t : my_maxb;
+  }
+  if (lane == 0) {
+    atomicAdd(&s_sum, my_sum);
+    atomicMax(&s_max, my_max);
+    atomicMax(&s_maxb, my_maxb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_sum) atomicAdd(&info->flop_total, s_sum);
+    atomicMax(&info->max_flop, s_max);
+    atomicMax(&info->max_brow, s_maxb);
+  }
+  if (count_bins && threadIdx.x < kMaxBins && s_bins[threadIdx.x])
+    atomicAdd(&info->sym_count[threadIdx.x], (unsigned long long)s_bins[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// a2: group row ids by bin (counting sort on the bin id; block-aggregated
+// atomics).  mode 0 = symbolic bins from flop[i] (skip rows get row_nnz = 0);
+// mode 1 = numeric bins from nnz(c_i) = C_rp[i+1] - C_rp[i].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *__restrict__ key,
+                                                     int64_t ncols, int mode, PlanInfo *info,
+                                                     int32_t *__restrict__ rows_out,
+                                                     int64_t *__restrict__ row_nnz) {
+  __shared__ unsigned s_cnt[kMaxBins];
+  __shared__ unsigned long long s_base[kMaxBins];
+  if (threadIdx.x < kMaxBins) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int b = 0;
+  unsigned local = 0;
+  if (i < m) {
+    if (mode == 0) {
+      b = sym_bin(key[i], ncols);
+      if (b == SB_SKIP) row_nnz[i] = 0;
+    } else {
+      b = num_bin(key[i + 1] - key[i]);
+    }
+    if (b != 0) local = atomicAdd(&s_cnt[b], 1u);
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t > 0 && t < kMaxBins && s_cnt[t]) {
+    const unsigned long long *cnt = mode == 0 ? info->sym_count : info->num_count;
+    unsigned long long off = 0;
+    for (int u = 1; u < t; ++u) off += cnt[u];
+    s_base[t] = off + atomicAdd(&(mode == 0 ? info->cursor : info->num_cursor)[t],
+                                (unsigned long long)s_cnt[t]);
+  }
+  __syncthreads();
+  if (b != 0) rows_out[s_base[b] + local] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------------------
+// a4: exclusive scan of per-row nnz into C_row_ptr (Fig:hash_spgemm
+// "Allocate(cols_C, rpts_C[N_row])", implies the prefix sum).
+// In place on data = C_row_ptr + 1 (inclusive scan of row_nnz there gives the
+// exclusive row pointer).  Three passes: tile sums, scan of tile sums, tile
+// scan + offset.  The last pass also counts numeric bins and max nnz(c_i).
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ long long block_excl_scan_1024(long long v, long long *s_warp,
+                                                          long long *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long t = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long y = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+    long long yi = y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long t = __shfl_up_sync(kFull, yi, o);
+      if (lane >= o) yi += t;
+    }
+    s_warp[lane] = yi - y;  // exclusive warp offsets
+    if (lane == 31) s_warp[32] = yi;
+  }
+  __syncthreads();
+  long long r = s_warp[w] + x - v;
+  *total = s_warp[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const int64_t *__restrict__ data,
+                                                              int64_t n,
+                                                              int64_t *__restrict__ partial) {
+  __shared__ long long s_warp[33];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile;
+  long long s = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t) {
+    const int64_t idx = base + int64_t(t) * kScanThreads + threadIdx.x;
+    if (idx < n) s += data[idx];
+  }
+  long long tot;
+  block_excl_scan_1024(s, s_warp, &tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_partials(int64_t *__restrict__ partial,
+                                                                int64_t nb) {
+  __shared__ long long s_warp[33];
+  long long carry = 0;
+  for (int64_t base = 0; base < nb; base += kScanThreads) {
+    const int64_t idx = base + threadIdx.x;
+    long long v = idx < nb ? partial[idx] : 0;
+    long long tot;
+    long long ex = block_excl_scan_1024(v, s_warp, &tot);
+    if (idx < nb) partial[idx] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict__ data, int64_t n,
+                                                            const int64_t *__restrict__ partial,
+                                                            PlanInfo *info) {
+  __shared__ long long s_warp[33];
+  __shared__ unsigned s_bins[kMaxBins];
+  __shared__ unsigned long long s_max;
+  if (threadIdx.x < kMaxBins) s_bins[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_max = 0;
+  const int64_t base = int64_t(blockIdx.x) * kScanTile + int64_t(threadIdx.x) * kScanItems;
+  long long v[kScanItems];
+  long long s = 0;
+  unsigned long long mx = 0;
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t) {
+    const int64_t idx = base + t;
+    v[t] = idx < n ? data[idx] : 0;
+    s += v[t];
+    mx = (unsigned long long)v[t] > mx ? (unsigned long long)v[t] : mx;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t)
+    if (base + t < n && v[t] > 0) atomicAdd(&s_bins[num_bin(v[t])], 1u);
+  long long tot;
+  long long ex = block_excl_scan_1024(s, s_warp, &tot) + partial[blockIdx.x];
+#pragma unroll
+  for (int t = 0; t < kScanItems; ++t) {
+    const int64_t idx = base + t;
+    ex += v[t];
+    if (idx < n) data[idx] = ex;
+    if (idx == n - 1) info->nnz_total = (unsigned long long)ex;
+  }
+  atomicMax(&s_max, mx);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&info->max_nnz, s_max);
+  if (threadIdx.x > 0 && threadIdx.x < kMaxBins && s_bins[threadIdx.x])
+    atomicAdd(&info->num_count[threadIdx.x], (unsigned long long)s_bins[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// a8: lowbnd of floor(total*t/nparts) in the flop prefix (length m+1).
+// ---------------------------------------------------------------------------
+__global__ void k_lowbnd(const int64_t *__restrict__ ps, int64_t m, int64_t nparts,
+                         int64_t *__restrict__ offsets) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t > nparts) return;
+  if (t == 0) { offsets[0] = 0; return; }
+  if (t == nparts) { offsets[nparts] = m; return; }
+  const int64_t total = ps[m];
+  const int64_t q = total / nparts, r = total % nparts;
+  const int64_t target = q * t + (r * t) / nparts;  // floor(total * t / nparts)
+  int64_t lo = 0, hi = m + 1;                        // first id with ps[id] >= target
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (ps[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  offsets[t] = lo;
+}
+
+// ---------------------------------------------------------------------------
+// a9: sum over stored C(i,j) with (i,j) in pattern(G) of (int64)C(i,j)
+// (triangle counting, Sec 5.6; BASELINE config 5).  Warp per C row,
+// binary search of each C column in the sorted G row.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mask_sum(DevCSR C, DevCSR G, int64_t g_row_begin,
+                                                  PlanInfo *info) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  long long acc = 0;
+  for (int64_t i = warp; i < C.nrows; i += nwarps) {
+    const int64_t gs = G.rp[g_row_begin + i], ge = G.rp[g_row_begin + i + 1];
+    if (gs == ge) continue;
+    for (int64_t q = C.rp[i] + lane; q < C.rp[i + 1]; q += 32) {
+      const int j = C.col[q];
+      int64_t lo = gs, hi = ge;
+      while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (__ldg(G.col + mid) < j) lo = mid + 1; else hi = mid;
+      }
+      if (lo < ge && __ldg(G.col + lo) == j) acc += (long long)C.val[q];
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && acc) atomicAdd(&info->mask_sum, (unsigned long long)acc);
+}
+
+// ---------------------------------------------------------------------------
+// Validation (untimed): flags bit0 = row_ptr decreasing, bit1 = column out of
+// range, bit2 = row not strictly increasing (only when check_sorted).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_validate(DevCSR M, int check_sorted,
+                                                  unsigned long long *flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long f = 0;
+  for (int64_t i = warp; i < M.nrows; i += nwarps) {
+    const int64_t s = M.rp[i], e = M.rp[i + 1];
+    if (e < s) { f |= 1; continue; }
+    for (int64_t q = s + lane; q < e; q += 32) {
+      const int c = M.col[q];
+      if (c < 0 || (int64_t)c >= M.ncols) f |= 2;
+      if (check_sorted && q > s && M.col[q - 1] >= c) f |= 4;
+    }
+  }
+  if (f) atomicOr(flags, f);
+}
+
+}  // namespace spg

@@ -1,0 +1,144 @@
+// spg_internal.cuh -- shared device helpers of the sm_100a hash SpGEMM library.
+// Product code: never includes or links anything under oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spgemm.h"
+
+namespace spg {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;     // P:283 "initialized by storing -1"
+constexpr uint32_t kHashMul = 2654435761u;   // odd 32-bit constant (reading R5)
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kMinLogT = 5;                  // GPU tables are at least 32 slots
+constexpr int64_t kMaxBRow = int64_t(1) << 26;  // 32 rows * 2^26 < 2^31 per chunk
+
+// ---------------------------------------------------------------- bins
+// Symbolic bins by T_s = lowest 2^n > min(flop_i, ncols), raised
+// to >= 32 slots on the GPU.  Numeric bins by T_n = lowest 2^n >= 2 nnz(c_i)
+// (load <= 1/2, reading R6).
+enum SymBin { SB_SKIP = 0, SB_W128, SB_W1024, SB_B2K, SB_B4K, SB_B8K, SB_B16K, SB_B32K,
+              SB_G, SB_COUNT };
+enum NumBin { NB_SKIP = 0, NB_W256, NB_W1024, NB_B2K, NB_B4K, NB_B8K, NB_B16K, NB_G,
+              NB_COUNT };
+constexpr int kMaxBins = 12;
+
+struct DevCSR {
+  int64_t nrows, ncols;
+  const int64_t *__restrict__ rp;
+  const int32_t *__restrict__ col;
+  const double *__restrict__ val;
+};
+
+// Device-side plan summary (atomics target), mirrored to pinned host memory.
+struct PlanInfo {
+  unsigned long long flop_total;
+  unsigned long long max_flop;
+  unsigned long long max_brow;
+  unsigned long long nnz_total;
+  unsigned long long max_nnz;
+  unsigned long long sym_count[kMaxBins];
+  unsigned long long num_count[kMaxBins];
+  unsigned long long cursor[kMaxBins];
+  unsigned long long num_cursor[kMaxBins];
+  unsigned long long mask_sum;
+  unsigned long long flags;
+};
+
+__host__ __device__ __forceinline__ int log2_ceil64(uint64_t x) {  // smallest n: 2^n >= x
+  int n = 0;
+  while ((uint64_t(1) << n) < x) ++n;
+  return n;
+}
+
+// log2 of the paper's symbolic table size: lowest 2^n STRICTLY greater than
+// min(flop, ncols)  (Fig:hash_spgemm l.10-12).
+__host__ __device__ __forceinline__ int sym_log2_paper(int64_t flop, int64_t ncols) {
+  int64_t s = flop < ncols ? flop : ncols;
+  int n = 0;
+  while ((int64_t(1) << n) <= s) ++n;
+  return n;
+}
+
+__device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {
+  int n = sym_log2_paper(flop, ncols);
+  return n < kMinLogT ? kMinLogT : n;
+}
+
+__device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols) {
+  if (flop == 0) return SB_SKIP;
+  int n = sym_log2_gpu(flop, ncols);
+  if (n <= 7) return SB_W128;
+  if (n <= 10) return SB_W1024;
+  if (n <= 15) return SB_B2K + (n - 11);
+  return SB_G;
+}
+
+__device__ __forceinline__ int num_log2(int64_t nnz) {
+  int n = log2_ceil64(uint64_t(2 * nnz));
+  return n < kMinLogT ? kMinLogT : n;
+}
+
+__device__ __forceinline__ int num_bin(int64_t nnz) {
+  if (nnz == 0) return NB_SKIP;
+  int n = num_log2(nnz);
+  if (n <= 8) return NB_W256;
+  if (n <= 10) return NB_W1024;
+  if (n <= 14) return NB_B2K + (n - 11);
+  return NB_G;
+}
+
+// Fibonacci hashing: HIGH bits of col*H (reading R5 of DESIGN.md; the paper's
+// "multiplied by constant number and divided by hash table size to compute
+// the remainder", with the remainder taken on the high bits).
+__device__ __forceinline__ uint32_t hash_slot(uint32_t c, int logT) {
+  return (c * kHashMul) >> (32 - logT);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(kFull, v, o);
+    if (l >= o) v += t;
+  }
+  return v;
+}
+
+// Owner lane of flattened product p inside a chunk: number of lanes whose
+// inclusive end is <= p (ends are nondecreasing across lanes).
+__device__ __forceinline__ int owner_lane(int incl, int p) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    int v = __shfl_sync(kFull, incl, pos + s - 1);
+    if (v <= p) pos += s;
+  }
+  return pos;
+}
+
+__device__ __forceinline__ int64_t shfl_i64(int64_t v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
+
+__device__ __forceinline__ double shfl_f64(double v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
+
+// fp64 add into shared memory for the (rare) case where several lanes of one
+// round share a key: a CAS loop (sm_100a has no native fp64 ATOMS add).
+__device__ __forceinline__ void smem_add_f64(double *addr, double v) {
+  atomicAdd(addr, v);
+}
+
+}  // namespace spg

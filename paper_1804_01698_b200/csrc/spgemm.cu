@@ -1,0 +1,679 @@
+// spgemm.cu -- C ABI (include/spgemm.h) of the sm_100a hash SpGEMM hot path.
+// Host orchestration only: every step of the path runs in the kernels of
+// plan.cuh / symbolic.cuh / numeric.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "numeric.cuh"
+#include "plan.cuh"
+#include "spg_internal.cuh"
+#include "symbolic.cuh"
+
+using namespace spg;
+
+namespace {
+
+constexpr int kSubStreams = 4;
+constexpr int kWarps = 8;  // warps per block of the W tier
+
+struct Buf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct spg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  spg_alloc_fn alloc = nullptr;
+  spg_free_fn free_fn = nullptr;
+  void *user = nullptr;
+  std::string err;
+  Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
+  PlanInfo *host_info = nullptr;  // pinned
+  cudaStream_t sub[kSubStreams] = {};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[kSubStreams] = {};
+  int64_t launches = 0;
+  // optional per-launch timing (events on the stream each kernel runs on)
+  int profiling = 0;
+  struct Rec { const char *name; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  // plan of the last symbolic
+  bool have_plan = false;
+  const int64_t *plan_a_rp = nullptr, *plan_b_rp = nullptr, *plan_c_rp = nullptr;
+  int64_t plan_m = 0, plan_ncols = 0;
+  PlanInfo plan{};
+};
+
+namespace {
+
+spg_status fail(spg_ctx *c, spg_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+spg_status cuda_check(spg_ctx *c, cudaError_t e, const char *where) {
+  if (e == cudaSuccess) return SPG_OK;
+  return fail(c, SPG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaEvent_t prof_event(spg_ctx *c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+// Brackets one launch with events when profiling is on.
+struct ProfScope {
+  spg_ctx *c;
+  cudaStream_t s;
+  const char *name;
+  cudaEvent_t a = nullptr;
+  ProfScope(spg_ctx *c_, cudaStream_t s_, const char *n) : c(c_), s(s_), name(n) {
+    if (c->profiling && (a = prof_event(c))) cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = prof_event(c);
+    if (!b) return;
+    cudaEventRecord(b, s);
+    c->recs.push_back({name, a, b});
+  }
+};
+
+#define SPG_CUDA(ctx, expr)                                  \
+  do {                                                       \
+    spg_status _s = cuda_check((ctx), (expr), #expr);        \
+    if (_s != SPG_OK) return _s;                             \
+  } while (0)
+
+#define SPG_LAUNCHED(ctx, name)                                                   \
+  do {                                                                            \
+    (ctx)->launches++;                                                            \
+    spg_status _s = cuda_check((ctx), cudaGetLastError(), "launch " name);        \
+    if (_s != SPG_OK) return _s;                                                  \
+  } while (0)
+
+void buf_release(spg_ctx *c, Buf &b, cudaStream_t s) {
+  if (!b.p) return;
+  if (c->free_fn) c->free_fn(b.p, s, c->user);
+  else cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+spg_status buf_ensure(spg_ctx *c, Buf &b, size_t bytes, cudaStream_t s) {
+  if (bytes <= b.bytes && b.p) return SPG_OK;
+  buf_release(c, b, s);
+  size_t want = std::max(bytes, size_t(256));
+  void *p = nullptr;
+  if (c->alloc) {
+    p = c->alloc(want, s, c->user);
+  } else if (cudaMalloc(&p, want) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+  }
+  if (!p) return fail(c, SPG_ERR_WORKSPACE, "workspace allocation of " + std::to_string(want) + " bytes failed");
+  b.p = p;
+  b.bytes = want;
+  return SPG_OK;
+}
+
+DevCSR dev(const spg_csr *M) { return DevCSR{M->nrows, M->ncols, M->row_ptr, M->col_idx, M->val}; }
+
+spg_status check_csr(spg_ctx *c, const spg_csr *M, const char *name, bool need_val) {
+  if (!M) return fail(c, SPG_ERR_INVALID_ARG, std::string(name) + " is NULL");
+  if (M->nrows < 0 || M->ncols < 0)
+    return fail(c, SPG_ERR_INVALID_ARG, std::string(name) + " has negative dimensions");
+  if (M->nrows > INT32_MAX - 1 || M->ncols > INT32_MAX)
+    return fail(c, SPG_ERR_OVERFLOW, std::string(name) + ": dimensions above 2^31-1");
+  if (!M->row_ptr) return fail(c, SPG_ERR_INVALID_ARG, std::string(name) + ".row_ptr is NULL");
+  if (need_val && !M->val) return fail(c, SPG_ERR_INVALID_ARG, std::string(name) + ".val is NULL");
+  return SPG_OK;
+}
+
+// Fork `n` internal streams off `s`; kernels of different bins run concurrently.
+spg_status fork(spg_ctx *c, cudaStream_t s) {
+  SPG_CUDA(c, cudaEventRecord(c->ev_fork, s));
+  for (int k = 0; k < kSubStreams; ++k) SPG_CUDA(c, cudaStreamWaitEvent(c->sub[k], c->ev_fork, 0));
+  return SPG_OK;
+}
+
+spg_status join(spg_ctx *c, cudaStream_t s) {
+  for (int k = 0; k < kSubStreams; ++k) {
+    SPG_CUDA(c, cudaEventRecord(c->ev_join[k], c->sub[k]));
+    SPG_CUDA(c, cudaStreamWaitEvent(s, c->ev_join[k], 0));
+  }
+  return SPG_OK;
+}
+
+template <typename K>
+spg_status set_smem(spg_ctx *c, K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    SPG_CUDA(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return SPG_OK;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// a1 (+ a2 counts): per-row flop with a lane-group size matched to nnz/row.
+spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count_bins,
+                       cudaStream_t s) {
+  const int64_t m = A->nrows;
+  if (m == 0) return SPG_OK;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  int64_t *flop = (int64_t *)c->flop.p;
+  DevCSR a = dev(A);
+  // lane group size: host does not know nnz(A) without a read; use the
+  // caller-independent choice G = 8 (rows of R-MAT/ER/stencil average 8-30).
+  constexpr int G = 8;
+  const int64_t rows_per_block = 256 / G;
+  int64_t grid = std::min<int64_t>(ceil_div(m, rows_per_block), int64_t(c->num_sms) * 16);
+  {
+    ProfScope _ps(c, s, "k_flop_bin");
+    k_flop_bin<G><<<(unsigned)grid, 256, 0, s>>>(a, B->row_ptr, B->ncols, flop, info, count_bins);
+  }
+  SPG_LAUNCHED(c, "k_flop_bin");
+  return SPG_OK;
+}
+
+// scan of data[0..n) in place (int64), numeric-bin counting in the last pass
+spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s) {
+  if (n == 0) return SPG_OK;
+  const int64_t nb = ceil_div(n, kScanTile);
+  SPG_CUDA(c, cudaGetLastError());
+  spg_status st = buf_ensure(c, c->partial, size_t(nb) * 8, s);
+  if (st != SPG_OK) return st;
+  int64_t *partial = (int64_t *)c->partial.p;
+  {
+    ProfScope _ps(c, s, "k_scan_reduce");
+    k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial);
+  }
+  SPG_LAUNCHED(c, "k_scan_reduce");
+  {
+    ProfScope _ps(c, s, "k_scan_partials");
+    k_scan_partials<<<1, kScanThreads, 0, s>>>(partial, nb);
+  }
+  SPG_LAUNCHED(c, "k_scan_partials");
+  {
+    ProfScope _ps(c, s, "k_scan_down");
+    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p);
+  }
+  SPG_LAUNCHED(c, "k_scan_down");
+  return SPG_OK;
+}
+
+spg_status read_info(spg_ctx *c, cudaStream_t s) {
+  SPG_CUDA(c, cudaMemcpyAsync(c->host_info, c->info.p, sizeof(PlanInfo), cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  return SPG_OK;
+}
+
+int64_t bin_offset(const unsigned long long *cnt, int b) {
+  int64_t off = 0;
+  for (int u = 1; u < b; ++u) off += (int64_t)cnt[u];
+  return off;
+}
+
+constexpr size_t kSymBitmapMaxWords = (200 * 1024) / 4;  // ncols <= 1.6M -> smem bitmap
+
+}  // namespace
+
+// paper's symbolic table size per row (debug export; Fig:hash_spgemm P:302-305)
+__global__ void k_plan_tsize(const int64_t *f, int64_t m, int64_t ncols, int64_t *o) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) o[i] = int64_t(1) << sym_log2_paper(f[i], ncols);
+}
+
+// ============================================================================
+extern "C" {
+
+spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn, void *user) {
+  if (!out) return SPG_ERR_INVALID_ARG;
+  *out = nullptr;
+  if ((alloc == nullptr) != (free_fn == nullptr)) return SPG_ERR_INVALID_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return SPG_ERR_CUDA; }
+  spg_ctx *c = new spg_ctx();
+  c->device = dev;
+  c->alloc = alloc;
+  c->free_fn = free_fn;
+  c->user = user;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) c->num_sms = v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess)
+    c->smem_optin = (size_t)v;
+  bool ok = cudaMallocHost(&c->host_info, sizeof(PlanInfo)) == cudaSuccess;
+  for (int k = 0; ok && k < kSubStreams; ++k) {
+    ok = cudaStreamCreateWithFlags(&c->sub[k], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming) == cudaSuccess;
+  }
+  ok = ok && cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+  if (ok) {
+    const size_t s_num_w1024 = size_t(4) * 1024 * 12;
+    const size_t s_num_b = size_t(16384) * 12;
+    ok = set_smem(c, k_num_warp<1024, 4>, s_num_w1024) == SPG_OK &&
+         set_smem(c, k_num_block<512>, s_num_b) == SPG_OK &&
+         set_smem(c, k_num_block<1024>, s_num_b) == SPG_OK &&
+         set_smem(c, k_sym_block<512>, size_t(32768) * 4) == SPG_OK &&
+         set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
+         set_smem(c, k_sym_bitmap<1024>, kSymBitmapMaxWords * 4) == SPG_OK &&
+         set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
+  }
+  if (!ok) {
+    cudaGetLastError();
+    spg_ctx_destroy(c);
+    return SPG_ERR_CUDA;
+  }
+  *out = c;
+  return SPG_OK;
+}
+
+spg_status spg_ctx_destroy(spg_ctx *c) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  cudaDeviceSynchronize();
+  Buf *bufs[] = {&c->flop, &c->rows_sym, &c->rows_num, &c->partial, &c->slab, &c->info, &c->scratch};
+  for (Buf *b : bufs) buf_release(c, *b, nullptr);
+  if (c->host_info) cudaFreeHost(c->host_info);
+  for (int k = 0; k < kSubStreams; ++k) {
+    if (c->sub[k]) cudaStreamDestroy(c->sub[k]);
+    if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+  return SPG_OK;
+}
+
+const char *spg_last_error(const spg_ctx *c) { return c ? c->err.c_str() : "null ctx"; }
+
+int64_t spg_launch_count(const spg_ctx *c) { return c ? c->launches : -1; }
+
+spg_status spg_profile_enable(spg_ctx *c, int enable) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  c->profiling = enable ? 1 : 0;
+  return SPG_OK;
+}
+
+spg_status spg_profile_reset(spg_ctx *c) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  for (auto &r : c->recs) cudaEventSynchronize(r.b);
+  c->recs.clear();
+  c->ev_used = 0;
+  return SPG_OK;
+}
+
+int64_t spg_profile_count(spg_ctx *c) {
+  if (!c) return -1;
+  for (auto &r : c->recs) cudaEventSynchronize(r.b);
+  return (int64_t)c->recs.size();
+}
+
+spg_status spg_profile_record(spg_ctx *c, int64_t idx, const char **name, float *ms) {
+  if (!c || !name || !ms || idx < 0 || idx >= (int64_t)c->recs.size()) return SPG_ERR_INVALID_ARG;
+  const auto &r = c->recs[(size_t)idx];
+  SPG_CUDA(c, cudaEventSynchronize(r.b));
+  SPG_CUDA(c, cudaEventElapsedTime(ms, r.a, r.b));
+  *name = r.name;
+  return SPG_OK;
+}
+
+spg_status spg_get_info(const spg_ctx *c, spg_info *o) {
+  if (!c || !o) return SPG_ERR_INVALID_ARG;
+  if (!c->have_plan) return SPG_ERR_STATE;
+  std::memset(o, 0, sizeof(*o));
+  const PlanInfo &p = c->plan;
+  o->nrows = c->plan_m;
+  o->flop_total = (int64_t)p.flop_total;
+  o->nnz_total = (int64_t)p.nnz_total;
+  o->max_row_flop = (int64_t)p.max_flop;
+  o->max_row_nnz = (int64_t)p.max_nnz;
+  for (int b = 0; b < 12 && b < kMaxBins; ++b) {
+    o->sym_bin_rows[b] = (int64_t)p.sym_count[b];
+    o->num_bin_rows[b] = (int64_t)p.num_count[b];
+  }
+  o->sym_bin_rows[0] = c->plan_m;  // skip bin = the rest
+  o->num_bin_rows[0] = c->plan_m;
+  for (int b = 1; b < kMaxBins; ++b) {
+    o->sym_bin_rows[0] -= o->sym_bin_rows[b];
+    o->num_bin_rows[0] -= o->num_bin_rows[b];
+  }
+  return SPG_OK;
+}
+
+spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t *C_row_ptr,
+                        int64_t *nnz_C, int64_t *flop_total, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  c->have_plan = false;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", false)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", false)) != SPG_OK) return st;
+  if (A->ncols != B->nrows)
+    return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows (" + std::to_string(A->ncols) + " vs " +
+                                             std::to_string(B->nrows) + ")");
+  if (!C_row_ptr || !nnz_C) return fail(c, SPG_ERR_INVALID_ARG, "C_row_ptr / nnz_C is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  const int64_t m = A->nrows;
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->flop, size_t(std::max<int64_t>(m, 1)) * 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rows_sym, size_t(std::max<int64_t>(m, 1)) * 4, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rows_num, size_t(std::max<int64_t>(m, 1)) * 4, s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
+  SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, sizeof(int64_t), s));
+  if (m > 0 && (A->col_idx == nullptr || B->col_idx == nullptr) && B->nrows > 0)
+    return fail(c, SPG_ERR_INVALID_ARG, "col_idx is NULL");
+  int64_t *row_nnz = C_row_ptr + 1;
+  int64_t *flop = (int64_t *)c->flop.p;
+  if (m > 0 && B->nrows > 0) {
+    // a1 + a2: flop, symbolic bins
+    if ((st = launch_flop(c, A, B, 1, s)) != SPG_OK) return st;
+    {
+      ProfScope _ps(c, s, "k_bin_scatter_sym");
+      k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, B->ncols, 0, info,
+                                                               (int32_t *)c->rows_sym.p, row_nnz);
+    }
+    SPG_LAUNCHED(c, "k_bin_scatter(sym)");
+    if ((st = read_info(c, s)) != SPG_OK) return st;
+    PlanInfo h = *c->host_info;
+    if ((int64_t)h.max_brow > kMaxBRow)
+      return fail(c, SPG_ERR_OVERFLOW, "a row of B has more than 2^26 entries");
+    // a3: symbolic per bin, bins on concurrent internal streams
+    if ((st = fork(c, s)) != SPG_OK) return st;
+    DevCSR a = dev(A), b = dev(B);
+    const int32_t *rows = (const int32_t *)c->rows_sym.p;
+    int sidx = 0;
+    for (int bin = 1; bin < SB_COUNT; ++bin) {
+      const int64_t n = (int64_t)h.sym_count[bin];
+      if (n == 0) continue;
+      const int32_t *rb = rows + bin_offset(h.sym_count, bin);
+      cudaStream_t ss = c->sub[sidx++ % kSubStreams];
+      if (bin == SB_W128 || bin == SB_W1024) {
+        const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
+        if (bin == SB_W128)
+          {
+            ProfScope _ps(c, ss, "k_sym_warp<128>");
+            k_sym_warp<128, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 128 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
+          }
+        else
+          {
+            ProfScope _ps(c, ss, "k_sym_warp<1024>");
+            k_sym_warp<1024, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 1024 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
+          }
+        SPG_LAUNCHED(c, "k_sym_warp");
+      } else if (bin >= SB_B2K && bin <= SB_B32K) {
+        const int logT = 11 + (bin - SB_B2K);
+        const size_t smem = (size_t(1) << logT) * 4;
+        const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 8);
+        if (logT <= 13)
+          {
+            ProfScope _ps(c, ss, "k_sym_block<512>");
+            k_sym_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, flop, row_nnz);
+          }
+        else
+          {
+            ProfScope _ps(c, ss, "k_sym_block<1024>");
+            k_sym_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, row_nnz);
+          }
+        SPG_LAUNCHED(c, "k_sym_block");
+      } else {  // SB_G
+        const size_t nwords = size_t((B->ncols + 31) / 32);
+        if (nwords <= kSymBitmapMaxWords) {
+          const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
+          {
+            ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
+            k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(rb, n, a, b, row_nnz);
+          }
+          SPG_LAUNCHED(c, "k_sym_bitmap");
+        } else {
+          const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
+          int lg = 0;
+          {
+            const int64_t mn = std::min<int64_t>((int64_t)h.max_flop, B->ncols);
+            while ((int64_t(1) << lg) <= mn) ++lg;
+          }
+          const int64_t slabT = int64_t(1) << std::max(lg, kMinLogT);
+          if ((st = buf_ensure(c, c->slab, size_t(grid) * size_t(slabT) * 4, s)) != SPG_OK) return st;
+          {
+            ProfScope _ps(c, ss, "k_sym_global<1024>");
+            k_sym_global<1024><<<(unsigned)grid, 1024, 0, ss>>>(rb, n, a, b, flop, row_nnz,
+                                                                 (uint32_t *)c->slab.p, slabT);
+          }
+          SPG_LAUNCHED(c, "k_sym_global");
+        }
+      }
+    }
+    if ((st = join(c, s)) != SPG_OK) return st;
+  } else if (m > 0) {
+    SPG_CUDA(c, cudaMemsetAsync(row_nnz, 0, size_t(m) * 8, s));
+  }
+  // a4: C_row_ptr = exclusive scan of row nnz (+ numeric bin counts)
+  if ((st = launch_scan(c, row_nnz, m, s)) != SPG_OK) return st;
+  if (m > 0) {
+    {
+      ProfScope _ps(c, s, "k_bin_scatter_num");
+      k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, 0, 1, info,
+                                                               (int32_t *)c->rows_num.p, nullptr);
+    }
+    SPG_LAUNCHED(c, "k_bin_scatter(num)");
+  }
+  if ((st = read_info(c, s)) != SPG_OK) return st;
+  c->plan = *c->host_info;
+  *nnz_C = (int64_t)c->plan.nnz_total;
+  if (flop_total) *flop_total = (int64_t)c->plan.flop_total;
+  c->have_plan = true;
+  c->plan_a_rp = A->row_ptr;
+  c->plan_b_rp = B->row_ptr;
+  c->plan_c_rp = C_row_ptr;
+  c->plan_m = m;
+  c->plan_ncols = B->ncols;
+  return SPG_OK;
+}
+
+spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int64_t *C_row_ptr,
+                       int32_t *C_col_idx, double *C_val, int sorted, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", true)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", true)) != SPG_OK) return st;
+  if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
+  if (sorted != 0 && sorted != 1) return fail(c, SPG_ERR_INVALID_ARG, "sorted must be 0 or 1");
+  if (!c->have_plan || c->plan_a_rp != A->row_ptr || c->plan_b_rp != B->row_ptr ||
+      c->plan_c_rp != C_row_ptr || c->plan_m != A->nrows || c->plan_ncols != B->ncols)
+    return fail(c, SPG_ERR_STATE, "spg_numeric without a matching spg_symbolic");
+  const PlanInfo &h = c->plan;
+  if (h.nnz_total == 0) return SPG_OK;
+  if (!C_col_idx || !C_val) return fail(c, SPG_ERR_INVALID_ARG, "C_col_idx / C_val is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  DevCSR a = dev(A), b = dev(B);
+  const int32_t *rows = (const int32_t *)c->rows_num.p;
+  // G-tier slab: keys + vals of lowest 2^n >= 2 * max nnz(c_i) per block
+  int64_t g_grid = 0, slabT = 0;
+  if (h.num_count[NB_G]) {
+    g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
+    int lg = log2_ceil64(2 * h.max_nnz);
+    slabT = int64_t(1) << std::max(lg, kMinLogT);
+    if ((st = buf_ensure(c, c->slab, size_t(g_grid) * size_t(slabT) * 12, s)) != SPG_OK) return st;
+  }
+  if ((st = fork(c, s)) != SPG_OK) return st;
+  int sidx = 0;
+  // largest bins first so the long rows start early
+  for (int bin = NB_COUNT - 1; bin >= 1; --bin) {
+    const int64_t n = (int64_t)h.num_count[bin];
+    if (n == 0) continue;
+    const int32_t *rb = rows + bin_offset(h.num_count, bin);
+    cudaStream_t ss = c->sub[sidx++ % kSubStreams];
+    if (bin == NB_W256) {
+      const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
+      {
+        ProfScope _ps(c, ss, "k_num_warp<256>");
+        k_num_warp<256, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 12, ss>>>(
+            rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted);
+      }
+      SPG_LAUNCHED(c, "k_num_warp<256>");
+    } else if (bin == NB_W1024) {
+      const int64_t grid = std::min<int64_t>(ceil_div(n, 4), int64_t(c->num_sms) * 32);
+      {
+        ProfScope _ps(c, ss, "k_num_warp<1024>");
+        k_num_warp<1024, 4><<<(unsigned)grid, 4 * 32, 4 * 1024 * 12, ss>>>(
+            rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted);
+      }
+      SPG_LAUNCHED(c, "k_num_warp<1024>");
+    } else if (bin >= NB_B2K && bin <= NB_B16K) {
+      const int logT = 11 + (bin - NB_B2K);
+      const int tmax = 1 << logT;
+      const size_t smem = size_t(tmax) * 12;
+      const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 8);
+      if (logT <= 12)
+        {
+          ProfScope _ps(c, ss, "k_num_block<512>");
+          k_num_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted, tmax);
+        }
+      else
+        {
+          ProfScope _ps(c, ss, "k_num_block<1024>");
+          k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted, tmax);
+        }
+      SPG_LAUNCHED(c, "k_num_block");
+    } else {  // NB_G
+      uint32_t *sk = (uint32_t *)c->slab.p;
+      double *sv = (double *)((char *)c->slab.p + size_t(g_grid) * size_t(slabT) * 4);
+      {
+        ProfScope _ps(c, ss, "k_num_global<1024>");
+        k_num_global<1024><<<(unsigned)g_grid, 1024, sorted ? kRankSmem : 0, ss>>>(
+            rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted, sk, sv, slabT);
+      }
+      SPG_LAUNCHED(c, "k_num_global");
+    }
+  }
+  return join(c, s);
+}
+
+spg_status spg_plan_export(spg_ctx *c, int64_t *flop_out, int64_t *tsize_out, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  if (!c->have_plan) return fail(c, SPG_ERR_STATE, "no symbolic plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t m = c->plan_m;
+  if (m == 0) return SPG_OK;
+  if (flop_out)
+    SPG_CUDA(c, cudaMemcpyAsync(flop_out, c->flop.p, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
+  if (tsize_out) {
+    // table size of the paper's rule, computed on the device from the plan
+    {
+      ProfScope _ps(c, s, "k_plan_tsize");
+      k_plan_tsize<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>((const int64_t *)c->flop.p, m,
+                                                              c->plan_ncols, tsize_out);
+    }
+    SPG_LAUNCHED(c, "k_plan_tsize");
+  }
+  return SPG_OK;
+}
+
+spg_status spg_rows_to_parts(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t nparts,
+                             int64_t *offsets, int64_t *flop_total, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", false)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", false)) != SPG_OK) return st;
+  if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
+  if (nparts < 1 || !offsets) return fail(c, SPG_ERR_INVALID_ARG, "nparts < 1 or offsets NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  const int64_t m = A->nrows;
+  c->have_plan = false;  // the flop buffer is reused
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->flop, size_t(m + 1) * 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->scratch, size_t(m + 1 + nparts + 1) * 8, s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  int64_t *ps = (int64_t *)c->scratch.p;
+  int64_t *doff = ps + (m + 1);
+  SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
+  SPG_CUDA(c, cudaMemsetAsync(ps, 0, size_t(m + 1) * 8, s));
+  if (m > 0 && B->nrows > 0) {
+    if ((st = launch_flop(c, A, B, 0, s)) != SPG_OK) return st;
+    SPG_CUDA(c, cudaMemcpyAsync(ps + 1, c->flop.p, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
+    if ((st = launch_scan(c, ps + 1, m, s)) != SPG_OK) return st;  // ParallelPrefixSum
+  }
+  {
+    ProfScope _ps(c, s, "k_lowbnd");
+    k_lowbnd<<<(unsigned)ceil_div(nparts + 1, 256), 256, 0, s>>>(ps, m, nparts, doff);
+  }
+  SPG_LAUNCHED(c, "k_lowbnd");
+  SPG_CUDA(c, cudaMemcpyAsync(offsets, doff, size_t(nparts + 1) * 8, cudaMemcpyDeviceToHost, s));
+  if (flop_total) SPG_CUDA(c, cudaMemcpyAsync(flop_total, ps + m, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  return SPG_OK;
+}
+
+spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t g_row_begin,
+                        int64_t *sum, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, C, "C", true)) != SPG_OK) return st;
+  if ((st = check_csr(c, G, "G", false)) != SPG_OK) return st;
+  if (!sum || g_row_begin < 0 || g_row_begin + C->nrows > G->nrows)
+    return fail(c, SPG_ERR_INVALID_ARG, "bad mask row range or NULL sum");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  SPG_CUDA(c, cudaMemsetAsync(&info->mask_sum, 0, 8, s));
+  if (C->nrows > 0) {
+    const int64_t grid = std::min<int64_t>(ceil_div(C->nrows, 8), int64_t(c->num_sms) * 16);
+    {
+      ProfScope _ps(c, s, "k_mask_sum");
+      k_mask_sum<<<(unsigned)grid, 256, 0, s>>>(dev(C), dev(G), g_row_begin, info);
+    }
+    SPG_LAUNCHED(c, "k_mask_sum");
+  }
+  unsigned long long h = 0;
+  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_sum, &info->mask_sum, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  h = c->host_info->mask_sum;
+  *sum = (int64_t)h;
+  return SPG_OK;
+}
+
+spg_status spg_validate(spg_ctx *c, const spg_csr *M, int check_sorted, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, M, "M", false)) != SPG_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  SPG_CUDA(c, cudaMemsetAsync(&info->flags, 0, 8, s));
+  if (M->nrows > 0) {
+    const int64_t grid = std::min<int64_t>(ceil_div(M->nrows, 8), int64_t(c->num_sms) * 16);
+    {
+      ProfScope _ps(c, s, "k_validate");
+      k_validate<<<(unsigned)grid, 256, 0, s>>>(dev(M), check_sorted, &info->flags);
+    }
+    SPG_LAUNCHED(c, "k_validate");
+  }
+  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->flags, &info->flags, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  const unsigned long long f = c->host_info->flags;
+  if (f & 1) return fail(c, SPG_ERR_INVALID_ARG, "row_ptr is not nondecreasing");
+  if (f & 2) return fail(c, SPG_ERR_INDEX_RANGE, "column index outside [0, ncols)");
+  if (f & 4) return fail(c, SPG_ERR_INVALID_ARG, "a row is not strictly increasing");
+  return SPG_OK;
+}
+
+}  // extern "C"
+

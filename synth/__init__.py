@@ -280,3 +280,37 @@ def workload(name: str, scale: int | None = None):
         G = symmetrise_pattern(R, drop_diagonal=True)
         return tril_strict(G), triu_strict(G), {"G": G}
     raise KeyError(name)
+
+
+def crafted_rows(specs, ncols: int, seed: int, shuffle: bool = False):
+    """(A, B) whose row i of A*B has exactly flop = specs[i][0] products and
+    nnz = specs[i][1] distinct columns (0 <= nnz <= min(flop, ncols); flop > 0
+    needs nnz > 0).  Row i of A selects fresh rows of B: q = flop // nnz copies
+    of one column set S (|S| = nnz) and one row holding the first flop % nnz
+    columns of S.  Used to hit every bin boundary of the GPU path; the values
+    are U[0.5, 1.5)."""
+    rng = np.random.default_rng(seed)
+    a_rows, a_cols, b_rows, b_cols = [], [], [], []
+    nb = 0
+    for i, (f, n) in enumerate(specs):
+        if f == 0:
+            continue
+        assert 0 < n <= min(f, ncols)
+        S = rng.choice(ncols, size=n, replace=False).astype(np.int64)
+        q, rem = divmod(f, n)
+        lens = [n] * q + ([rem] if rem else [])
+        for L in lens:
+            a_rows.append(i)
+            a_cols.append(nb)
+            b_rows.append(np.full(L, nb, np.int64))
+            b_cols.append(S[:L])
+            nb += 1
+    m = len(specs)
+    A = from_coo(m, nb, np.array(a_rows, np.int64), np.array(a_cols, np.int64))
+    B = from_coo(nb, ncols, np.concatenate(b_rows) if b_rows else np.zeros(0, np.int64),
+                 np.concatenate(b_cols) if b_cols else np.zeros(0, np.int64))
+    A = with_values(A, seed + 1, 0.5, 1.5)
+    B = with_values(B, seed + 2, 0.5, 1.5)
+    if shuffle:
+        A, B = shuffle_within_rows(A, seed + 3), shuffle_within_rows(B, seed + 4)
+    return A, B

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on the same
+seeded inputs.  Every test here needs a B200 (marker `gpu`)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import compare, compare_rows, gpu_vs_oracle, sampled_rows
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_01698_b200 as m
+    from paper_1804_01698_b200 import build
+    build.build()
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(spg):
+    return spg.Context()
+
+
+# ------------------------------------------------------------------ small
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_worked_example(spg, ctx, sorted_out):
+    A = synth.CSR(2, 2, np.array([0, 1, 3], np.int64), np.array([0, 0, 1], np.int32),
+                  np.array([1.0, 2.0, 3.0]))
+    B = synth.CSR(2, 2, np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32),
+                  np.array([4.0, 5.0]))
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="2x2")
+
+
+@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_random_shapes(spg, ctx, seed, sorted_out):
+    rng = np.random.default_rng(seed)
+    m, n, k = (int(x) for x in rng.integers(1, 300, size=3))
+    A = synth.random_sparse(m, n, float(rng.uniform(0.001, 0.1)), seed, 0.0, 1.0, empty_rows=0.2)
+    B = synth.random_sparse(n, k, float(rng.uniform(0.001, 0.1)), seed + 50, 0.0, 1.0,
+                            empty_rows=0.1)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what=f"random{seed}")
+
+
+def test_empty_and_degenerate(spg, ctx):
+    for (m, n, k) in [(0, 5, 7), (5, 0, 7), (5, 7, 0), (1, 1, 1)]:
+        A = synth.random_sparse(m, n, 0.5, 1)
+        B = synth.random_sparse(n, k, 0.5, 2)
+        gpu_vs_oracle(A, B, True, ctx=ctx, what=f"{m}x{n}x{k}")
+    Z = synth.CSR(6, 4, np.zeros(7, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    gpu_vs_oracle(Z, synth.random_sparse(4, 9, 0.5, 3), True, ctx=ctx, what="nnz(A)=0")
+
+
+def test_dimension_mismatch(spg, ctx):
+    A = spg.DeviceCSR.from_host(synth.random_sparse(4, 5, 0.5, 1))
+    with pytest.raises(ValueError):
+        spg.spgemm(A, A, ctx=ctx)
+    from paper_1804_01698_b200 import _lib
+    rp = torch.zeros(5, dtype=torch.int64, device="cuda")
+    with pytest.raises(_lib.SpgError, match="DIM_MISMATCH"):
+        _lib.spg_symbolic(ctx.handle, A.c(), A.c(), rp.data_ptr(), 0)
+
+
+def test_numeric_without_symbolic_is_state_error(spg):
+    from paper_1804_01698_b200 import _lib
+    c2 = spg.Context()
+    A = spg.DeviceCSR.from_host(synth.random_sparse(4, 4, 0.5, 1))
+    rp = torch.zeros(5, dtype=torch.int64, device="cuda")
+    with pytest.raises(_lib.SpgError, match="STATE"):
+        _lib.spg_numeric(c2.handle, A.c(), A.c(), rp.data_ptr(), 0, 0, True, 0)
+
+
+def test_identity_bitexact(spg, ctx):
+    A = synth.er_poisson(2000, 8.0, 5)
+    I = synth.identity(2000)
+    for X, Y in ((A, I), (I, A)):
+        C = spg.spgemm(spg.DeviceCSR.from_host(X), spg.DeviceCSR.from_host(Y), True, ctx)
+        rp, col, val = C.to_host()
+        assert (rp == A.row_ptr).all() and (col == A.col).all() and (val == A.val).all()
+
+
+def test_unsorted_input_order(spg, ctx):
+    A, B, _ = synth.workload("c3_rmat20", scale=11)
+    As, Bs = synth.shuffle_within_rows(A, 1), synth.shuffle_within_rows(B, 2)
+    for so in (True, False):
+        gpu_vs_oracle(As, Bs, so, ctx=ctx, what="shuffled input")
+
+
+# ------------------------------------------------------------------ bins
+def _boundary_specs():
+    specs = [(0, 0)]
+    for T in [128, 1024, 2048, 4096, 8192, 16384, 32768, 65536]:
+        for f in (T - 1, T, T + 1):
+            specs.append((f, 37))          # symbolic-bin boundaries, low nnz
+    for h in [16, 128, 512, 1024, 2048, 4096, 8192, 16384]:
+        for n in (h - 1, h, h + 1):
+            specs.append((n, n))           # numeric-bin boundaries, CR = 1
+            specs.append((3 * n + 1, n))   # same nnz, CR ~ 3
+    specs += [(200000, 60000), (50000, 50000), (1, 1), (2, 1), (33, 33)]
+    return specs
+
+
+@pytest.mark.parametrize("sorted_out", [True, False])
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_bin_boundaries(spg, ctx, sorted_out, shuffle):
+    A, B = synth.crafted_rows(_boundary_specs(), 1 << 17, 11, shuffle=shuffle)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="bin boundaries")
+
+
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_wide_columns_global_tables(spg, ctx, sorted_out):
+    """ncols > the smem bitmap limit: global-hash symbolic, multi-chunk rank sort."""
+    specs = [(70000, 30000), (40000, 20000), (100, 100), (3000, 1000)]
+    A, B = synth.crafted_rows(specs, 3_000_000, 12)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="wide ncols")
+
+
+@pytest.mark.parametrize("ncols", [1, 2, 16])
+def test_small_ncols_cap(spg, ctx, ncols):
+    """min(N_col, flop) cap of the table size: large flop, tiny ncols."""
+    specs = [(5000, ncols), (40000, ncols), (7, min(7, ncols)), (100000, ncols)]
+    A, B = synth.crafted_rows(specs, ncols, 13)
+    gpu_vs_oracle(A, B, True, ctx=ctx, what=f"ncols={ncols}")
+
+
+def test_dense_output_rows(spg, ctx):
+    A = synth.random_sparse(40, 60, 0.9, 3, 0.5, 1.5)
+    B = synth.random_sparse(60, 700, 0.5, 4, 0.5, 1.5)
+    for so in (True, False):
+        gpu_vs_oracle(A, B, so, ctx=ctx, what="dense rows")
+
+
+# ------------------------------------------------------------------ plan
+def test_plan_flop_and_table_size(spg, ctx):
+    A, B = synth.crafted_rows(_boundary_specs(), 1 << 17, 21)
+    dA, dB = spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B)
+    rp, nnz, flop_tot = spg.spg_symbolic(dA, dB, ctx)
+    f, t = spg.plan_export(ctx, A.nrows)
+    of, otot = oracle.flop(A, B)
+    assert flop_tot == otot
+    assert (f.cpu().numpy() == of).all()
+    ot = np.array([oracle.table_size(x, B.ncols) for x in of])
+    assert (t.cpu().numpy() == ot).all()
+    assert (np.diff(rp.cpu().numpy()) == oracle.row_nnz(A, B)).all()
+    info = ctx.info()
+    assert info["nnz_total"] == nnz and info["flop_total"] == otot
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8, 64])
+def test_rows_to_parts(spg, ctx, nparts):
+    A, B, _ = synth.workload("c3_rmat20", scale=12)
+    offs, tot = spg.rows_to_parts(spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B),
+                                  nparts, ctx)
+    of, otot = oracle.flop(A, B)
+    assert tot == otot
+    assert offs == oracle.rows_to_threads(of, nparts).tolist()
+
+
+# ------------------------------------------------------------------ configs
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_c1_er_full(spg, ctx, sorted_out):
+    A, B, _ = synth.workload("c1_er4096")
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="C1")
+
+
+@pytest.mark.parametrize("g", [8, 33])
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_c2_stencil_small(spg, ctx, g, sorted_out):
+    A, B, _ = synth.workload("c2_stencil64", scale=g)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what=f"C2 g={g}")
+
+
+@pytest.mark.parametrize("scale", [10, 14])
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_c3_rmat_small(spg, ctx, scale, sorted_out):
+    A, B, _ = synth.workload("c3_rmat20", scale=scale)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what=f"C3 s{scale}")
+
+
+def test_c4_tallskinny_small(spg, ctx):
+    A, B, _ = synth.workload("c4_tallskinny", scale=14)
+    gpu_vs_oracle(A, B, False, ctx=ctx, what="C4 s14")
+
+
+@pytest.mark.parametrize("scale", [10, 14])
+def test_c5_triangles_small(spg, ctx, scale):
+    L, U, ex = synth.workload("c5_triangle", scale=scale)
+    G = ex["G"]
+    gpu_vs_oracle(L, U, True, ctx=ctx, what=f"C5 s{scale} L*U")
+    want = oracle.triangle_count(L, U, G)
+    dL, dU, dG = (spg.DeviceCSR.from_host(x) for x in (L, U, G))
+    for so in (False, True):
+        assert spg.triangle_count(dL, dU, dG, sorted=so, ctx=ctx) == want
+    # force several row blocks (streaming path)
+    assert spg.triangle_count(dL, dU, dG, block_entries=max(1, L.nnz // 3), ctx=ctx) == want
+
+
+def test_triangles_complete_graph(spg, ctx):
+    n = 60
+    G = synth.complete_graph(n)
+    L, U = synth.tril_strict(G), synth.triu_strict(G)
+    dL, dU, dG = (spg.DeviceCSR.from_host(x) for x in (L, U, G))
+    assert spg.triangle_count(dL, dU, dG, ctx=ctx) == n * (n - 1) * (n - 2) // 6
+
+
+def test_validate(spg, ctx):
+    from paper_1804_01698_b200 import _lib
+    A = synth.random_sparse(50, 40, 0.2, 1)
+    spg.validate(spg.DeviceCSR.from_host(A), True, ctx)
+    bad = synth.CSR(A.nrows, A.ncols, A.row_ptr, A.col.copy(), A.val)
+    bad.col[3] = 45
+    with pytest.raises(_lib.SpgError, match="INDEX_RANGE"):
+        spg.validate(spg.DeviceCSR.from_host(bad), False, ctx)
+    S = synth.shuffle_within_rows(synth.random_sparse(50, 40, 0.5, 2), 3)
+    spg.validate(spg.DeviceCSR.from_host(S), False, ctx)
+    with pytest.raises(_lib.SpgError):
+        spg.validate(spg.DeviceCSR.from_host(S), True, ctx)
+
+
+def test_sorted_equals_sorted_unsorted(spg, ctx):
+    A, B, _ = synth.workload("c3_rmat20", scale=13)
+    dA = spg.DeviceCSR.from_host(A)
+    Cs = spg.spgemm(dA, dA, True, ctx)
+    Cu = spg.spgemm(dA, dA, False, ctx)
+    rs, cs, vs = Cs.to_host()
+    ru, cu, vu = Cu.to_host()
+    compare(ru, cu, vu, rs, cs, vs, False, "sorted vs unsorted")
+
+
+def test_row_range_view(spg, ctx):
+    A, B, _ = synth.workload("c3_rmat20", scale=12)
+    dA = spg.DeviceCSR.from_host(A)
+    r0, r1 = 777, 2900
+    C = spg.spgemm(dA.rows(r0, r1), dA, True, ctx)
+    g = C.to_host()
+    o = oracle.spgemm(A, B, r0, r1)
+    compare(*g, *o, True, "row view")
+
+
+# ------------------------------------------------------------------ full size
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_c2_full_size(spg, ctx, sorted_out):
+    """BASELINE config 2 at full size, whole product vs the oracle."""
+    A, B, _ = synth.workload("c2_stencil64")
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="C2 full")
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled(spg, ctx):
+    """BASELINE config 3 at full size (C = 116 GB): sampled rows (heaviest +
+    random) vs the oracle, and the row-sum identity over all rows."""
+    A, B, _ = synth.workload("c3_rmat20")
+    dA = spg.DeviceCSR.from_host(A)
+    free, _ = torch.cuda.mem_get_info()
+    of, otot = oracle.flop(A, B)
+    for so in (False, True):
+        C = spg.spgemm(dA, dA, so, ctx)
+        assert ctx.info()["flop_total"] == otot
+        rows = sampled_rows(A, B, of, nsample=150, seed=3, top=8)
+        compare_rows(C, A, B, rows, so, what=f"C3 full sorted={so}")
+        # row sums: C*1 vs A*(B*1) computed on the host from A, B (fp64)
+        rp = C.row_ptr
+        rs = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
+        rows_idx = torch.repeat_interleave(torch.arange(A.nrows, device="cuda"), rp.diff())
+        rs.index_add_(0, rows_idx, C.val)
+        bsum = np.bincount(np.repeat(np.arange(B.nrows), np.diff(B.row_ptr)), weights=B.val,
+                           minlength=B.nrows)
+        ref = np.bincount(np.repeat(np.arange(A.nrows), np.diff(A.row_ptr)),
+                          weights=A.val * bsum[A.col], minlength=A.nrows)
+        np.testing.assert_allclose(rs.cpu().numpy(), ref, rtol=1e-11, atol=1e-300)
+        del C, rs, rows_idx
+        torch.cuda.empty_cache()
