@@ -115,6 +115,7 @@ __device__ __forceinline__ void block_bitonic(uint32_t *keys, double *vals, int 
 template <int TMAX, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restrict__ rows,
                                                          int64_t nrows, DevCSR A, DevCSR B,
+                                                         const int64_t *__restrict__ flop,
                                                          const int64_t *__restrict__ c_rp,
                                                          int32_t *__restrict__ c_col,
                                                          double *__restrict__ c_val,
@@ -132,16 +133,25 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
     const int T = 1 << logT;
     for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
     __syncwarp();
-    for_row_products(A, B, A.rp[i], A.rp[i + 1], 0, 1, [&](bool act, uint32_t c, double v) {
-      uint32_t slot = 0;
-      if (act) slot = num_probe(keys, c, logT);
-      const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
-      if (act) {
-        if (__popc(grp) == 1) vals[slot] += v;   // c_ij <- c_ij + value (l.8)
-        else atomicAdd(vals + slot, v);
-      }
-      __syncwarp();
-    });
+    const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    if (use_seq(flop[i], ae - as)) {
+      // keys of a round are distinct: plain read-modify-write of the value
+      for_row_seq<true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
+        if (act) vals[num_probe(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
+        __syncwarp();
+      });
+    } else {
+      for_row_products(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
+        uint32_t slot = 0;
+        if (act) slot = num_probe(keys, c, logT);
+        const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
+        if (act) {
+          if (__popc(grp) == 1) vals[slot] += v;   // c_ij <- c_ij + value (l.8)
+          else atomicAdd(vals + slot, v);
+        }
+        __syncwarp();
+      });
+    }
     if (!sorted) {
       int base = 0;
       for (int s0 = 0; s0 < T; s0 += 32) {
@@ -216,6 +226,7 @@ __device__ __forceinline__ void block_emit_unsorted(const uint32_t *keys, const 
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict__ rows,
                                                        int64_t nrows, DevCSR A, DevCSR B,
+                                                       const int64_t *__restrict__ flop,
                                                        const int64_t *__restrict__ c_rp,
                                                        int32_t *__restrict__ c_col,
                                                        double *__restrict__ c_val, int sorted,
@@ -235,9 +246,14 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
     for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
-    for_row_products(A, B, A.rp[i], A.rp[i + 1], w, NW, [&](bool act, uint32_t c, double v) {
-      if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
-    });
+    {
+      const int64_t as = A.rp[i], ae = A.rp[i + 1];
+      auto acc = [&](bool act, uint32_t c, double v) {
+        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
+      };
+      if (use_seq(flop[i], ae - as)) for_row_seq<true>(A, B, as, ae, w, NW, acc);
+      else for_row_products(A, B, as, ae, w, NW, acc);
+    }
     __syncthreads();
     block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
     if (sorted) {
@@ -275,6 +291,7 @@ constexpr size_t kRankSmem = size_t(kRankWords) * 4 + size_t(kRankWords) * 2 +
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restrict__ rows,
                                                         int64_t nrows, DevCSR A, DevCSR B,
+                                                        const int64_t *__restrict__ flop,
                                                         const int64_t *__restrict__ c_rp,
                                                         int32_t *__restrict__ c_col,
                                                         double *__restrict__ c_val, int sorted,
@@ -300,9 +317,14 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
     for (int64_t s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
     if (threadIdx.x == 0) { s_cnt = 0; s_chunk_base = 0; }
     __syncthreads();
-    for_row_products(A, B, A.rp[i], A.rp[i + 1], w, NW, [&](bool act, uint32_t c, double v) {
-      if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
-    });
+    {
+      const int64_t as = A.rp[i], ae = A.rp[i + 1];
+      auto acc = [&](bool act, uint32_t c, double v) {
+        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
+      };
+      if (use_seq(flop[i], ae - as)) for_row_seq<true>(A, B, as, ae, w, NW, acc);
+      else for_row_products(A, B, as, ae, w, NW, acc);
+    }
     __syncthreads();
     if (!sorted) {
       block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);

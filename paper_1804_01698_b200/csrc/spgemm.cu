@@ -488,8 +488,8 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
                        int32_t *C_col_idx, double *C_val, int sorted, void *stream) {
   if (!c) return SPG_ERR_INVALID_ARG;
   spg_status st;
-  if ((st = check_csr(c, A, "A", true)) != SPG_OK) return st;
-  if ((st = check_csr(c, B, "B", true)) != SPG_OK) return st;
+  if ((st = check_csr(c, A, "A", false)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", false)) != SPG_OK) return st;
   if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
   if (sorted != 0 && sorted != 1) return fail(c, SPG_ERR_INVALID_ARG, "sorted must be 0 or 1");
   if (!c->have_plan || c->plan_a_rp != A->row_ptr || c->plan_b_rp != B->row_ptr ||
@@ -498,10 +498,12 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   const PlanInfo &h = c->plan;
   if (h.nnz_total == 0) return SPG_OK;
   if (!C_col_idx || !C_val) return fail(c, SPG_ERR_INVALID_ARG, "C_col_idx / C_val is NULL");
+  if (!A->val || !B->val) return fail(c, SPG_ERR_INVALID_ARG, "A.val / B.val is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   SPG_CUDA(c, cudaSetDevice(c->device));
   DevCSR a = dev(A), b = dev(B);
   const int32_t *rows = (const int32_t *)c->rows_num.p;
+  const int64_t *flop = (const int64_t *)c->flop.p;
   // G-tier slab: keys + vals of lowest 2^n >= 2 * max nnz(c_i) per block
   int64_t g_grid = 0, slabT = 0;
   if (h.num_count[NB_G]) {
@@ -523,7 +525,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       {
         ProfScope _ps(c, ss, "k_num_warp<256>");
         k_num_warp<256, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 12, ss>>>(
-            rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted);
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted);
       }
       SPG_LAUNCHED(c, "k_num_warp<256>");
     } else if (bin == NB_W1024) {
@@ -531,7 +533,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       {
         ProfScope _ps(c, ss, "k_num_warp<1024>");
         k_num_warp<1024, 4><<<(unsigned)grid, 4 * 32, 4 * 1024 * 12, ss>>>(
-            rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted);
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted);
       }
       SPG_LAUNCHED(c, "k_num_warp<1024>");
     } else if (bin >= NB_B2K && bin <= NB_B16K) {
@@ -542,12 +544,12 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       if (logT <= 12)
         {
           ProfScope _ps(c, ss, "k_num_block<512>");
-          k_num_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted, tmax);
+          k_num_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
         }
       else
         {
           ProfScope _ps(c, ss, "k_num_block<1024>");
-          k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted, tmax);
+          k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
         }
       SPG_LAUNCHED(c, "k_num_block");
     } else {  // NB_G
@@ -556,7 +558,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       {
         ProfScope _ps(c, ss, "k_num_global<1024>");
         k_num_global<1024><<<(unsigned)g_grid, 1024, sorted ? kRankSmem : 0, ss>>>(
-            rb, n, a, b, C_row_ptr, C_col_idx, C_val, sorted, sk, sv, slabT);
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, sk, sv, slabT);
       }
       SPG_LAUNCHED(c, "k_num_global");
     }

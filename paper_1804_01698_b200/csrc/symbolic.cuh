@@ -62,6 +62,81 @@ __device__ __forceinline__ void for_row_cols(const DevCSR &A, const DevCSR &B, i
   }
 }
 
+// Sequential enumeration: the warp walks the a_ik of its chunks one at a time
+// and a round is up to 32 consecutive b_kj of ONE B row, so the keys of a
+// round are distinct (CSR rows hold unique columns).  The gathers of round
+// r+1 are issued before round r is hashed (software prefetch).  Calls
+// f(active, col, a_ik * b_kj) with all 32 lanes; kVal = false skips values.
+template <bool kVal, typename F>
+__device__ __forceinline__ void for_row_seq(const DevCSR &A, const DevCSR &B, int64_t as,
+                                            int64_t ae, int64_t c0, int64_t cstride, F &&f) {
+  const int lane = lane_id();
+  for (int64_t cb = as + c0 * 32; cb < ae; cb += cstride * 32) {
+    const int64_t e = cb + lane;
+    int len = 0;
+    int64_t bs = 0;
+    double a = 0.0;
+    if (e < ae) {
+      const int k = __ldg(A.col + e);
+      if (kVal) a = __ldg(A.val + e);
+      bs = __ldg(B.rp + k);
+      len = (int)(__ldg(B.rp + k + 1) - bs);
+    }
+    unsigned pend = __ballot_sync(kFull, len > 0);  // entries with a nonempty B row
+    if (!pend) continue;
+    int j = __ffs(pend) - 1;
+    pend &= pend - 1;
+    int64_t jbs = shfl_i64(bs, j);
+    int jlen = __shfl_sync(kFull, len, j);
+    double ja = kVal ? shfl_f64(a, j) : 0.0;
+    int t = 0;
+    bool act = lane < jlen;
+    uint32_t c = act ? (uint32_t)__ldg(B.col + jbs + lane) : 0u;
+    double bv = (kVal && act) ? __ldg(B.val + jbs + lane) : 0.0;
+    while (true) {
+      // next round descriptor (warp-uniform)
+      int nt = t + 32;
+      int64_t nbs = jbs;
+      int nlen = jlen;
+      double na = ja;
+      bool have = true;
+      if (nt >= jlen) {
+        if (pend) {
+          const int nj = __ffs(pend) - 1;
+          pend &= pend - 1;
+          nbs = shfl_i64(bs, nj);
+          nlen = __shfl_sync(kFull, len, nj);
+          if (kVal) na = shfl_f64(a, nj);
+          nt = 0;
+        } else {
+          have = false;
+        }
+      }
+      bool nact = false;
+      uint32_t nc = 0u;
+      double nbv = 0.0;
+      if (have) {
+        nact = nt + lane < nlen;
+        if (nact) {
+          nc = (uint32_t)__ldg(B.col + nbs + nt + lane);
+          if (kVal) nbv = __ldg(B.val + nbs + nt + lane);
+        }
+      }
+      f(act, c, ja * bv);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+      if (!have) break;
+      t = nt; jbs = nbs; jlen = nlen; ja = na; act = nact; c = nc; bv = nbv;
+    }
+  }
+}
+
+// Rows whose B rows average >= kSeqMinLen entries use the sequential
+// enumeration (no owner search, distinct keys per round); shorter ones the
+// flattened one (full 32-lane rounds).
+constexpr int kSeqMinLen = 16;
+__device__ __forceinline__ bool use_seq(int64_t flop, int64_t nnz_a) {
+  return flop >= int64_t(kSeqMinLen) * nnz_a;
+}
+
 // ---------------------------------------------------------------------------
 // W tier: one warp per row, warp-private table of T <= TMAX slots in smem.
 // ---------------------------------------------------------------------------
@@ -80,8 +155,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     for (int s = lane; s < T; s += 32) tab[s] = kEmpty;
     __syncwarp();
     int cnt = 0;
-    for_row_cols(A, B, A.rp[i], A.rp[i + 1], 0, 1,
-                 [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
+    const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    if (use_seq(flop[i], ae - as))
+      for_row_seq<false>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double) {
+        if (act) cnt += sym_insert(tab, c, logT);
+      });
+    else
+      for_row_cols(A, B, as, ae, 0, 1, [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
     cnt = warp_sum(cnt);
     if (lane == 0) row_nnz[i] = cnt;
     __syncwarp();
@@ -110,8 +190,13 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     int cnt = 0;
-    for_row_cols(A, B, A.rp[i], A.rp[i + 1], w, NW,
-                 [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
+    const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    if (use_seq(flop[i], ae - as))
+      for_row_seq<false>(A, B, as, ae, w, NW, [&](bool act, uint32_t c, double) {
+        if (act) cnt += sym_insert(tab, c, logT);
+      });
+    else
+      for_row_cols(A, B, as, ae, w, NW, [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();

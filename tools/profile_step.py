@@ -1,0 +1,27 @@
+"""Minimal driver for ncu: a few C = A*B calls on one workload (no oracle)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_1804_01698_b200 as spg  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2_stencil64")
+ap.add_argument("--scale", type=int, default=None)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--sorted", type=int, default=1)
+a = ap.parse_args()
+A, B, _ = synth.workload(a.config, a.scale)
+dA = spg.DeviceCSR.from_host(A)
+dB = dA if B is A else spg.DeviceCSR.from_host(B)
+ctx = spg.Context()
+for _ in range(a.reps):
+    C = spg.spgemm(dA, dB, sorted=bool(a.sorted), ctx=ctx)
+    torch.cuda.synchronize()
+    del C
+print("ok", ctx.info()["nnz_total"], ctx.launches)
