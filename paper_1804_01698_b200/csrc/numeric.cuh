@@ -107,7 +107,8 @@ __device__ __forceinline__ void block_bitonic(uint32_t *keys, double *vals, int 
 }
 
 // ---------------------------------------------------------------------------
-// W tier: one warp per row, warp-private keys[TMAX] + vals[TMAX] in smem.
+// W tier: one warp per row, warp-private keys[TMAX] + vals[TMAX] (+ cnt[TMAX]
+// bucket counters for the sort) in smem.
 // Distinct keys of one round go to distinct slots, so the value add is a
 // plain read-modify-write; lanes that share a key in a round (found with
 // __match_any_sync) use the atomic add.  Rounds are separated by __syncwarp.
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *vals = s_dyn_f64 + w * TMAX;
   uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + w * TMAX;
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + WARPS * TMAX + w * TMAX;
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int64_t r = int64_t(blockIdx.x) * WARPS + w; r < nrows; r += int64_t(gridDim.x) * WARPS) {
     const int i = rows[r];
@@ -166,7 +168,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
         base += __popc(bal);
       }
     } else {
-      // compact occupied slots to the front (destination <= source), in order
+      // a7: ascending columns by a bucket (counting) sort.  Buckets
+      // are monotone in the column: b(c) = (c - min) >> sh, T buckets for
+      // nnz <= T/2 keys; each key's position = bucket offset + its rank
+      // among the (few) keys of its bucket.
+      // 1. compact occupied slots to the front (destination <= source)
       int base = 0;
       for (int s0 = 0; s0 < T; s0 += 32) {
         const uint32_t k = keys[s0 + lane];
@@ -182,14 +188,49 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
         base += __popc(bal);
         __syncwarp();
       }
-      int P = 1;
-      while (P < nnz) P <<= 1;
-      for (int s = nnz + lane; s < P; s += 32) keys[s] = kEmpty;
+      // 2. key range and bucket shift
+      unsigned mn = 0xFFFFFFFFu, mx = 0u;
+      for (int e = lane; e < nnz; e += 32) {
+        const unsigned k = keys[e];
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+      }
+      mn = __reduce_min_sync(kFull, mn);
+      mx = __reduce_max_sync(kFull, mx);
+      int sh = log2_ceil64(uint64_t(mx - mn) + 1) - logT;
+      sh = sh < 0 ? 0 : sh;
+      for (int b = lane; b < T; b += 32) cnt[b] = 0u;
       __syncwarp();
-      warp_bitonic(keys, vals, P);
-      for (int s = lane; s < nnz; s += 32) {
-        c_col[rp0 + s] = (int32_t)keys[s];
-        c_val[rp0 + s] = vals[s];
+      uint32_t *loc = reinterpret_cast<uint32_t *>(vals + (T >> 1));  // free half
+      uint32_t *grp = keys + (T >> 1);                                  // free half
+      for (int e = lane; e < nnz; e += 32) loc[e] = atomicAdd(cnt + ((keys[e] - mn) >> sh), 1u);
+      __syncwarp();
+      // 3. exclusive scan of the bucket counts (lane owns T/32 consecutive)
+      const int per = T >> 5;
+      int run = 0;
+      for (int q = 0; q < per; ++q) run += (int)cnt[lane * per + q];
+      int ex = warp_incl_scan(run) - run;
+      for (int q = 0; q < per; ++q) {
+        const int v = (int)cnt[lane * per + q];
+        cnt[lane * per + q] = (uint32_t)ex;
+        ex += v;
+      }
+      __syncwarp();
+      // 4. group keys by bucket, 5. rank inside the bucket and store
+      for (int e = lane; e < nnz; e += 32) {
+        const uint32_t k = keys[e];
+        grp[cnt[(k - mn) >> sh] + loc[e]] = k;
+      }
+      __syncwarp();
+      for (int e = lane; e < nnz; e += 32) {
+        const uint32_t k = keys[e];
+        const uint32_t b = (k - mn) >> sh;
+        const int lo = (int)cnt[b];
+        const int hi = (int)b + 1 < T ? (int)cnt[b + 1] : nnz;
+        int rnk = 0;
+        for (int q = lo; q < hi; ++q) rnk += grp[q] < k;
+        c_col[rp0 + lo + rnk] = (int32_t)k;
+        c_val[rp0 + lo + rnk] = vals[e];
       }
     }
     __syncwarp();

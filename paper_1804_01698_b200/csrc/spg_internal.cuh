@@ -47,18 +47,26 @@ struct PlanInfo {
 };
 
 __host__ __device__ __forceinline__ int log2_ceil64(uint64_t x) {  // smallest n: 2^n >= x
+#ifdef __CUDA_ARCH__
+  return x <= 1 ? 0 : 64 - __clzll((long long)(x - 1));
+#else
   int n = 0;
   while ((uint64_t(1) << n) < x) ++n;
   return n;
+#endif
 }
 
 // log2 of the paper's symbolic table size: lowest 2^n STRICTLY greater than
 // min(flop, ncols)  (Fig:hash_spgemm l.10-12).
 __host__ __device__ __forceinline__ int sym_log2_paper(int64_t flop, int64_t ncols) {
-  int64_t s = flop < ncols ? flop : ncols;
+  const int64_t s = flop < ncols ? flop : ncols;
+#ifdef __CUDA_ARCH__
+  return s <= 0 ? 0 : 64 - __clzll((long long)s);  // bits of s = lowest n: 2^n > s
+#else
   int n = 0;
   while ((int64_t(1) << n) <= s) ++n;
   return n;
+#endif
 }
 
 __device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {

@@ -263,7 +263,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
   }
   ok = ok && cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
   if (ok) {
-    const size_t s_num_w1024 = size_t(4) * 1024 * 12;
+    const size_t s_num_w1024 = size_t(4) * 1024 * 16;
     const size_t s_num_b = size_t(16384) * 12;
     ok = set_smem(c, k_num_warp<1024, 4>, s_num_w1024) == SPG_OK &&
          set_smem(c, k_num_block<512>, s_num_b) == SPG_OK &&
@@ -375,8 +375,6 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   PlanInfo *info = (PlanInfo *)c->info.p;
   SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
   SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, sizeof(int64_t), s));
-  if (m > 0 && (A->col_idx == nullptr || B->col_idx == nullptr) && B->nrows > 0)
-    return fail(c, SPG_ERR_INVALID_ARG, "col_idx is NULL");
   int64_t *row_nnz = C_row_ptr + 1;
   int64_t *flop = (int64_t *)c->flop.p;
   if (m > 0 && B->nrows > 0) {
@@ -524,7 +522,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
       {
         ProfScope _ps(c, ss, "k_num_warp<256>");
-        k_num_warp<256, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 12, ss>>>(
+        k_num_warp<256, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 16, ss>>>(
             rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted);
       }
       SPG_LAUNCHED(c, "k_num_warp<256>");
@@ -532,7 +530,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       const int64_t grid = std::min<int64_t>(ceil_div(n, 4), int64_t(c->num_sms) * 32);
       {
         ProfScope _ps(c, ss, "k_num_warp<1024>");
-        k_num_warp<1024, 4><<<(unsigned)grid, 4 * 32, 4 * 1024 * 12, ss>>>(
+        k_num_warp<1024, 4><<<(unsigned)grid, 4 * 32, 4 * 1024 * 16, ss>>>(
             rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted);
       }
       SPG_LAUNCHED(c, "k_num_warp<1024>");

@@ -64,8 +64,7 @@ __device__ __forceinline__ void for_row_cols(const DevCSR &A, const DevCSR &B, i
 
 // Sequential enumeration: the warp walks the a_ik of its chunks one at a time
 // and a round is up to 32 consecutive b_kj of ONE B row, so the keys of a
-// round are distinct (CSR rows hold unique columns).  The gathers of round
-// r+1 are issued before round r is hashed (software prefetch).  Calls
+// round are distinct (CSR rows hold unique columns).  Calls
 // f(active, col, a_ik * b_kj) with all 32 lanes; kVal = false skips values.
 template <bool kVal, typename F>
 __device__ __forceinline__ void for_row_seq(const DevCSR &A, const DevCSR &B, int64_t as,
@@ -83,48 +82,24 @@ __device__ __forceinline__ void for_row_seq(const DevCSR &A, const DevCSR &B, in
       len = (int)(__ldg(B.rp + k + 1) - bs);
     }
     unsigned pend = __ballot_sync(kFull, len > 0);  // entries with a nonempty B row
-    if (!pend) continue;
-    int j = __ffs(pend) - 1;
-    pend &= pend - 1;
-    int64_t jbs = shfl_i64(bs, j);
-    int jlen = __shfl_sync(kFull, len, j);
-    double ja = kVal ? shfl_f64(a, j) : 0.0;
-    int t = 0;
-    bool act = lane < jlen;
-    uint32_t c = act ? (uint32_t)__ldg(B.col + jbs + lane) : 0u;
-    double bv = (kVal && act) ? __ldg(B.val + jbs + lane) : 0.0;
-    while (true) {
-      // next round descriptor (warp-uniform)
-      int nt = t + 32;
-      int64_t nbs = jbs;
-      int nlen = jlen;
-      double na = ja;
-      bool have = true;
-      if (nt >= jlen) {
-        if (pend) {
-          const int nj = __ffs(pend) - 1;
-          pend &= pend - 1;
-          nbs = shfl_i64(bs, nj);
-          nlen = __shfl_sync(kFull, len, nj);
-          if (kVal) na = shfl_f64(a, nj);
-          nt = 0;
-        } else {
-          have = false;
+    while (pend) {
+      const int j = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int64_t jbs = shfl_i64(bs, j);
+      const int L = __shfl_sync(kFull, len, j);
+      const double aj = kVal ? shfl_f64(a, j) : 0.0;
+      const int32_t *bc = B.col + jbs;
+      const double *bv = kVal ? B.val + jbs : nullptr;
+      for (int t = 0; t < L; t += 32) {
+        const bool act = t + lane < L;
+        uint32_t c = 0u;
+        double v = 0.0;
+        if (act) {
+          c = (uint32_t)__ldg(bc + t + lane);
+          if (kVal) v = aj * __ldg(bv + t + lane);  // value <- a_ik * b_kj (l.5)
         }
+        f(act, c, v);
       }
-      bool nact = false;
-      uint32_t nc = 0u;
-      double nbv = 0.0;
-      if (have) {
-        nact = nt + lane < nlen;
-        if (nact) {
-          nc = (uint32_t)__ldg(B.col + nbs + nt + lane);
-          if (kVal) nbv = __ldg(B.val + nbs + nt + lane);
-        }
-      }
-      f(act, c, ja * bv);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
-      if (!have) break;
-      t = nt; jbs = nbs; jlen = nlen; ja = na; act = nact; c = nc; bv = nbv;
     }
   }
 }
