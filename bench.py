@@ -325,7 +325,8 @@ def run_ours(args):
             ev[i][0].record(s)
             out = step(sorted_out)
             ev[i][1].record(s)
-            last = out
+            if i == k - 1:
+                last = out                       # keep only the final C (no 2nd allocation)
             del out
         torch.cuda.synchronize()
         if world > 1:
@@ -340,10 +341,12 @@ def run_ours(args):
         tot = torch.tensor([float(np.sum(ms))], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        log(f"[rank {rank}] sorted={sorted_out} step ms: {[round(x, 3) for x in ms]}")
         return float(tot.item()) / k, launches, recs, last
 
     clocks = ClockSampler(local)
-    clocks.start()
+    if not os.environ.get("SPG_BENCH_NO_CLOCKS"):
+        clocks.start()
     for _ in range(args.warmup):
         step(True)
         step(False)
