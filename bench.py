@@ -325,8 +325,8 @@ def run_ours(args):
             ev[i][0].record(s)
             out = step(sorted_out)
             ev[i][1].record(s)
-            if i == k - 1:
-                last = out                       # keep only the final C (no 2nd allocation)
+            if i == k - 1 and out is not None and not isinstance(out, int):
+                last = out.row_ptr               # keep only the final row_ptr (C can be >100 GB)
             del out
         torch.cuda.synchronize()
         if world > 1:
@@ -378,7 +378,7 @@ def run_ours(args):
         # per-row flop from the library's plan (last symbolic = last sorted step)
         spg.spg_symbolic(Aloc, dB, ctx)
         f_row = spg.plan_export(ctx, r1 - r0)[0].cpu().numpy()
-        c_nnz = np.diff(Cs.row_ptr.cpu().numpy()) if Cs is not None else np.zeros(r1 - r0, np.int64)
+        c_nnz = np.diff(Cs.cpu().numpy()) if Cs is not None else np.zeros(r1 - r0, np.int64)
         byts = kernel_bytes(top, a_nnz, f_row, c_nnz, r1 - r0, int(a_nnz.sum()), dB.ncols, dB.nrows)
         launches_per_step = cnt / args.steps
         if byts is not None:
@@ -397,7 +397,7 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = oracle_sample(A, B, target_s=args.cpu_seconds)
-        nnzC = int(Cs.row_ptr[-1].item()) if (Cs is not None and not tri) else None
+        nnzC = int(Cs[-1].item()) if (Cs is not None and not tri) else None
         mb = None
         if nnzC is not None:
             mb = (8 * (A.nrows + 1) + 12 * A.nnz + 8 * (B.nrows + 1) + 12 * flop_total

@@ -24,48 +24,6 @@ __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int lo
   }
 }
 
-// Enumerate products of A row [as, ae) (chunks c0, c0+cstride, ... of 32
-// a_ik) and call f(active, col, a_ik * b_kj) once per lane per round; all 32
-// lanes call f (inactive lanes with active = false) so f may use warp
-// collectives.
-template <typename F>
-__device__ __forceinline__ void for_row_products(const DevCSR &A, const DevCSR &B, int64_t as,
-                                                 int64_t ae, int64_t c0, int64_t cstride,
-                                                 F &&f) {
-  const int lane = lane_id();
-  for (int64_t cb = as + c0 * 32; cb < ae; cb += cstride * 32) {
-    const int64_t e = cb + lane;
-    int len = 0;
-    int64_t bs = 0;
-    double a = 0.0;
-    if (e < ae) {
-      const int k = __ldg(A.col + e);
-      a = __ldg(A.val + e);
-      bs = __ldg(B.rp + k);
-      len = (int)(__ldg(B.rp + k + 1) - bs);
-    }
-    const int incl = warp_incl_scan(len);
-    const int excl = incl - len;
-    const int total = __shfl_sync(kFull, incl, 31);
-    for (int p0 = 0; p0 < total; p0 += 32) {
-      const int p = p0 + lane;
-      const int own = owner_lane(incl, p);
-      const int64_t obs = shfl_i64(bs, own);
-      const int oex = __shfl_sync(kFull, excl, own);
-      const double oa = shfl_f64(a, own);
-      uint32_t c = 0;
-      double v = 0.0;
-      const bool act = p < total;
-      if (act) {
-        const int64_t q = obs + (p - oex);
-        c = (uint32_t)__ldg(B.col + q);
-        v = oa * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
-      }
-      f(act, c, v);
-    }
-  }
-}
-
 // Warp-cooperative bitonic sort of P (power of two) (key, val) pairs in smem.
 __device__ __forceinline__ void warp_bitonic(uint32_t *keys, double *vals, int P) {
   const int lane = lane_id();
@@ -138,12 +96,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     if (use_seq(flop[i], ae - as)) {
       // keys of a round are distinct: plain read-modify-write of the value
-      for_row_seq<true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
+      for_row<true, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         if (act) vals[num_probe(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
         __syncwarp();
       });
     } else {
-      for_row_products(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
+      for_row<false, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         uint32_t slot = 0;
         if (act) slot = num_probe(keys, c, logT);
         const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
@@ -292,8 +250,8 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
       auto acc = [&](bool act, uint32_t c, double v) {
         if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
       };
-      if (use_seq(flop[i], ae - as)) for_row_seq<true>(A, B, as, ae, w, NW, acc);
-      else for_row_products(A, B, as, ae, w, NW, acc);
+      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc);
     }
     __syncthreads();
     block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
@@ -363,8 +321,8 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
       auto acc = [&](bool act, uint32_t c, double v) {
         if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
       };
-      if (use_seq(flop[i], ae - as)) for_row_seq<true>(A, B, as, ae, w, NW, acc);
-      else for_row_products(A, B, as, ae, w, NW, acc);
+      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc);
     }
     __syncthreads();
     if (!sorted) {

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -42,6 +43,7 @@ struct spg_ctx {
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[kSubStreams] = {};
   int64_t launches = 0;
+  int serial = 0;  // SPG_SERIAL_BINS=1: all bins on the caller's stream (diagnosis)
   // optional per-launch timing (events on the stream each kernel runs on)
   int profiling = 0;
   struct Rec { const char *name; cudaEvent_t a, b; };
@@ -252,6 +254,10 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
   c->alloc = alloc;
   c->free_fn = free_fn;
   c->user = user;
+  {
+    const char *e = getenv("SPG_SERIAL_BINS");
+    c->serial = (e && e[0] == '1') ? 1 : 0;
+  }
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) c->num_sms = v;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess)
@@ -399,7 +405,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       const int64_t n = (int64_t)h.sym_count[bin];
       if (n == 0) continue;
       const int32_t *rb = rows + bin_offset(h.sym_count, bin);
-      cudaStream_t ss = c->sub[sidx++ % kSubStreams];
+      cudaStream_t ss = c->serial ? s : c->sub[sidx++ % kSubStreams];
       if (bin == SB_W128 || bin == SB_W1024) {
         const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
         if (bin == SB_W128)
@@ -517,7 +523,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
     const int64_t n = (int64_t)h.num_count[bin];
     if (n == 0) continue;
     const int32_t *rb = rows + bin_offset(h.num_count, bin);
-    cudaStream_t ss = c->sub[sidx++ % kSubStreams];
+    cudaStream_t ss = c->serial ? s : c->sub[sidx++ % kSubStreams];
     if (bin == NB_W256) {
       const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
       {

@@ -34,43 +34,25 @@ __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
   return (atomicOr(bm + (c >> 5), bit) & bit) ? 0 : 1;
 }
 
-// Enumerate the products of A row [as, ae) in chunks of 32 a_ik assigned to
-// this warp (chunk c0, c0+cstride, ...) and call f(col) for each b_kj.
-template <typename F>
-__device__ __forceinline__ void for_row_cols(const DevCSR &A, const DevCSR &B, int64_t as,
-                                             int64_t ae, int64_t c0, int64_t cstride, F &&f) {
+// ---------------------------------------------------------------------------
+// Product enumeration.  The products of row i are cut into ROUNDS of <= 32
+// products; the NW warps of the row's owner (one warp in the W tier, a block
+// in the B/G tiers) take rounds round-robin (round g goes to warp g % NW), so
+// a row with few a_ik but long B rows still keeps every warp busy.  f(active,
+// col, a_ik * b_kj) is called by all 32 lanes of a warp once per round.
+//
+//  - sequential rounds (kSeq): a round is <= 32 consecutive b_kj of ONE B row,
+//    so the keys of a round are distinct (CSR rows hold unique columns);
+//  - flattened rounds: 32 consecutive products of the row's product list,
+//    whatever the B-row lengths (full lanes for short B rows).
+// kVal = false skips the values (symbolic phase).
+// ---------------------------------------------------------------------------
+template <bool kSeq, bool kVal, typename F>
+__device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_t as,
+                                        int64_t ae, int w, int NW, F &&f) {
   const int lane = lane_id();
-  for (int64_t cb = as + c0 * 32; cb < ae; cb += cstride * 32) {
-    const int64_t e = cb + lane;
-    int len = 0;
-    int64_t bs = 0;
-    if (e < ae) {
-      const int k = __ldg(A.col + e);
-      bs = __ldg(B.rp + k);
-      len = (int)(__ldg(B.rp + k + 1) - bs);
-    }
-    const int incl = warp_incl_scan(len);
-    const int excl = incl - len;
-    const int total = __shfl_sync(kFull, incl, 31);
-    for (int p0 = 0; p0 < total; p0 += 32) {
-      const int p = p0 + lane;
-      const int own = owner_lane(incl, p);
-      const int64_t obs = shfl_i64(bs, own);
-      const int oex = __shfl_sync(kFull, excl, own);
-      if (p < total) f((uint32_t)__ldg(B.col + obs + (p - oex)));
-    }
-  }
-}
-
-// Sequential enumeration: the warp walks the a_ik of its chunks one at a time
-// and a round is up to 32 consecutive b_kj of ONE B row, so the keys of a
-// round are distinct (CSR rows hold unique columns).  Calls
-// f(active, col, a_ik * b_kj) with all 32 lanes; kVal = false skips values.
-template <bool kVal, typename F>
-__device__ __forceinline__ void for_row_seq(const DevCSR &A, const DevCSR &B, int64_t as,
-                                            int64_t ae, int64_t c0, int64_t cstride, F &&f) {
-  const int lane = lane_id();
-  for (int64_t cb = as + c0 * 32; cb < ae; cb += cstride * 32) {
+  int64_t gbase = 0;  // rounds of the previous chunks
+  for (int64_t cb = as; cb < ae; cb += 32) {
     const int64_t e = cb + lane;
     int len = 0;
     int64_t bs = 0;
@@ -81,26 +63,60 @@ __device__ __forceinline__ void for_row_seq(const DevCSR &A, const DevCSR &B, in
       bs = __ldg(B.rp + k);
       len = (int)(__ldg(B.rp + k + 1) - bs);
     }
-    unsigned pend = __ballot_sync(kFull, len > 0);  // entries with a nonempty B row
-    while (pend) {
-      const int j = __ffs(pend) - 1;
-      pend &= pend - 1;
-      const int64_t jbs = shfl_i64(bs, j);
-      const int L = __shfl_sync(kFull, len, j);
-      const double aj = kVal ? shfl_f64(a, j) : 0.0;
-      const int32_t *bc = B.col + jbs;
-      const double *bv = kVal ? B.val + jbs : nullptr;
-      for (int t = 0; t < L; t += 32) {
-        const bool act = t + lane < L;
-        uint32_t c = 0u;
-        double v = 0.0;
-        if (act) {
-          c = (uint32_t)__ldg(bc + t + lane);
-          if (kVal) v = aj * __ldg(bv + t + lane);  // value <- a_ik * b_kj (l.5)
+    if (kSeq && NW == 1) {
+      // one warp owns the row: walk the nonempty entries directly
+      unsigned pend = __ballot_sync(kFull, len > 0);
+      while (pend) {
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const int64_t jbs = shfl_i64(bs, j);
+        const int L = __shfl_sync(kFull, len, j);
+        const double aj = kVal ? shfl_f64(a, j) : 0.0;
+        for (int t = 0; t < L; t += 32) {
+          const bool act = t + lane < L;
+          uint32_t c = 0u;
+          double v = 0.0;
+          if (act) {
+            c = (uint32_t)__ldg(B.col + jbs + t + lane);
+            if (kVal) v = aj * __ldg(B.val + jbs + t + lane);  // value <- a_ik*b_kj (l.5)
+          }
+          f(act, c, v);
         }
-        f(act, c, v);
       }
+      continue;
     }
+    const int r = kSeq ? ((len + 31) >> 5) : len;  // rounds (seq) or products per entry
+    const int incl = warp_incl_scan(r);
+    const int excl = incl - r;
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int nr = kSeq ? total : ((total + 31) >> 5);
+    int g = (int)((w - gbase % NW + NW) % NW);
+    for (; g < nr; g += NW) {
+      int64_t q;
+      double oa = 0.0;
+      bool act;
+      if (kSeq) {
+        const int own = owner_lane(incl, g);
+        const int t = (g - __shfl_sync(kFull, excl, own)) * 32 + lane;
+        q = shfl_i64(bs, own) + t;
+        act = t < __shfl_sync(kFull, len, own);
+        if (kVal) oa = shfl_f64(a, own);
+      } else {
+        const int p = g * 32 + lane;
+        const int own = owner_lane(incl, p);
+        q = shfl_i64(bs, own) + (p - __shfl_sync(kFull, excl, own));
+        act = p < total;
+        if (kVal) oa = shfl_f64(a, own);
+      }
+      uint32_t c = 0u;
+      double v = 0.0;
+      if (act) {
+        c = (uint32_t)__ldg(B.col + q);
+        if (kVal) v = oa * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+      }
+      f(act, c, v);
+    }
+    gbase += nr;
   }
 }
 
@@ -131,12 +147,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     __syncwarp();
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
-    if (use_seq(flop[i], ae - as))
-      for_row_seq<false>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double) {
-        if (act) cnt += sym_insert(tab, c, logT);
-      });
-    else
-      for_row_cols(A, B, as, ae, 0, 1, [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
+    auto ins = [&](bool act, uint32_t c, double) {
+      if (act) cnt += sym_insert(tab, c, logT);
+    };
+    if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, 0, 1, ins);
+    else for_row<false, false>(A, B, as, ae, 0, 1, ins);
     cnt = warp_sum(cnt);
     if (lane == 0) row_nnz[i] = cnt;
     __syncwarp();
@@ -166,12 +181,11 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
     __syncthreads();
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
-    if (use_seq(flop[i], ae - as))
-      for_row_seq<false>(A, B, as, ae, w, NW, [&](bool act, uint32_t c, double) {
-        if (act) cnt += sym_insert(tab, c, logT);
-      });
-    else
-      for_row_cols(A, B, as, ae, w, NW, [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
+    auto ins = [&](bool act, uint32_t c, double) {
+      if (act) cnt += sym_insert(tab, c, logT);
+    };
+    if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
+    else for_row<false, false>(A, B, as, ae, w, NW, ins);
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
@@ -199,8 +213,9 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     int cnt = 0;
-    for_row_cols(A, B, A.rp[i], A.rp[i + 1], w, NW,
-                 [&](uint32_t c) { cnt += sym_bitmap_insert(bm, c); });
+    for_row<false, false>(A, B, A.rp[i], A.rp[i + 1], w, NW, [&](bool act, uint32_t c, double) {
+      if (act) cnt += sym_bitmap_insert(bm, c);
+    });
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
@@ -231,8 +246,14 @@ __global__ void __launch_bounds__(THREADS) k_sym_global(const int32_t *__restric
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     int cnt = 0;
-    for_row_cols(A, B, A.rp[i], A.rp[i + 1], w, NW,
-                 [&](uint32_t c) { cnt += sym_insert(tab, c, logT); });
+    {
+      const int64_t as = A.rp[i], ae = A.rp[i + 1];
+      auto ins = [&](bool act, uint32_t c, double) {
+        if (act) cnt += sym_insert(tab, c, logT);
+      };
+      if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
+      else for_row<false, false>(A, B, as, ae, w, NW, ins);
+    }
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();

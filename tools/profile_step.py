@@ -15,13 +15,22 @@ ap.add_argument("--config", default="c2_stencil64")
 ap.add_argument("--scale", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--sorted", type=int, default=1)
+ap.add_argument("--records", action="store_true")
 a = ap.parse_args()
 A, B, _ = synth.workload(a.config, a.scale)
 dA = spg.DeviceCSR.from_host(A)
 dB = dA if B is A else spg.DeviceCSR.from_host(B)
 ctx = spg.Context()
+from paper_1804_01698_b200 import _lib  # noqa: E402
 for _ in range(a.reps):
+    if a.records:
+        _lib.spg_profile_reset(ctx.handle)
+        _lib.spg_profile_enable(ctx.handle, True)
     C = spg.spgemm(dA, dB, sorted=bool(a.sorted), ctx=ctx)
     torch.cuda.synchronize()
+    if a.records:
+        _lib.spg_profile_enable(ctx.handle, False)
+        print([(n, round(t, 3)) for n, t in _lib.spg_profile_records(ctx.handle)], flush=True)
+        print(ctx.info(), flush=True)
     del C
 print("ok", ctx.info()["nnz_total"], ctx.launches)
