@@ -117,6 +117,9 @@ def bin_of_rows_num(nnz_c: np.ndarray) -> np.ndarray:
 
 
 def bin_of_rows_sym(flop: np.ndarray, ncols: int) -> np.ndarray:
+    """Symbolic bin of each row (library rule: T = max(32, lowest 2^n >
+    min(flop, ncols)); W128 / W1024 / B2K..B8K; above: BM bitmap when ncols <=
+    1.6M, else B16K / B32K / G).  Accounting only."""
     s = np.minimum(flop, ncols)
     lg = np.zeros(len(flop), np.int64)
     nz = flop > 0
@@ -125,18 +128,23 @@ def bin_of_rows_sym(flop: np.ndarray, ncols: int) -> np.ndarray:
     b = np.zeros(len(flop), np.int64)
     b[nz & (lg <= 7)] = 1
     b[nz & (lg > 7) & (lg <= 10)] = 2
-    mid = nz & (lg >= 11) & (lg <= 15)
+    mid = nz & (lg >= 11) & (lg <= 13)
     b[mid] = 3 + (lg[mid] - 11)
-    b[nz & (lg > 15)] = 8
+    big = nz & (lg >= 14)
+    if ncols <= 200 * 1024 * 8:
+        b[big] = 9
+    else:
+        b[big & (lg <= 15)] = 3 + (lg[big & (lg <= 15)] - 11)
+        b[big & (lg > 15)] = 8
     return b
 
 
 NUM_KERNEL_BIN = {"k_num_warp<256>": [1], "k_num_warp<1024>": [2],
                   "k_num_block<512>": [3, 4], "k_num_block<1024>": [5, 6],
-                  "k_num_global<1024>": [7]}
+                  "k_num_global<1024>": [7], "k_num_part<1024>": [7]}
 SYM_KERNEL_BIN = {"k_sym_warp<128>": [1], "k_sym_warp<1024>": [2],
                   "k_sym_block<512>": [3, 4, 5], "k_sym_block<1024>": [6, 7],
-                  "k_sym_bitmap<1024>": [8], "k_sym_global<1024>": [8]}
+                  "k_sym_bitmap<1024>": [9], "k_sym_global<1024>": [8]}
 
 
 def kernel_bytes(name: str, a_nnz_row, flop_row, c_nnz_row, m, nnzA, ncols, krows):

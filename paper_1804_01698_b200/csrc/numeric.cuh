@@ -287,6 +287,68 @@ constexpr int kRankGroups = kRankWords / kRankGroup;
 constexpr size_t kRankSmem = size_t(kRankWords) * 4 + size_t(kRankWords) * 2 +
                              size_t(kRankGroups) * 4;
 
+// Sorted emit by bitmap rank (block-wide): the keys of table [0, T) that lie
+// in [cbase, cbase + nbits) (nbits <= 32 * words of bm) are written to
+// out_col/out_val at out_base + (number of smaller keys in the range).
+// Returns the number of such keys (same value in every thread).
+__device__ __forceinline__ int block_rank_emit(const uint32_t *keys, const double *vals,
+                                               int64_t T, int64_t cbase, int64_t nbits,
+                                               uint32_t *bm, uint16_t *wpre, int *gpre,
+                                               int *s_tot, int64_t out_base,
+                                               int32_t *__restrict__ c_col,
+                                               double *__restrict__ c_val) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int nwords = (int)((nbits + 31) >> 5);
+  for (int s = threadIdx.x; s < nwords; s += blockDim.x) bm[s] = 0u;
+  __syncthreads();
+  for (int64_t s = threadIdx.x; s < T; s += blockDim.x) {
+    const uint32_t k = keys[s];
+    if (k != kEmpty && int64_t(k) >= cbase && int64_t(k) - cbase < nbits) {
+      const uint32_t off = (uint32_t)(int64_t(k) - cbase);
+      atomicOr(bm + (off >> 5), 1u << (off & 31u));
+    }
+  }
+  __syncthreads();
+  const int ngroups = (nwords + kRankGroup - 1) / kRankGroup;
+  for (int g = w; g < ngroups; g += NW) {  // u16 prefix inside each 64-word group
+    const int w0 = g * kRankGroup + 2 * lane;
+    const int c0 = w0 < nwords ? __popc(bm[w0]) : 0;
+    const int c1 = w0 + 1 < nwords ? __popc(bm[w0 + 1]) : 0;
+    const int incl = warp_incl_scan(c0 + c1);
+    const int ex = incl - c0 - c1;
+    if (w0 < nwords) wpre[w0] = (uint16_t)ex;
+    if (w0 + 1 < nwords) wpre[w0 + 1] = (uint16_t)(ex + c0);
+    if (lane == 31) gpre[g] = incl;
+  }
+  __syncthreads();
+  if (w == 0) {  // exclusive scan of the group totals
+    int carry = 0;
+    for (int g0 = 0; g0 < ngroups; g0 += 32) {
+      const int g = g0 + lane;
+      const int v = g < ngroups ? gpre[g] : 0;
+      const int incl = warp_incl_scan(v);
+      if (g < ngroups) gpre[g] = carry + incl - v;
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) *s_tot = carry;
+  }
+  __syncthreads();
+  for (int64_t s = threadIdx.x; s < T; s += blockDim.x) {
+    const uint32_t k = keys[s];
+    if (k != kEmpty && int64_t(k) >= cbase && int64_t(k) - cbase < nbits) {
+      const uint32_t off = (uint32_t)(int64_t(k) - cbase);
+      const uint32_t wd = off >> 5;
+      const int pos = gpre[wd / kRankGroup] + wpre[wd] +
+                      __popc(bm[wd] & ((1u << (off & 31u)) - 1u));
+      c_col[out_base + pos] = (int32_t)k;
+      c_val[out_base + pos] = vals[s];
+    }
+  }
+  const int tot = *s_tot;
+  __syncthreads();
+  return tot;
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restrict__ rows,
                                                         int64_t nrows, DevCSR A, DevCSR B,
@@ -299,9 +361,8 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
                                                         int64_t slabT) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt;
-  __shared__ long long s_chunk_base;
   constexpr int NW = THREADS / 32;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
   uint32_t *keys = slab_keys + int64_t(blockIdx.x) * slabT;
   double *vals = slab_vals + int64_t(blockIdx.x) * slabT;
   uint32_t *bm = s_dyn_u32;                                          // [kRankWords]
@@ -314,7 +375,7 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
     const int logT = num_log2(nnz);
     const int64_t T = int64_t(1) << logT;
     for (int64_t s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
-    if (threadIdx.x == 0) { s_cnt = 0; s_chunk_base = 0; }
+    if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
@@ -328,62 +389,132 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
     if (!sorted) {
       block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
     } else {
+      int64_t done = 0;
       for (int64_t cbase = 0; cbase < B.ncols; cbase += kRankBits) {
         const int64_t nbits = (B.ncols - cbase) < kRankBits ? (B.ncols - cbase) : kRankBits;
-        const int nwords = (int)((nbits + 31) >> 5);
-        for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;
-        __syncthreads();
-        for (int64_t s = threadIdx.x; s < T; s += THREADS) {
-          const uint32_t k = keys[s];
-          if (k != kEmpty && int64_t(k) >= cbase && int64_t(k) - cbase < nbits) {
-            const uint32_t off = (uint32_t)(int64_t(k) - cbase);
-            atomicOr(bm + (off >> 5), 1u << (off & 31u));
-          }
-        }
-        __syncthreads();
-        // per-group prefix: warp handles groups g = w, w + NW, ...; 2 words/lane
-        const int ngroups = (nwords + kRankGroup - 1) / kRankGroup;
-        for (int g = w; g < ngroups; g += NW) {
-          const int w0 = g * kRankGroup + 2 * lane;
-          const int c0 = w0 < nwords ? __popc(bm[w0]) : 0;
-          const int c1 = w0 + 1 < nwords ? __popc(bm[w0 + 1]) : 0;
-          const int incl = warp_incl_scan(c0 + c1);
-          const int ex = incl - c0 - c1;
-          if (w0 < nwords) wpre[w0] = (uint16_t)ex;
-          if (w0 + 1 < nwords) wpre[w0 + 1] = (uint16_t)(ex + c0);
-          if (lane == 31) gpre[g] = incl;
-        }
-        __syncthreads();
-        if (w == 0) {  // exclusive scan of group totals
-          int carry = 0;
-          for (int g0 = 0; g0 < ngroups; g0 += 32) {
-            const int g = g0 + lane;
-            const int v = g < ngroups ? gpre[g] : 0;
-            const int incl = warp_incl_scan(v);
-            if (g < ngroups) gpre[g] = carry + incl - v;
-            carry += __shfl_sync(kFull, incl, 31);
-          }
-          if (lane == 0) s_cnt = carry;  // set bits in this chunk
-        }
-        __syncthreads();
-        const long long cb = s_chunk_base;
-        for (int64_t s = threadIdx.x; s < T; s += THREADS) {
-          const uint32_t k = keys[s];
-          if (k != kEmpty && int64_t(k) >= cbase && int64_t(k) - cbase < nbits) {
-            const uint32_t off = (uint32_t)(int64_t(k) - cbase);
-            const uint32_t wd = off >> 5;
-            const int pos = gpre[wd / kRankGroup] + wpre[wd] +
-                            __popc(bm[wd] & ((1u << (off & 31u)) - 1u));
-            c_col[rp0 + cb + pos] = (int32_t)k;
-            c_val[rp0 + cb + pos] = vals[s];
-          }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_chunk_base += s_cnt;
-        __syncthreads();
+        done += block_rank_emit(keys, vals, T, cbase, nbits, bm, wpre, gpre, &s_cnt, rp0 + done,
+                                c_col, c_val);
       }
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// G tier, column-range parts (B rows sorted, parts from the BM symbolic): one
+// block per row at a time (dynamic row queue), the row's parts in column
+// order.  For part [lo, hi) every a_ik's B row contributes the segment of
+// columns in [lo, hi): it starts where the previous part's segment ended and
+// ends at the first column >= hi (galloping search).  The part's <= kPartKeys
+// keys are accumulated in an smem hash table of kPartT slots and emitted at
+// C_row_ptr[i] + (keys of the row before lo) -- in order, by a bitmap rank
+// over [lo, lo + kPartWidth), when sorted.  No global atomics.
+// ---------------------------------------------------------------------------
+constexpr int kPartT = 2 * kPartKeys;               // table slots (load <= 1/2)
+constexpr int kSegSmem = 2048;                      // a_ik with smem segment cursors
+constexpr int kPartRankWords = int(kPartWidth / 32);
+constexpr size_t kPartSmem = size_t(kPartT) * 12 + size_t(kSegSmem) * 8 +
+                             size_t(kPartRankWords) * 6 +
+                             size_t(kPartRankWords / kRankGroup) * 4;
+
+// first q in [s, len) with col[q] >= hi (col sorted), searching from s
+__device__ __forceinline__ int gallop_lb(const int32_t *__restrict__ col, int s, int len,
+                                         int64_t hi) {
+  if (s >= len || int64_t(__ldg(col + s)) >= hi) return s;
+  int lo = s, step = 1;  // invariant: col[lo] < hi
+  while (lo + step < len && int64_t(__ldg(col + lo + step)) < hi) {
+    lo += step;
+    step <<= 1;
+  }
+  int a = lo + 1, b = min(lo + step, len);
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (int64_t(__ldg(col + m)) < hi) a = m + 1; else b = m;
+  }
+  return a;
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_num_part(
+    const int32_t *__restrict__ rows, int64_t nrows, DevCSR A, DevCSR B,
+    const int64_t *__restrict__ flop, const int64_t *__restrict__ c_rp,
+    int32_t *__restrict__ c_col, double *__restrict__ c_val, int sorted,
+    const int2 *__restrict__ parts, const int32_t *__restrict__ part_off,
+    const int32_t *__restrict__ part_n, int32_t *__restrict__ seg_scratch, int64_t seg_stride,
+    unsigned long long *row_counter) {
+  extern __shared__ double s_dyn_f64[];
+  __shared__ int s_cnt;
+  __shared__ long long s_row;
+  constexpr int NW = THREADS / 32;
+  const int w = threadIdx.x >> 5;
+  double *vals = s_dyn_f64;
+  uint32_t *keys = reinterpret_cast<uint32_t *>(vals + kPartT);
+  int32_t *seg_a = reinterpret_cast<int32_t *>(keys + kPartT);
+  int32_t *seg_b = seg_a + kSegSmem;
+  uint32_t *bm = reinterpret_cast<uint32_t *>(seg_b + kSegSmem);
+  uint16_t *wpre = reinterpret_cast<uint16_t *>(bm + kPartRankWords);
+  int *gpre = reinterpret_cast<int *>(wpre + kPartRankWords);
+  while (true) {
+    if (threadIdx.x == 0) s_row = (long long)atomicAdd(row_counter, 1ull);
+    __syncthreads();
+    const int64_t r = s_row;
+    if (r >= nrows) break;
+    const int i = rows[r];
+    const int64_t rp0 = c_rp[i];
+    const int nnz = (int)(c_rp[i + 1] - rp0);
+    const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    const int na = (int)(ae - as);
+    const int np = part_n[i];
+    const int2 *pr = parts + part_off[i];
+    int32_t *sb = seg_a, *se = seg_b;  // segment begin / end (offsets in each B row)
+    if (na > kSegSmem) {
+      sb = seg_scratch + int64_t(blockIdx.x) * seg_stride;
+      se = sb + seg_stride / 2;
+    }
+    for (int j = threadIdx.x; j < na; j += THREADS) sb[j] = 0;
+    const bool seq = flop[i] >= int64_t(kSeqMinLen) * na * (np > 0 ? np : 1);
+    __syncthreads();
+    for (int p = 0; p < np; ++p) {
+      const int2 P = pr[p];
+      const int64_t hi = p + 1 < np ? int64_t(pr[p + 1].x) : B.ncols;
+      const int cnt = (p + 1 < np ? pr[p + 1].y : nnz) - P.y;
+      const int logT = num_log2(cnt);
+      const int T = 1 << logT;
+      for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
+      for (int j = threadIdx.x; j < na; j += THREADS) {
+        const int k = __ldg(A.col + as + j);
+        const int64_t bs = __ldg(B.rp + k);
+        const int len = (int)(__ldg(B.rp + k + 1) - bs);
+        se[j] = p + 1 == np ? len : gallop_lb(B.col + bs, sb[j], len, hi);
+      }
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
+      auto entry = [&](int64_t j) {
+        const int k = __ldg(A.col + as + j);
+        Entry en;
+        en.bs = __ldg(B.rp + k) + sb[j];
+        en.len = se[j] - sb[j];
+        en.a = __ldg(A.val + as + j);
+        return en;
+      };
+      auto acc = [&](bool act, uint32_t c, double v) {
+        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);  // c_ij <- c_ij + value
+      };
+      if (seq) for_entries<true, true>(B, na, w, NW, entry, acc);
+      else for_entries<false, true>(B, na, w, NW, entry, acc);
+      __syncthreads();
+      if (!sorted) {
+        block_emit_unsorted(keys, vals, T, rp0 + P.y, c_col, c_val, &s_cnt);
+      } else {
+        const int64_t width = (hi - P.x) < kPartWidth ? (hi - P.x) : kPartWidth;
+        block_rank_emit(keys, vals, T, P.x, width, bm, wpre, gpre, &s_cnt, rp0 + P.y, c_col,
+                        c_val);
+      }
+      int32_t *t = sb;  // the next part's segments start where these ended
+      sb = se;
+      se = t;
+      __syncthreads();
+    }
   }
 }
 

@@ -26,12 +26,13 @@ __global__ void __launch_bounds__(256) k_flop_bin(DevCSR A, const int64_t *__res
   constexpr int kRowsPerWarp = 32 / G;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  unsigned long long my_sum = 0, my_max = 0, my_maxb = 0;
+  unsigned long long my_sum = 0, my_max = 0, my_maxb = 0, my_maxa = 0;
   for (int64_t base = warp * kRowsPerWarp; base < A.nrows; base += nwarps * kRowsPerWarp) {
     const int64_t i = base + lane / G;
     if (i < A.nrows) {  // uniform inside the G-lane group
       const int64_t s = A.rp[i], e = A.rp[i + 1];
       int64_t f = 0, mb = 0;
+      if (gl == 0) my_maxa = (unsigned long long)(e - s) > my_maxa ? (unsigned long long)(e - s) : my_maxa;
       for (int64_t j = s + gl; j < e; j += G) {
         const int k = __ldg(A.col + j);
         const int64_t len = __ldg(b_rp + k + 1) - __ldg(b_rp + k);
@@ -56,11 +57,14 @@ __global__ void __launch_bounds__(256) k_flop_bin(DevCSR A, const int64_t *__res
     my_max = t > my_max ? t : my_max;
     t = __shfl_xor_sync(kFull, my_maxb, o);
     my_maxb = t > my_maxb ? t : my_maxb;
+    t = __shfl_xor_sync(kFull, my_maxa, o);
+    my_maxa = t > my_maxa ? t : my_maxa;
   }
   if (lane == 0) {
     atomicAdd(&s_sum, my_sum);
     atomicMax(&s_max, my_max);
     atomicMax(&s_maxb, my_maxb);
+    if (my_maxa) atomicMax(&info->max_arow, my_maxa);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -217,6 +221,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
   if (threadIdx.x == 0) atomicMax(&info->max_nnz, s_max);
   if (threadIdx.x > 0 && threadIdx.x < kMaxBins && s_bins[threadIdx.x])
     atomicAdd(&info->num_count[threadIdx.x], (unsigned long long)s_bins[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// Are all rows of B strictly increasing?  (Enables the column-range parts of
+// the numeric G tier, which binary-search B rows.)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_check_sorted(DevCSR B, PlanInfo *info) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  bool bad = false;
+  for (int64_t i = warp; i < B.nrows && !bad; i += nwarps) {
+    const int64_t s = B.rp[i], e = B.rp[i + 1];
+    for (int64_t q = s + 1 + lane; q < e; q += 32) bad |= __ldg(B.col + q - 1) >= __ldg(B.col + q);
+    bad = __any_sync(kFull, bad);
+  }
+  if (bad && lane == 0) atomicOr(&info->b_unsorted, 1ull);
 }
 
 // ---------------------------------------------------------------------------

@@ -19,7 +19,7 @@ constexpr int64_t kMaxBRow = int64_t(1) << 26;  // 32 rows * 2^26 < 2^31 per chu
 // to >= 32 slots on the GPU.  Numeric bins by T_n = lowest 2^n >= 2 nnz(c_i)
 // (load <= 1/2, reading R6).
 enum SymBin { SB_SKIP = 0, SB_W128, SB_W1024, SB_B2K, SB_B4K, SB_B8K, SB_B16K, SB_B32K,
-              SB_G, SB_COUNT };
+              SB_G, SB_BM, SB_COUNT };
 enum NumBin { NB_SKIP = 0, NB_W256, NB_W1024, NB_B2K, NB_B4K, NB_B8K, NB_B16K, NB_G,
               NB_COUNT };
 constexpr int kMaxBins = 12;
@@ -44,6 +44,11 @@ struct PlanInfo {
   unsigned long long num_cursor[kMaxBins];
   unsigned long long mask_sum;
   unsigned long long flags;
+  unsigned long long max_arow;    // max nnz(a_i)
+  unsigned long long b_unsorted;  // 1 if some B row is not strictly increasing
+  unsigned long long parts_used;  // bump allocator of the parts buffer
+  unsigned long long parts_overflow;
+  unsigned long long row_counter;   // dynamic row queue of the numeric G tier
 };
 
 __host__ __device__ __forceinline__ int log2_ceil64(uint64_t x) {  // smallest n: 2^n >= x
@@ -74,14 +79,28 @@ __device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {
   return n < kMinLogT ? kMinLogT : n;
 }
 
+// Rows whose table would exceed 8192 slots use the smem BITMAP tier when the
+// column space fits one (it also cuts the row into column-range parts for the
+// numeric phase); otherwise the larger smem hash tables / global hash.
+constexpr int64_t kBitmapMaxCols = int64_t(200 * 1024) * 8;  // 200 KB of bits
+
 __device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols) {
   if (flop == 0) return SB_SKIP;
   int n = sym_log2_gpu(flop, ncols);
   if (n <= 7) return SB_W128;
   if (n <= 10) return SB_W1024;
+  if (n <= 13) return SB_B2K + (n - 11);
+  if (ncols <= kBitmapMaxCols) return SB_BM;
   if (n <= 15) return SB_B2K + (n - 11);
   return SB_G;
 }
+
+// Column-range parts of a long row (numeric G tier): at most kPartKeys keys
+// and at most kPartWidth columns each.
+constexpr int kPartKeys = 4096;
+constexpr int kPartWidthLog = 18;
+constexpr int64_t kPartWidth = int64_t(1) << kPartWidthLog;
+constexpr int kMaxPartsPerRow = 512;  // >= kBitmapMaxCols / kPartKeys + kBitmapMaxCols / kPartWidth + 2
 
 __device__ __forceinline__ int num_log2(int64_t nnz) {
   int n = log2_ceil64(uint64_t(2 * nnz));

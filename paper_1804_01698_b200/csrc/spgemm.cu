@@ -38,6 +38,8 @@ struct spg_ctx {
   void *user = nullptr;
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
+  Buf parts, part_off, part_n, seg;  // column-range parts of long rows (BM tier)
+  bool plan_parts = false;           // parts were produced for the numeric G tier
   PlanInfo *host_info = nullptr;  // pinned
   cudaStream_t sub[kSubStreams] = {};
   cudaEvent_t ev_fork = nullptr;
@@ -230,7 +232,6 @@ int64_t bin_offset(const unsigned long long *cnt, int b) {
   return off;
 }
 
-constexpr size_t kSymBitmapMaxWords = (200 * 1024) / 4;  // ncols <= 1.6M -> smem bitmap
 
 }  // namespace
 
@@ -276,7 +277,8 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_num_block<1024>, s_num_b) == SPG_OK &&
          set_smem(c, k_sym_block<512>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
-         set_smem(c, k_sym_bitmap<1024>, kSymBitmapMaxWords * 4) == SPG_OK &&
+         set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
+         set_smem(c, k_num_part<1024>, kPartSmem) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
   if (!ok) {
@@ -291,7 +293,8 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
 spg_status spg_ctx_destroy(spg_ctx *c) {
   if (!c) return SPG_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
-  Buf *bufs[] = {&c->flop, &c->rows_sym, &c->rows_num, &c->partial, &c->slab, &c->info, &c->scratch};
+  Buf *bufs[] = {&c->flop,  &c->rows_sym, &c->rows_num, &c->partial, &c->slab,
+                 &c->info,  &c->scratch,  &c->parts,    &c->part_off, &c->part_n, &c->seg};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {
@@ -396,6 +399,25 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     PlanInfo h = *c->host_info;
     if ((int64_t)h.max_brow > kMaxBRow)
       return fail(c, SPG_ERR_OVERFLOW, "a row of B has more than 2^26 entries");
+    // BM tier: is B row-sorted (column-range parts need it)?  parts buffers
+    c->plan_parts = false;
+    int2 *parts = nullptr;
+    int64_t parts_cap = 0;
+    if (h.sym_count[SB_BM]) {
+      const int64_t gridc = std::min<int64_t>(ceil_div(B->nrows, 8), int64_t(c->num_sms) * 16);
+      {
+        ProfScope _ps(c, s, "k_check_sorted");
+        k_check_sorted<<<(unsigned)std::max<int64_t>(gridc, 1), 256, 0, s>>>(dev(B), info);
+      }
+      SPG_LAUNCHED(c, "k_check_sorted");
+      const int64_t nwd = (B->ncols + kPartWidth - 1) / kPartWidth;
+      parts_cap = (int64_t)(h.flop_total / kPartKeys) + (int64_t)h.sym_count[SB_BM] * (nwd + 2) + 16;
+      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * sizeof(int2), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->part_off, size_t(m) * 4, s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->part_n, size_t(m) * 4, s)) != SPG_OK) return st;
+      parts = (int2 *)c->parts.p;
+      c->plan_parts = true;
+    }
     // a3: symbolic per bin, bins on concurrent internal streams
     if ((st = fork(c, s)) != SPG_OK) return st;
     DevCSR a = dev(A), b = dev(B);
@@ -434,16 +456,18 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
             k_sym_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, row_nnz);
           }
         SPG_LAUNCHED(c, "k_sym_block");
-      } else {  // SB_G
+      } else if (bin == SB_BM) {
         const size_t nwords = size_t((B->ncols + 31) / 32);
-        if (nwords <= kSymBitmapMaxWords) {
-          const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
-          {
-            ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
-            k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(rb, n, a, b, row_nnz);
-          }
-          SPG_LAUNCHED(c, "k_sym_bitmap");
-        } else {
+        const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
+        {
+          ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
+          k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(
+              rb, n, a, b, flop, row_nnz, info, parts, parts_cap, (int32_t *)c->part_off.p,
+              (int32_t *)c->part_n.p);
+        }
+        SPG_LAUNCHED(c, "k_sym_bitmap");
+      } else {  // SB_G
+        {
           const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
           int lg = 0;
           {
@@ -509,12 +533,22 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   const int32_t *rows = (const int32_t *)c->rows_num.p;
   const int64_t *flop = (const int64_t *)c->flop.p;
   // G-tier slab: keys + vals of lowest 2^n >= 2 * max nnz(c_i) per block
-  int64_t g_grid = 0, slabT = 0;
+  int64_t g_grid = 0, slabT = 0, seg_stride = 0;
+  const bool use_parts = c->plan_parts && h.b_unsorted == 0 && h.parts_overflow == 0;
   if (h.num_count[NB_G]) {
     g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
-    int lg = log2_ceil64(2 * h.max_nnz);
-    slabT = int64_t(1) << std::max(lg, kMinLogT);
-    if ((st = buf_ensure(c, c->slab, size_t(g_grid) * size_t(slabT) * 12, s)) != SPG_OK) return st;
+    if (use_parts) {
+      SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));
+      if ((int64_t)h.max_arow > kSegSmem) {
+        seg_stride = 2 * (int64_t)h.max_arow;
+        if ((st = buf_ensure(c, c->seg, size_t(g_grid) * size_t(seg_stride) * 4, s)) != SPG_OK)
+          return st;
+      }
+    } else {
+      int lg = log2_ceil64(2 * h.max_nnz);
+      slabT = int64_t(1) << std::max(lg, kMinLogT);
+      if ((st = buf_ensure(c, c->slab, size_t(g_grid) * size_t(slabT) * 12, s)) != SPG_OK) return st;
+    }
   }
   if ((st = fork(c, s)) != SPG_OK) return st;
   int sidx = 0;
@@ -556,6 +590,15 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
           k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
         }
       SPG_LAUNCHED(c, "k_num_block");
+    } else if (use_parts) {  // NB_G with column-range parts
+      {
+        ProfScope _ps(c, ss, "k_num_part<1024>");
+        k_num_part<1024><<<(unsigned)g_grid, 1024, kPartSmem, ss>>>(
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
+            (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p, (int32_t *)c->seg.p,
+            seg_stride, &((PlanInfo *)c->info.p)->row_counter);
+      }
+      SPG_LAUNCHED(c, "k_num_part");
     } else {  // NB_G
       uint32_t *sk = (uint32_t *)c->slab.p;
       double *sv = (double *)((char *)c->slab.p + size_t(g_grid) * size_t(slabT) * 4);

@@ -35,43 +35,42 @@ __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
 }
 
 // ---------------------------------------------------------------------------
-// Product enumeration.  The products of row i are cut into ROUNDS of <= 32
-// products; the NW warps of the row's owner (one warp in the W tier, a block
-// in the B/G tiers) take rounds round-robin (round g goes to warp g % NW), so
-// a row with few a_ik but long B rows still keeps every warp busy.  f(active,
-// col, a_ik * b_kj) is called by all 32 lanes of a warp once per round.
-//
+// Product enumeration.  The products of a row are cut into ROUNDS of <= 32
+// products; f(active, col, a_ik * b_kj) is called by all 32 lanes of a warp
+// once per round.
 //  - sequential rounds (kSeq): a round is <= 32 consecutive b_kj of ONE B row,
 //    so the keys of a round are distinct (CSR rows hold unique columns);
 //  - flattened rounds: 32 consecutive products of the row's product list,
 //    whatever the B-row lengths (full lanes for short B rows).
-// kVal = false skips the values (symbolic phase).
+// With NW warps per row (B/G tiers) each chunk of 32 a_ik has its rounds cut
+// into NW contiguous ranges, one per warp, so a row with few a_ik but long B
+// rows still keeps every warp busy; a warp takes two rounds per step (two
+// independent gathers in flight).
+// `entry(j) -> Entry{bs, len, a}` describes entry j of the row: the B
+// segment [bs, bs+len) that its a_ik multiplies.  kVal = false skips values.
 // ---------------------------------------------------------------------------
-template <bool kSeq, bool kVal, typename F>
-__device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_t as,
-                                        int64_t ae, int w, int NW, F &&f) {
+struct Entry {
+  int64_t bs;
+  int len;
+  double a;
+};
+
+template <bool kSeq, bool kVal, typename EF, typename F>
+__device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w, int NW,
+                                            EF &&entry, F &&f) {
   const int lane = lane_id();
-  int64_t gbase = 0;  // rounds of the previous chunks
-  for (int64_t cb = as; cb < ae; cb += 32) {
-    const int64_t e = cb + lane;
-    int len = 0;
-    int64_t bs = 0;
-    double a = 0.0;
-    if (e < ae) {
-      const int k = __ldg(A.col + e);
-      if (kVal) a = __ldg(A.val + e);
-      bs = __ldg(B.rp + k);
-      len = (int)(__ldg(B.rp + k + 1) - bs);
-    }
+  for (int64_t cb = 0; cb < nent; cb += 32) {
+    Entry en{0, 0, 0.0};
+    if (cb + lane < nent) en = entry(cb + lane);
     if (kSeq && NW == 1) {
       // one warp owns the row: walk the nonempty entries directly
-      unsigned pend = __ballot_sync(kFull, len > 0);
+      unsigned pend = __ballot_sync(kFull, en.len > 0);
       while (pend) {
         const int j = __ffs(pend) - 1;
         pend &= pend - 1;
-        const int64_t jbs = shfl_i64(bs, j);
-        const int L = __shfl_sync(kFull, len, j);
-        const double aj = kVal ? shfl_f64(a, j) : 0.0;
+        const int64_t jbs = shfl_i64(en.bs, j);
+        const int L = __shfl_sync(kFull, en.len, j);
+        const double aj = kVal ? shfl_f64(en.a, j) : 0.0;
         for (int t = 0; t < L; t += 32) {
           const bool act = t + lane < L;
           uint32_t c = 0u;
@@ -85,39 +84,89 @@ __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_
       }
       continue;
     }
-    const int r = kSeq ? ((len + 31) >> 5) : len;  // rounds (seq) or products per entry
+    const int r = kSeq ? ((en.len + 31) >> 5) : en.len;  // rounds (seq) or products
     const int incl = warp_incl_scan(r);
-    const int excl = incl - r;
     const int total = __shfl_sync(kFull, incl, 31);
     const int nr = kSeq ? total : ((total + 31) >> 5);
-    int g = (int)((w - gbase % NW + NW) % NW);
-    for (; g < nr; g += NW) {
-      int64_t q;
+    const int g0 = (int)((int64_t)nr * w / NW), g1 = (int)((int64_t)nr * (w + 1) / NW);
+    if (g0 >= g1) continue;
+    if (kSeq) {
+      // the owner entry of round g advances monotonically along [g0, g1)
+      int own = 0, obeg = 0, oend = 0, olen = 0;
+      int64_t obs = 0;
       double oa = 0.0;
-      bool act;
-      if (kSeq) {
-        const int own = owner_lane(incl, g);
-        const int t = (g - __shfl_sync(kFull, excl, own)) * 32 + lane;
-        q = shfl_i64(bs, own) + t;
-        act = t < __shfl_sync(kFull, len, own);
-        if (kVal) oa = shfl_f64(a, own);
-      } else {
+      auto advance = [&](int g) {
+        while (g >= oend) {
+          own = owner_lane(incl, g);
+          oend = __shfl_sync(kFull, incl, own);
+          obeg = oend - __shfl_sync(kFull, r, own);
+          obs = shfl_i64(en.bs, own);
+          olen = __shfl_sync(kFull, en.len, own);
+          if (kVal) oa = shfl_f64(en.a, own);
+        }
+      };
+      for (int g = g0; g < g1; g += 2) {
+        advance(g);
+        const int t0 = (g - obeg) * 32 + lane;
+        const bool act0 = t0 < olen;
+        const int64_t q0 = obs + t0;
+        const double a0 = oa;
+        bool act1 = false;
+        int64_t q1 = 0;
+        double a1 = 0.0;
+        if (g + 1 < g1) {
+          advance(g + 1);
+          const int t1 = (g + 1 - obeg) * 32 + lane;
+          act1 = t1 < olen;
+          q1 = obs + t1;
+          a1 = oa;
+        }
+        uint32_t c0 = 0u, c1 = 0u;
+        double v0 = 0.0, v1 = 0.0;
+        if (act0) c0 = (uint32_t)__ldg(B.col + q0);
+        if (act1) c1 = (uint32_t)__ldg(B.col + q1);
+        if (kVal) {
+          if (act0) v0 = a0 * __ldg(B.val + q0);  // value <- a_ik * b_kj (l.5)
+          if (act1) v1 = a1 * __ldg(B.val + q1);
+        }
+        f(act0, c0, v0);
+        f(act1, c1, v1);
+      }
+    } else {
+      for (int g = g0; g < g1; ++g) {
         const int p = g * 32 + lane;
         const int own = owner_lane(incl, p);
-        q = shfl_i64(bs, own) + (p - __shfl_sync(kFull, excl, own));
-        act = p < total;
-        if (kVal) oa = shfl_f64(a, own);
+        const int oex = __shfl_sync(kFull, incl - r, own);
+        const int64_t q = shfl_i64(en.bs, own) + (p - oex);
+        const double oa = kVal ? shfl_f64(en.a, own) : 0.0;
+        const bool act = p < total;
+        uint32_t c = 0u;
+        double v = 0.0;
+        if (act) {
+          c = (uint32_t)__ldg(B.col + q);
+          if (kVal) v = oa * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+        }
+        f(act, c, v);
       }
-      uint32_t c = 0u;
-      double v = 0.0;
-      if (act) {
-        c = (uint32_t)__ldg(B.col + q);
-        if (kVal) v = oa * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
-      }
-      f(act, c, v);
     }
-    gbase += nr;
   }
+}
+
+// All products of row [as, ae) of A.
+template <bool kSeq, bool kVal, typename F>
+__device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_t as,
+                                        int64_t ae, int w, int NW, F &&f) {
+  for_entries<kSeq, kVal>(
+      B, ae - as, w, NW,
+      [&](int64_t j) {
+        const int k = __ldg(A.col + as + j);
+        Entry en;
+        en.bs = __ldg(B.rp + k);
+        en.len = (int)(__ldg(B.rp + k + 1) - en.bs);
+        en.a = kVal ? __ldg(A.val + as + j) : 0.0;
+        return en;
+      },
+      f);
 }
 
 // Rows whose B rows average >= kSeqMinLen entries use the sequential
@@ -194,32 +243,124 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 }
 
 // ---------------------------------------------------------------------------
-// G tier, bitmap form (ncols small enough for an ncols-bit set in smem): the
-// set of distinct columns of c_i* is exactly the set bits.
+// BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
+// c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
+// sorted it also cuts rows with nnz > kPartKeys into column-range parts for the
+// numeric G tier: cuts at every kPartKeys-th key (rank cuts) and at every
+// multiple of kPartWidth (width cuts); part = (first column, keys of the row
+// before it); ranges holding no key are merged into the previous part.
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restrict__ rows,
                                                         int64_t nrows, DevCSR A, DevCSR B,
-                                                        int64_t *__restrict__ row_nnz) {
+                                                        const int64_t *__restrict__ flop,
+                                                        int64_t *__restrict__ row_nnz,
+                                                        PlanInfo *info, int2 *__restrict__ parts,
+                                                        int64_t parts_cap,
+                                                        int32_t *__restrict__ part_off,
+                                                        int32_t *__restrict__ part_n) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt;
+  __shared__ int s_warp[THREADS / 32];
+  __shared__ int2 s_rank[kMaxPartsPerRow];   // rank cuts (col, cum)
+  __shared__ int2 s_width[kMaxPartsPerRow];  // width cuts (col, cum)
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwords = (int)((B.ncols + 31) >> 5);
   uint32_t *bm = s_dyn_u32;
+  const bool want_parts = parts != nullptr && info->b_unsorted == 0;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int i = rows[r];
     for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     int cnt = 0;
-    for_row<false, false>(A, B, A.rp[i], A.rp[i + 1], w, NW, [&](bool act, uint32_t c, double) {
+    const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    auto ins = [&](bool act, uint32_t c, double) {
       if (act) cnt += sym_bitmap_insert(bm, c);
-    });
+    };
+    if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
+    else for_row<false, false>(A, B, as, ae, w, NW, ins);
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
-    if (threadIdx.x == 0) row_nnz[i] = s_cnt;
+    const int nnz = s_cnt;
+    if (threadIdx.x == 0) row_nnz[i] = nnz;
+    if (want_parts && nnz > kPartKeys) {
+      // each thread owns a contiguous range of words; block scan of popcounts
+      const int per = (nwords + THREADS - 1) / THREADS;
+      const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
+      int mine = 0;
+      for (int q = w0; q < w1; ++q) mine += __popc(bm[q]);
+      const int incl = warp_incl_scan(mine);
+      if (lane == 31) s_warp[w] = incl;
+      __syncthreads();
+      if (w == 0) {
+        const int v = lane < NW ? s_warp[lane] : 0;
+        const int vi = warp_incl_scan(v);
+        if (lane < NW) s_warp[lane] = vi - v;
+      }
+      __syncthreads();
+      int cum = s_warp[w] + incl - mine;  // keys before word w0
+      for (int q = w0; q < w1; ++q) {
+        const uint32_t word = bm[q];
+        const int pc = __popc(word);
+        if (q > 0 && ((int64_t(q) * 32) & (kPartWidth - 1)) == 0) {  // width cut
+          const int k = (int)((int64_t(q) * 32) >> kPartWidthLog);
+          if (k < kMaxPartsPerRow) s_width[k] = make_int2(q * 32, cum);
+        }
+        int nextR = ((cum + kPartKeys - 1) / kPartKeys) * kPartKeys;  // rank cuts
+        if (nextR == 0) nextR = kPartKeys;
+        while (nextR < cum + pc) {
+          uint32_t wv = word;
+          for (int t = 0; t < nextR - cum; ++t) wv &= wv - 1;  // drop lower set bits
+          const int k = nextR / kPartKeys;
+          if (k < kMaxPartsPerRow) s_rank[k] = make_int2(q * 32 + __ffs(wv) - 1, nextR);
+          nextR += kPartKeys;
+        }
+        cum += pc;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        // merge rank cuts [1, nrk) and width cuts [1, nwd) by column
+        const int nrk = min((nnz - 1) / kPartKeys + 1, kMaxPartsPerRow);
+        const int nwd = min((int)((B.ncols - 1) >> kPartWidthLog) + 1, kMaxPartsPerRow);
+        int np = 0;
+        int64_t base = 0;
+        for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts, pass 1 writes
+          if (pass == 1) {
+            base = (int64_t)atomicAdd(&info->parts_used, (unsigned long long)np);
+            if (base + np > parts_cap) {
+              atomicAdd(&info->parts_overflow, 1ull);
+              part_n[i] = 0;
+              break;
+            }
+            part_off[i] = (int32_t)base;
+            part_n[i] = np;
+          }
+          np = 0;
+          int a = 1, b = 1;
+          int2 cur = make_int2(0, 0);
+          while (a < nrk || b < nwd) {
+            int2 nx;
+            if (a < nrk && (b >= nwd || s_rank[a].x <= s_width[b].x)) nx = s_rank[a++];
+            else nx = s_width[b++];
+            if (nx.y > cur.y) {  // [cur, nx) holds keys: emit it
+              if (pass == 1) parts[base + np] = cur;
+              ++np;
+            }
+            cur = nx;  // an empty range [cur, nx) is merged into its neighbours
+          }
+          if (nnz > cur.y) {
+            if (pass == 1) parts[base + np] = cur;
+            ++np;
+          }
+        }
+      }
+    } else if (threadIdx.x == 0 && part_n != nullptr) {
+      part_n[i] = 0;  // a single part: the whole row
+    }
+    __syncthreads();
   }
 }
 

@@ -120,6 +120,17 @@ def test_wide_columns_global_tables(spg, ctx, sorted_out):
     gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="wide ncols")
 
 
+@pytest.mark.parametrize("sorted_out", [True, False])
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_column_parts(spg, ctx, sorted_out, shuffle):
+    """Long rows over a 1M-column space: column-range parts with rank and width
+    cuts (sorted B), or the global-hash fallback (shuffled B)."""
+    specs = [(150000, 50000), (30000, 9000), (9000, 8193), (8193, 8193), (70000, 4097),
+             (20000, 12000), (5, 5), (0, 0), (600000, 200000)]
+    A, B = synth.crafted_rows(specs, 1_000_000, 14, shuffle=shuffle)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="column parts")
+
+
 @pytest.mark.parametrize("ncols", [1, 2, 16])
 def test_small_ncols_cap(spg, ctx, ncols):
     """min(N_col, flop) cap of the table size: large flop, tiny ncols."""
