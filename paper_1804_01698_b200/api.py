@@ -183,21 +183,31 @@ def row_blocks_by_bytes(A: DeviceCSR, B: DeviceCSR, budget_entries: int,
     return out
 
 
-def triangle_count(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, sorted: bool = False,
-                   block_entries: int | None = None, ctx: Context | None = None) -> int:
-    """Triangles = sum(C o G)/2, C = L*U (Sec 5.6, BASELINE config 5).
-    C is produced and consumed in row blocks (row-range views of L) so it never
-    has to fit whole in HBM."""
+def triangle_count_rows(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, r0: int, r1: int,
+                        sorted: bool = False, block_entries: int | None = None,
+                        ctx: Context | None = None) -> int:
+    """sum(C o G) over rows [r0, r1) of C = L*U, produced and consumed in row
+    blocks (row-range views of L) so C never has to fit whole in HBM."""
     ctx = ctx or default_context()
+    if r1 <= r0:
+        return 0
+    Lr = L.rows(r0, r1)
     if block_entries is None:
         free, _ = torch.cuda.mem_get_info(L.row_ptr.device)
         block_entries = max(1 << 20, int(free * 0.6) // 12)
-    offs = row_blocks_by_bytes(L, U, block_entries, ctx)
+    offs = row_blocks_by_bytes(Lr, U, block_entries, ctx)
     total = 0
-    for r0, r1 in zip(offs[:-1], offs[1:]):
-        C = spgemm(L.rows(r0, r1), U, sorted, ctx)
-        total += mask_sum(C, G, r0, ctx)
+    for b0, b1 in zip(offs[:-1], offs[1:]):
+        C = spgemm(Lr.rows(b0, b1), U, sorted, ctx)
+        total += mask_sum(C, G, r0 + b0, ctx)
         del C
+    return total
+
+
+def triangle_count(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, sorted: bool = False,
+                   block_entries: int | None = None, ctx: Context | None = None) -> int:
+    """Triangles = sum(C o G)/2, C = L*U (Sec 5.6, BASELINE config 5)."""
+    total = triangle_count_rows(L, U, G, 0, L.nrows, sorted, block_entries, ctx)
     if total % 2:
         raise RuntimeError("sum(C o G) is odd: G is not symmetric")
     return total // 2

@@ -59,11 +59,18 @@ template <bool kSeq, bool kVal, typename EF, typename F>
 __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w, int NW,
                                             EF &&entry, F &&f) {
   const int lane = lane_id();
-  for (int64_t cb = 0; cb < nent; cb += 32) {
+  // Many chunks: each warp owns whole chunks (chunk overhead paid once).  Few
+  // chunks: every warp walks every chunk and takes a contiguous slice of its
+  // rounds (keeps all warps busy on rows with few, long B rows).
+  const int64_t nchunks = (nent + 31) >> 5;
+  const bool own_chunks = NW == 1 || nchunks >= 2 * int64_t(NW);
+  const int64_t c_first = own_chunks ? int64_t(w) * 32 : 0;
+  const int64_t c_step = own_chunks ? int64_t(NW) * 32 : 32;
+  for (int64_t cb = c_first; cb < nent; cb += c_step) {
     Entry en{0, 0, 0.0};
     if (cb + lane < nent) en = entry(cb + lane);
-    if (kSeq && NW == 1) {
-      // one warp owns the row: walk the nonempty entries directly
+    if (kSeq && own_chunks) {
+      // this warp owns the chunk: walk its nonempty entries directly
       unsigned pend = __ballot_sync(kFull, en.len > 0);
       while (pend) {
         const int j = __ffs(pend) - 1;
@@ -88,7 +95,8 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
     const int incl = warp_incl_scan(r);
     const int total = __shfl_sync(kFull, incl, 31);
     const int nr = kSeq ? total : ((total + 31) >> 5);
-    const int g0 = (int)((int64_t)nr * w / NW), g1 = (int)((int64_t)nr * (w + 1) / NW);
+    const int g0 = own_chunks ? 0 : (int)((int64_t)nr * w / NW);
+    const int g1 = own_chunks ? nr : (int)((int64_t)nr * (w + 1) / NW);
     if (g0 >= g1) continue;
     if (kSeq) {
       // the owner entry of round g advances monotonically along [g0, g1)
