@@ -64,6 +64,98 @@ __device__ __forceinline__ void block_bitonic(uint32_t *keys, double *vals, int 
   }
 }
 
+// Warp emit of a warp-private table keys/vals[0, T) holding nnz keys to
+// out_base: unsorted = ballot compaction in slot order; sorted (a7) =
+// bucket (counting) sort: buckets b(c) = (c - min) >> sh are monotone in the
+// column, T buckets for nnz <= T/2 keys, each key's position = bucket offset
+// + its rank among the (few) keys of its bucket.  cnt[T] is scratch.
+__device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t *cnt, int T,
+                                          int logT, int nnz, int64_t rp0,
+                                          int32_t *__restrict__ c_col,
+                                          double *__restrict__ c_val, int sorted) {
+  const int lane = lane_id();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (!sorted) {
+    int base = 0;
+    for (int s0 = 0; s0 < T; s0 += 32) {
+      const uint32_t k = keys[s0 + lane];
+      const bool occ = k != kEmpty;
+      const unsigned bal = __ballot_sync(kFull, occ);
+      if (occ) {
+        const int64_t o = rp0 + base + __popc(bal & lt_mask);
+        c_col[o] = (int32_t)k;
+        c_val[o] = vals[s0 + lane];
+      }
+      base += __popc(bal);
+    }
+  } else {
+    // a7: ascending columns by a bucket (counting) sort.  Buckets
+    // are monotone in the column: b(c) = (c - min) >> sh, T buckets for
+    // nnz <= T/2 keys; each key's position = bucket offset + its rank
+    // among the (few) keys of its bucket.
+    // 1. compact occupied slots to the front (destination <= source)
+    int base = 0;
+    for (int s0 = 0; s0 < T; s0 += 32) {
+      const uint32_t k = keys[s0 + lane];
+      const double v = vals[s0 + lane];
+      const bool occ = k != kEmpty;
+      const unsigned bal = __ballot_sync(kFull, occ);
+      __syncwarp();
+      if (occ) {
+        const int d = base + __popc(bal & lt_mask);
+        keys[d] = k;
+        vals[d] = v;
+      }
+      base += __popc(bal);
+      __syncwarp();
+    }
+    // 2. key range and bucket shift
+    unsigned mn = 0xFFFFFFFFu, mx = 0u;
+    for (int e = lane; e < nnz; e += 32) {
+      const unsigned k = keys[e];
+      mn = k < mn ? k : mn;
+      mx = k > mx ? k : mx;
+    }
+    mn = __reduce_min_sync(kFull, mn);
+    mx = __reduce_max_sync(kFull, mx);
+    int sh = log2_ceil64(uint64_t(mx - mn) + 1) - logT;
+    sh = sh < 0 ? 0 : sh;
+    for (int b = lane; b < T; b += 32) cnt[b] = 0u;
+    __syncwarp();
+    uint32_t *loc = reinterpret_cast<uint32_t *>(vals + (T >> 1));  // free half
+    uint32_t *grp = keys + (T >> 1);                                  // free half
+    for (int e = lane; e < nnz; e += 32) loc[e] = atomicAdd(cnt + ((keys[e] - mn) >> sh), 1u);
+    __syncwarp();
+    // 3. exclusive scan of the bucket counts (lane owns T/32 consecutive)
+    const int per = T >> 5;
+    int run = 0;
+    for (int q = 0; q < per; ++q) run += (int)cnt[lane * per + q];
+    int ex = warp_incl_scan(run) - run;
+    for (int q = 0; q < per; ++q) {
+      const int v = (int)cnt[lane * per + q];
+      cnt[lane * per + q] = (uint32_t)ex;
+      ex += v;
+    }
+    __syncwarp();
+    // 4. group keys by bucket, 5. rank inside the bucket and store
+    for (int e = lane; e < nnz; e += 32) {
+      const uint32_t k = keys[e];
+      grp[cnt[(k - mn) >> sh] + loc[e]] = k;
+    }
+    __syncwarp();
+    for (int e = lane; e < nnz; e += 32) {
+      const uint32_t k = keys[e];
+      const uint32_t b = (k - mn) >> sh;
+      const int lo = (int)cnt[b];
+      const int hi = (int)b + 1 < T ? (int)cnt[b + 1] : nnz;
+      int rnk = 0;
+      for (int q = lo; q < hi; ++q) rnk += grp[q] < k;
+      c_col[rp0 + lo + rnk] = (int32_t)k;
+      c_val[rp0 + lo + rnk] = vals[e];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // W tier: one warp per row, warp-private keys[TMAX] + vals[TMAX] (+ cnt[TMAX]
 // bucket counters for the sort) in smem.
@@ -112,85 +204,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
         __syncwarp();
       });
     }
-    if (!sorted) {
-      int base = 0;
-      for (int s0 = 0; s0 < T; s0 += 32) {
-        const uint32_t k = keys[s0 + lane];
-        const bool occ = k != kEmpty;
-        const unsigned bal = __ballot_sync(kFull, occ);
-        if (occ) {
-          const int64_t o = rp0 + base + __popc(bal & lt_mask);
-          c_col[o] = (int32_t)k;
-          c_val[o] = vals[s0 + lane];
-        }
-        base += __popc(bal);
-      }
-    } else {
-      // a7: ascending columns by a bucket (counting) sort.  Buckets
-      // are monotone in the column: b(c) = (c - min) >> sh, T buckets for
-      // nnz <= T/2 keys; each key's position = bucket offset + its rank
-      // among the (few) keys of its bucket.
-      // 1. compact occupied slots to the front (destination <= source)
-      int base = 0;
-      for (int s0 = 0; s0 < T; s0 += 32) {
-        const uint32_t k = keys[s0 + lane];
-        const double v = vals[s0 + lane];
-        const bool occ = k != kEmpty;
-        const unsigned bal = __ballot_sync(kFull, occ);
-        __syncwarp();
-        if (occ) {
-          const int d = base + __popc(bal & lt_mask);
-          keys[d] = k;
-          vals[d] = v;
-        }
-        base += __popc(bal);
-        __syncwarp();
-      }
-      // 2. key range and bucket shift
-      unsigned mn = 0xFFFFFFFFu, mx = 0u;
-      for (int e = lane; e < nnz; e += 32) {
-        const unsigned k = keys[e];
-        mn = k < mn ? k : mn;
-        mx = k > mx ? k : mx;
-      }
-      mn = __reduce_min_sync(kFull, mn);
-      mx = __reduce_max_sync(kFull, mx);
-      int sh = log2_ceil64(uint64_t(mx - mn) + 1) - logT;
-      sh = sh < 0 ? 0 : sh;
-      for (int b = lane; b < T; b += 32) cnt[b] = 0u;
-      __syncwarp();
-      uint32_t *loc = reinterpret_cast<uint32_t *>(vals + (T >> 1));  // free half
-      uint32_t *grp = keys + (T >> 1);                                  // free half
-      for (int e = lane; e < nnz; e += 32) loc[e] = atomicAdd(cnt + ((keys[e] - mn) >> sh), 1u);
-      __syncwarp();
-      // 3. exclusive scan of the bucket counts (lane owns T/32 consecutive)
-      const int per = T >> 5;
-      int run = 0;
-      for (int q = 0; q < per; ++q) run += (int)cnt[lane * per + q];
-      int ex = warp_incl_scan(run) - run;
-      for (int q = 0; q < per; ++q) {
-        const int v = (int)cnt[lane * per + q];
-        cnt[lane * per + q] = (uint32_t)ex;
-        ex += v;
-      }
-      __syncwarp();
-      // 4. group keys by bucket, 5. rank inside the bucket and store
-      for (int e = lane; e < nnz; e += 32) {
-        const uint32_t k = keys[e];
-        grp[cnt[(k - mn) >> sh] + loc[e]] = k;
-      }
-      __syncwarp();
-      for (int e = lane; e < nnz; e += 32) {
-        const uint32_t k = keys[e];
-        const uint32_t b = (k - mn) >> sh;
-        const int lo = (int)cnt[b];
-        const int hi = (int)b + 1 < T ? (int)cnt[b + 1] : nnz;
-        int rnk = 0;
-        for (int q = lo; q < hi; ++q) rnk += grp[q] < k;
-        c_col[rp0 + lo + rnk] = (int32_t)k;
-        c_val[rp0 + lo + rnk] = vals[e];
-      }
-    }
+    warp_emit(keys, vals, cnt, T, logT, nnz, rp0, c_col, c_val, sorted);
     __syncwarp();
   }
 }
@@ -514,6 +528,98 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
       sb = se;
       se = t;
       __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// G tier, warp parts (rows with <= kWPartMaxEntries a_ik, B rows sorted):
+// one warp per row at a time (dynamic row queue), the row's parts of
+// kWPartKeys keys in column order, each accumulated in a warp-private smem
+// table (plain fp64 read-modify-write, as in the W tier) and emitted at
+// C_row_ptr[i] + (keys of the row before the part), sorted by the warp
+// bucket sort when requested.  B-row segments of a part: galloping search
+// from where the previous part's segment ended.
+// ---------------------------------------------------------------------------
+constexpr int kWPartT = 2 * kWPartKeys;
+constexpr size_t kWPartSmemPerWarp = size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * 8;
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
+    const int32_t *__restrict__ rows, int64_t nrows, DevCSR A, DevCSR B,
+    const int64_t *__restrict__ flop, const int64_t *__restrict__ c_rp,
+    int32_t *__restrict__ c_col, double *__restrict__ c_val, int sorted,
+    const int2 *__restrict__ parts, const int32_t *__restrict__ part_off,
+    const int32_t *__restrict__ part_n, unsigned long long *row_counter) {
+  extern __shared__ double s_dyn_f64[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *vals = s_dyn_f64 + w * kWPartT;
+  uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * kWPartT) + w * kWPartT;
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * kWPartT) + WARPS * kWPartT +
+                  w * kWPartT;
+  int32_t *sa = reinterpret_cast<int32_t *>(cnt + (WARPS - w) * kWPartT) +
+                w * 2 * kWPartMaxEntries;
+  int32_t *sbv = sa + kWPartMaxEntries;
+  while (true) {
+    long long r = 0;
+    if (lane == 0) r = (long long)atomicAdd(row_counter, 1ull);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= nrows) break;
+    const int i = rows[r];
+    const int64_t rp0 = c_rp[i];
+    const int nnz = (int)(c_rp[i + 1] - rp0);
+    const int64_t as = A.rp[i];
+    const int na = (int)(A.rp[i + 1] - as);
+    const int np = -part_n[i];
+    const int2 *pr = parts + part_off[i];
+    int32_t *sb = sa, *se = sbv;
+    for (int j = lane; j < na; j += 32) sb[j] = 0;
+    const bool seq = flop[i] >= int64_t(kSeqMinLen) * na * np;
+    __syncwarp();
+    for (int p = 0; p < np; ++p) {
+      const int2 P = pr[p];
+      const int64_t hi = p + 1 < np ? int64_t(pr[p + 1].x) : B.ncols;
+      const int cntp = (p + 1 < np ? pr[p + 1].y : nnz) - P.y;
+      const int logT = num_log2(cntp);
+      const int T = 1 << logT;
+      for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
+      for (int j = lane; j < na; j += 32) {
+        const int k = __ldg(A.col + as + j);
+        const int64_t bs = __ldg(B.rp + k);
+        const int len = (int)(__ldg(B.rp + k + 1) - bs);
+        se[j] = p + 1 == np ? len : gallop_lb(B.col + bs, sb[j], len, hi);
+      }
+      __syncwarp();
+      auto entry = [&](int64_t j) {
+        const int k = __ldg(A.col + as + j);
+        Entry en;
+        en.bs = __ldg(B.rp + k) + sb[j];
+        en.len = se[j] - sb[j];
+        en.a = __ldg(A.val + as + j);
+        return en;
+      };
+      if (seq) {
+        for_entries<true, true>(B, na, 0, 1, entry, [&](bool act, uint32_t c, double v) {
+          if (act) vals[num_probe(keys, c, logT)] += v;  // c_ij <- c_ij + value (l.8)
+          __syncwarp();
+        });
+      } else {
+        for_entries<false, true>(B, na, 0, 1, entry, [&](bool act, uint32_t c, double v) {
+          uint32_t slot = 0;
+          if (act) slot = num_probe(keys, c, logT);
+          const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
+          if (act) {
+            if (__popc(grp) == 1) vals[slot] += v;
+            else atomicAdd(vals + slot, v);
+          }
+          __syncwarp();
+        });
+      }
+      warp_emit(keys, vals, cnt, T, logT, cntp, rp0 + P.y, c_col, c_val, sorted);
+      int32_t *t = sb;
+      sb = se;
+      se = t;
+      __syncwarp();
     }
   }
 }

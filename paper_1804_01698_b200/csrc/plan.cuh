@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(256) k_flop_bin(DevCSR A, const int64_t *__res
 __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *__restrict__ key,
                                                      int64_t ncols, int mode, PlanInfo *info,
                                                      int32_t *__restrict__ rows_out,
-                                                     int64_t *__restrict__ row_nnz) {
+                                                     int64_t *__restrict__ row_nnz,
+                                                     const int32_t *__restrict__ part_n) {
   __shared__ unsigned s_cnt[kMaxBins];
   __shared__ unsigned long long s_base[kMaxBins];
   if (threadIdx.x < kMaxBins) s_cnt[threadIdx.x] = 0;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
       b = sym_bin(key[i], ncols);
       if (b == SB_SKIP) row_nnz[i] = 0;
     } else {
-      b = num_bin(key[i + 1] - key[i]);
+      b = num_bin_row(key[i + 1] - key[i], part_n, i);
     }
     if (b != 0) local = atomicAdd(&s_cnt[b], 1u);
   }
@@ -186,7 +187,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partials(int64_t *__restr
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict__ data, int64_t n,
                                                             const int64_t *__restrict__ partial,
-                                                            PlanInfo *info) {
+                                                            PlanInfo *info,
+                                                            const int32_t *__restrict__ part_n) {
   __shared__ long long s_warp[33];
   __shared__ unsigned s_bins[kMaxBins];
   __shared__ unsigned long long s_max;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < kScanItems; ++t)
-    if (base + t < n && v[t] > 0) atomicAdd(&s_bins[num_bin(v[t])], 1u);
+    if (base + t < n && v[t] > 0) atomicAdd(&s_bins[num_bin_row(v[t], part_n, base + t)], 1u);
   long long tot;
   long long ex = block_excl_scan_1024(s, s_warp, &tot) + partial[blockIdx.x];
 #pragma unroll

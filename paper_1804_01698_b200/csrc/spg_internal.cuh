@@ -20,7 +20,7 @@ constexpr int64_t kMaxBRow = int64_t(1) << 26;  // 32 rows * 2^26 < 2^31 per chu
 // (load <= 1/2, reading R6).
 enum SymBin { SB_SKIP = 0, SB_W128, SB_W1024, SB_B2K, SB_B4K, SB_B8K, SB_B16K, SB_B32K,
               SB_G, SB_BM, SB_COUNT };
-enum NumBin { NB_SKIP = 0, NB_W256, NB_W1024, NB_B2K, NB_B4K, NB_B8K, NB_B16K, NB_G,
+enum NumBin { NB_SKIP = 0, NB_W256, NB_W1024, NB_B2K, NB_B4K, NB_B8K, NB_B16K, NB_G, NB_GW,
               NB_COUNT };
 constexpr int kMaxBins = 12;
 
@@ -49,6 +49,7 @@ struct PlanInfo {
   unsigned long long parts_used;  // bump allocator of the parts buffer
   unsigned long long parts_overflow;
   unsigned long long row_counter;   // dynamic row queue of the numeric G tier
+  unsigned long long row_counter_w; // dynamic row queue of the warp-part tier
 };
 
 __host__ __device__ __forceinline__ int log2_ceil64(uint64_t x) {  // smallest n: 2^n >= x
@@ -101,6 +102,11 @@ constexpr int kPartKeys = 4096;
 constexpr int kPartWidthLog = 18;
 constexpr int64_t kPartWidth = int64_t(1) << kPartWidthLog;
 constexpr int kMaxPartsPerRow = 512;  // >= kBitmapMaxCols / kPartKeys + kBitmapMaxCols / kPartWidth + 2
+// Rows with few a_ik are cut into small WARP parts instead (one warp per
+// part, warp-private table): rank cuts every kWPartKeys keys.
+constexpr int kWPartKeys = 256;
+constexpr int kWPartMaxEntries = 128;
+
 
 __device__ __forceinline__ int num_log2(int64_t nnz) {
   int n = log2_ceil64(uint64_t(2 * nnz));
@@ -114,6 +120,13 @@ __device__ __forceinline__ int num_bin(int64_t nnz) {
   if (n <= 10) return NB_W1024;
   if (n <= 14) return NB_B2K + (n - 11);
   return NB_G;
+}
+
+// numeric bin of a row, with the part kind of long rows (part_n < 0: warp parts)
+__device__ __forceinline__ int num_bin_row(int64_t nnz, const int32_t *part_n, int64_t i) {
+  const int b = num_bin(nnz);
+  if (b == NB_G && part_n != nullptr && part_n[i] < 0) return NB_GW;
+  return b;
 }
 
 // Fibonacci hashing: HIGH bits of col*H (reading R5 of DESIGN.md; the paper's

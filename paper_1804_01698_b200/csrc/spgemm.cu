@@ -195,7 +195,8 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
 }
 
 // scan of data[0..n) in place (int64), numeric-bin counting in the last pass
-spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s) {
+spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
+                       const int32_t *part_n = nullptr) {
   if (n == 0) return SPG_OK;
   const int64_t nb = ceil_div(n, kScanTile);
   SPG_CUDA(c, cudaGetLastError());
@@ -214,7 +215,8 @@ spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s) {
   SPG_LAUNCHED(c, "k_scan_partials");
   {
     ProfScope _ps(c, s, "k_scan_down");
-    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p);
+    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p,
+                                                      part_n);
   }
   SPG_LAUNCHED(c, "k_scan_down");
   return SPG_OK;
@@ -279,6 +281,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_part<1024>, kPartSmem) == SPG_OK &&
+         set_smem(c, k_num_wpart<8>, 8 * kWPartSmemPerWarp) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
   if (!ok) {
@@ -367,6 +370,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
                         int64_t *nnz_C, int64_t *flop_total, void *stream) {
   if (!c) return SPG_ERR_INVALID_ARG;
   c->have_plan = false;
+  c->plan_parts = false;
   spg_status st;
   if ((st = check_csr(c, A, "A", false)) != SPG_OK) return st;
   if ((st = check_csr(c, B, "B", false)) != SPG_OK) return st;
@@ -392,7 +396,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     {
       ProfScope _ps(c, s, "k_bin_scatter_sym");
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, B->ncols, 0, info,
-                                                               (int32_t *)c->rows_sym.p, row_nnz);
+                                                               (int32_t *)c->rows_sym.p, row_nnz, nullptr);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(sym)");
     if ((st = read_info(c, s)) != SPG_OK) return st;
@@ -411,7 +415,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       }
       SPG_LAUNCHED(c, "k_check_sorted");
       const int64_t nwd = (B->ncols + kPartWidth - 1) / kPartWidth;
-      parts_cap = (int64_t)(h.flop_total / kPartKeys) + (int64_t)h.sym_count[SB_BM] * (nwd + 2) + 16;
+      parts_cap = (int64_t)(h.flop_total / kWPartKeys) + (int64_t)h.sym_count[SB_BM] * (nwd + 2) + 16;
       if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * sizeof(int2), s)) != SPG_OK) return st;
       if ((st = buf_ensure(c, c->part_off, size_t(m) * 4, s)) != SPG_OK) return st;
       if ((st = buf_ensure(c, c->part_n, size_t(m) * 4, s)) != SPG_OK) return st;
@@ -490,12 +494,13 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     SPG_CUDA(c, cudaMemsetAsync(row_nnz, 0, size_t(m) * 8, s));
   }
   // a4: C_row_ptr = exclusive scan of row nnz (+ numeric bin counts)
-  if ((st = launch_scan(c, row_nnz, m, s)) != SPG_OK) return st;
+  const int32_t *pn = c->plan_parts ? (const int32_t *)c->part_n.p : nullptr;
+  if ((st = launch_scan(c, row_nnz, m, s, pn)) != SPG_OK) return st;
   if (m > 0) {
     {
       ProfScope _ps(c, s, "k_bin_scatter_num");
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, 0, 1, info,
-                                                               (int32_t *)c->rows_num.p, nullptr);
+                                                               (int32_t *)c->rows_num.p, nullptr, pn);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(num)");
   }
@@ -590,6 +595,17 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
           k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
         }
       SPG_LAUNCHED(c, "k_num_block");
+    } else if (bin == NB_GW) {  // warp parts
+      const int64_t grid = std::min<int64_t>(ceil_div(n, 8), int64_t(c->num_sms) * 3);
+      SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter_w, 0, 8, ss));
+      {
+        ProfScope _ps(c, ss, "k_num_wpart<8>");
+        k_num_wpart<8><<<(unsigned)grid, 256, 8 * kWPartSmemPerWarp, ss>>>(
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
+            (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p,
+            &((PlanInfo *)c->info.p)->row_counter_w);
+      }
+      SPG_LAUNCHED(c, "k_num_wpart");
     } else if (use_parts) {  // NB_G with column-range parts
       {
         ProfScope _ps(c, ss, "k_num_part<1024>");

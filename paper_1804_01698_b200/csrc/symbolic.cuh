@@ -69,6 +69,46 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
   for (int64_t cb = c_first; cb < nent; cb += c_step) {
     Entry en{0, 0, 0.0};
     if (cb + lane < nent) en = entry(cb + lane);
+    if (kSeq && own_chunks && __all_sync(kFull, en.len <= 32)) {
+      // this warp owns the chunk and every B row fits one round: one round per
+      // nonempty entry, the gathers of the next round issued before this one
+      // is hashed (software pipeline)
+      unsigned pend = __ballot_sync(kFull, en.len > 0);
+      if (!pend) continue;
+      int j = __ffs(pend) - 1;
+      pend &= pend - 1;
+      int L = __shfl_sync(kFull, en.len, j);
+      double aj = kVal ? shfl_f64(en.a, j) : 0.0;
+      int64_t jbs = shfl_i64(en.bs, j);
+      bool act = lane < L;
+      uint32_t c = act ? (uint32_t)__ldg(B.col + jbs + lane) : 0u;
+      double bv = (kVal && act) ? __ldg(B.val + jbs + lane) : 0.0;
+      while (true) {
+        const bool more = pend != 0;
+        int nL = 0;
+        double na = 0.0;
+        uint32_t nc = 0u;
+        double nbv = 0.0;
+        if (more) {
+          const int nj = __ffs(pend) - 1;
+          pend &= pend - 1;
+          nL = __shfl_sync(kFull, en.len, nj);
+          if (kVal) na = shfl_f64(en.a, nj);
+          const int64_t nbs = shfl_i64(en.bs, nj);
+          if (lane < nL) {
+            nc = (uint32_t)__ldg(B.col + nbs + lane);
+            if (kVal) nbv = __ldg(B.val + nbs + lane);
+          }
+        }
+        f(act, c, aj * bv);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+        if (!more) break;
+        act = lane < nL;
+        c = nc;
+        bv = nbv;
+        aj = na;
+      }
+      continue;
+    }
     if (kSeq && own_chunks) {
       // this warp owns the chunk: walk its nonempty entries directly
       unsigned pend = __ballot_sync(kFull, en.len > 0);
@@ -294,7 +334,57 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     __syncthreads();
     const int nnz = s_cnt;
     if (threadIdx.x == 0) row_nnz[i] = nnz;
-    if (want_parts && nnz > kPartKeys) {
+    const bool wkind = (ae - as) <= kWPartMaxEntries;  // few a_ik: warp parts
+    if (want_parts && wkind && nnz > kWPartKeys) {
+      // warp parts: rank cuts only, part k = (column of the key of rank k*kWPartKeys, k*kWPartKeys)
+      const int np = (nnz + kWPartKeys - 1) / kWPartKeys;
+      if (threadIdx.x == 0) {
+        const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
+        if (base + np > parts_cap) {
+          atomicAdd(&info->parts_overflow, 1ull);
+          s_warp[0] = -1;
+        } else {
+          s_warp[0] = (int)base;
+          part_off[i] = (int32_t)base;
+          part_n[i] = -np;
+          parts[base] = make_int2(0, 0);
+        }
+      }
+      __syncthreads();
+      const int base = s_warp[0];
+      __syncthreads();
+      if (base >= 0) {
+        const int per = (nwords + THREADS - 1) / THREADS;
+        const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
+        int mine = 0;
+        for (int q = w0; q < w1; ++q) mine += __popc(bm[q]);
+        const int incl = warp_incl_scan(mine);
+        if (lane == 31) s_warp[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+          const int v = lane < NW ? s_warp[lane] : 0;
+          const int vi = warp_incl_scan(v);
+          if (lane < NW) s_warp[lane] = vi - v;
+        }
+        __syncthreads();
+        int cum = s_warp[w] + incl - mine;
+        for (int q = w0; q < w1; ++q) {
+          const uint32_t word = bm[q];
+          const int pc = __popc(word);
+          int nextR = ((cum + kWPartKeys - 1) / kWPartKeys) * kWPartKeys;
+          if (nextR == 0) nextR = kWPartKeys;
+          while (nextR < cum + pc) {
+            uint32_t wv = word;
+            for (int t = 0; t < nextR - cum; ++t) wv &= wv - 1;
+            parts[base + nextR / kWPartKeys] = make_int2(q * 32 + __ffs(wv) - 1, nextR);
+            nextR += kWPartKeys;
+          }
+          cum += pc;
+        }
+      } else if (threadIdx.x == 0) {
+        part_n[i] = 0;
+      }
+    } else if (want_parts && !wkind && nnz > kPartKeys) {
       // each thread owns a contiguous range of words; block scan of popcounts
       const int per = (nwords + THREADS - 1) / THREADS;
       const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
