@@ -176,7 +176,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
   double *vals = s_dyn_f64 + w * TMAX;
   uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + w * TMAX;
   uint32_t *cnt = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + WARPS * TMAX + w * TMAX;
-  const unsigned lt_mask = (1u << lane) - 1u;
   for (int64_t r = int64_t(blockIdx.x) * WARPS + w; r < nrows; r += int64_t(gridDim.x) * WARPS) {
     const int i = rows[r];
     const int64_t rp0 = c_rp[i];
@@ -425,9 +424,10 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // over [lo, lo + kPartWidth), when sorted.  No global atomics.
 // ---------------------------------------------------------------------------
 constexpr int kPartT = 2 * kPartKeys;               // table slots (load <= 1/2)
-constexpr int kSegSmem = 2048;                      // a_ik with smem segment cursors
+constexpr int kSegSmem = 1024;                      // a_ik whose segments live in smem
+constexpr int kSegBytes = 28;                       // sb, se, pre (int32), sabs (int64), a (f64)
 constexpr int kPartRankWords = int(kPartWidth / 32);
-constexpr size_t kPartSmem = size_t(kPartT) * 12 + size_t(kSegSmem) * 8 +
+constexpr size_t kPartSmem = size_t(kPartT) * 12 + size_t(kSegSmem) * kSegBytes + 16 +
                              size_t(kPartRankWords) * 6 +
                              size_t(kPartRankWords / kRankGroup) * 4;
 
@@ -448,24 +448,109 @@ __device__ __forceinline__ int gallop_lb(const int32_t *__restrict__ col, int s,
   return a;
 }
 
+// Per-entry segment arrays of a part (smem or global scratch).
+struct Segs {
+  int32_t *sb, *se, *pre;  // begin / end offsets in the B row; exclusive prefix of lengths
+  int64_t *sabs;           // absolute position of the segment start in B.col / B.val
+  double *a;               // a_ik
+};
+
+__device__ __forceinline__ Segs segs_at(void *base, int cap) {
+  Segs g;
+  g.sabs = reinterpret_cast<int64_t *>(base);
+  g.a = reinterpret_cast<double *>(g.sabs + cap);
+  g.sb = reinterpret_cast<int32_t *>(g.a + cap);
+  g.se = g.sb + cap;
+  g.pre = g.se + cap;  // cap + 1 entries
+  return g;
+}
+
+// Flat enumeration of the products of one part: product p (0 <= p < P) lies
+// in the segment of entry j with pre[j] <= p < pre[j+1].  Rounds [g0, g1) of
+// 32 consecutive products; each lane keeps its owner entry j and advances it
+// (products of a lane increase by 32 per round).  Two rounds in flight.
+template <typename F>
+__device__ __forceinline__ void for_part_rounds(const DevCSR &B, const Segs &sg, int na, int P,
+                                                int g0, int g1, F &&f) {
+  if (g0 >= g1) return;
+  const int lane = lane_id();
+  int p = g0 * 32 + lane;
+  int lo = 0, hi = na;  // owner: last j with pre[j] <= p
+  while (hi - lo > 1) {
+    const int m = (lo + hi) >> 1;
+    if (sg.pre[m] <= p) lo = m; else hi = m;
+  }
+  int j = lo;
+  for (int g = g0; g < g1; g += 2, p += 64) {
+    const bool act0 = p < P;
+    const bool act1 = (g + 1 < g1) && (p + 32 < P);
+    uint32_t c0 = 0u, c1 = 0u;
+    double v0 = 0.0, v1 = 0.0;
+    if (act0) {
+      while (j + 1 < na && sg.pre[j + 1] <= p) ++j;
+      const int64_t q = sg.sabs[j] + (p - sg.pre[j]);
+      c0 = (uint32_t)__ldg(B.col + q);
+      v0 = sg.a[j] * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+    }
+    if (act1) {
+      while (j + 1 < na && sg.pre[j + 1] <= p + 32) ++j;
+      const int64_t q = sg.sabs[j] + (p + 32 - sg.pre[j]);
+      c1 = (uint32_t)__ldg(B.col + q);
+      v1 = sg.a[j] * __ldg(B.val + q);
+    }
+    f(act0, c0, v0);
+    f(act1, c1, v1);
+  }
+}
+
+__device__ __forceinline__ int block_excl_scan_int(int v, int *s_warp, int *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int incl = warp_incl_scan(v);
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int x = lane < NW ? s_warp[lane] : 0;
+    const int xi = warp_incl_scan(x);
+    if (lane < NW) s_warp[lane] = xi - x;
+    if (lane == 31) s_warp[32] = xi;
+  }
+  __syncthreads();
+  const int r = s_warp[w] + incl - v;
+  *total = s_warp[32];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// G tier, column-range BLOCK parts (rows with many a_ik, B rows sorted; parts
+// from the BM symbolic): one block per row at a time (dynamic row queue), the
+// row's parts in column order.  Per part [lo, hi): every a_ik's B row
+// contributes the segment of columns in [lo, hi) -- it starts where the
+// previous part's segment ended and ends at the first column >= hi (galloping
+// search); one block scan of the segment lengths makes the part's products a
+// flat list, cut into equal contiguous ranges of 32-product rounds, one per
+// warp.  The part's <= kPartKeys keys are accumulated in an smem hash table
+// and emitted at C_row_ptr[i] + (keys of the row before lo) -- in order, by a
+// bitmap rank over [lo, lo + kPartWidth), when sorted.  No global atomics.
+// ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_num_part(
     const int32_t *__restrict__ rows, int64_t nrows, DevCSR A, DevCSR B,
     const int64_t *__restrict__ flop, const int64_t *__restrict__ c_rp,
     int32_t *__restrict__ c_col, double *__restrict__ c_val, int sorted,
     const int2 *__restrict__ parts, const int32_t *__restrict__ part_off,
-    const int32_t *__restrict__ part_n, int32_t *__restrict__ seg_scratch, int64_t seg_stride,
+    const int32_t *__restrict__ part_n, char *__restrict__ seg_scratch, int64_t seg_cap,
     unsigned long long *row_counter) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_cnt;
+  __shared__ int s_warp[33];
   __shared__ long long s_row;
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5;
   double *vals = s_dyn_f64;
   uint32_t *keys = reinterpret_cast<uint32_t *>(vals + kPartT);
-  int32_t *seg_a = reinterpret_cast<int32_t *>(keys + kPartT);
-  int32_t *seg_b = seg_a + kSegSmem;
-  uint32_t *bm = reinterpret_cast<uint32_t *>(seg_b + kSegSmem);
+  char *seg_smem = reinterpret_cast<char *>(keys + kPartT);
+  uint32_t *bm = reinterpret_cast<uint32_t *>(seg_smem + size_t(kSegSmem) * kSegBytes + 16);
   uint16_t *wpre = reinterpret_cast<uint16_t *>(bm + kPartRankWords);
   int *gpre = reinterpret_cast<int *>(wpre + kPartRankWords);
   while (true) {
@@ -476,73 +561,85 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
     const int i = rows[r];
     const int64_t rp0 = c_rp[i];
     const int nnz = (int)(c_rp[i + 1] - rp0);
-    const int64_t as = A.rp[i], ae = A.rp[i + 1];
-    const int na = (int)(ae - as);
+    const int64_t as = A.rp[i];
+    const int na = (int)(A.rp[i + 1] - as);
     const int np = part_n[i];
     const int2 *pr = parts + part_off[i];
-    int32_t *sb = seg_a, *se = seg_b;  // segment begin / end (offsets in each B row)
-    if (na > kSegSmem) {
-      sb = seg_scratch + int64_t(blockIdx.x) * seg_stride;
-      se = sb + seg_stride / 2;
+    Segs sg = na <= kSegSmem ? segs_at(seg_smem, kSegSmem)
+                             : segs_at(seg_scratch + int64_t(blockIdx.x) * seg_cap * kSegBytes,
+                                       (int)seg_cap);
+    for (int j = threadIdx.x; j < na; j += THREADS) {
+      sg.sb[j] = 0;
+      const int k = __ldg(A.col + as + j);
+      sg.sabs[j] = __ldg(B.rp + k);  // B row start (the segment offset is added per part)
+      sg.a[j] = __ldg(A.val + as + j);
     }
-    for (int j = threadIdx.x; j < na; j += THREADS) sb[j] = 0;
-    const bool seq = flop[i] >= int64_t(kSeqMinLen) * na * (np > 0 ? np : 1);
     __syncthreads();
+    const int per = (na + THREADS - 1) / THREADS;  // entries per thread for the scan
     for (int p = 0; p < np; ++p) {
-      const int2 P = pr[p];
+      const int2 Pp = pr[p];
       const int64_t hi = p + 1 < np ? int64_t(pr[p + 1].x) : B.ncols;
-      const int cnt = (p + 1 < np ? pr[p + 1].y : nnz) - P.y;
+      const int cnt = (p + 1 < np ? pr[p + 1].y : nnz) - Pp.y;
       const int logT = num_log2(cnt);
       const int T = 1 << logT;
       for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
+      // segment ends and lengths (thread owns entries [t*per, t*per + per))
+      int mine = 0;
+      for (int j = threadIdx.x * per; j < na && j < (threadIdx.x + 1) * per; ++j) {
+        const int k = __ldg(A.col + as + j);
+        const int len = (int)(__ldg(B.rp + k + 1) - __ldg(B.rp + k));
+        const int64_t bs0 = __ldg(B.rp + k);
+        const int e = p + 1 == np ? len : gallop_lb(B.col + bs0, sg.sb[j], len, hi);
+        sg.se[j] = e;
+        mine += e - sg.sb[j];
+      }
+      int P;
+      int ex = block_excl_scan_int(mine, s_warp, &P);
+      for (int j = threadIdx.x * per; j < na && j < (threadIdx.x + 1) * per; ++j) {
+        sg.pre[j] = ex;
+        ex += sg.se[j] - sg.sb[j];
+      }
+      if (threadIdx.x == 0) {
+        sg.pre[na] = P;
+        s_cnt = 0;
+      }
+      __syncthreads();
+      // absolute segment starts for this part
       for (int j = threadIdx.x; j < na; j += THREADS) {
         const int k = __ldg(A.col + as + j);
-        const int64_t bs = __ldg(B.rp + k);
-        const int len = (int)(__ldg(B.rp + k + 1) - bs);
-        se[j] = p + 1 == np ? len : gallop_lb(B.col + bs, sb[j], len, hi);
+        sg.sabs[j] = __ldg(B.rp + k) + sg.sb[j];
       }
-      if (threadIdx.x == 0) s_cnt = 0;
       __syncthreads();
-      auto entry = [&](int64_t j) {
-        const int k = __ldg(A.col + as + j);
-        Entry en;
-        en.bs = __ldg(B.rp + k) + sb[j];
-        en.len = se[j] - sb[j];
-        en.a = __ldg(A.val + as + j);
-        return en;
-      };
-      auto acc = [&](bool act, uint32_t c, double v) {
-        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);  // c_ij <- c_ij + value
-      };
-      if (seq) for_entries<true, true>(B, na, w, NW, entry, acc);
-      else for_entries<false, true>(B, na, w, NW, entry, acc);
+      const int R = (P + 31) >> 5;
+      for_part_rounds(B, sg, na, P, (int)((int64_t)R * w / NW), (int)((int64_t)R * (w + 1) / NW),
+                      [&](bool act, uint32_t c, double v) {
+                        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);  // c_ij += value
+                      });
       __syncthreads();
       if (!sorted) {
-        block_emit_unsorted(keys, vals, T, rp0 + P.y, c_col, c_val, &s_cnt);
+        block_emit_unsorted(keys, vals, T, rp0 + Pp.y, c_col, c_val, &s_cnt);
       } else {
-        const int64_t width = (hi - P.x) < kPartWidth ? (hi - P.x) : kPartWidth;
-        block_rank_emit(keys, vals, T, P.x, width, bm, wpre, gpre, &s_cnt, rp0 + P.y, c_col,
+        const int64_t width = (hi - Pp.x) < kPartWidth ? (hi - Pp.x) : kPartWidth;
+        block_rank_emit(keys, vals, T, Pp.x, width, bm, wpre, gpre, &s_cnt, rp0 + Pp.y, c_col,
                         c_val);
       }
-      int32_t *t = sb;  // the next part's segments start where these ended
-      sb = se;
-      se = t;
+      for (int j = threadIdx.x; j < na; j += THREADS) sg.sb[j] = sg.se[j];
       __syncthreads();
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// G tier, warp parts (rows with <= kWPartMaxEntries a_ik, B rows sorted):
+// G tier, WARP parts (rows with <= kWPartMaxEntries a_ik, B rows sorted):
 // one warp per row at a time (dynamic row queue), the row's parts of
 // kWPartKeys keys in column order, each accumulated in a warp-private smem
-// table (plain fp64 read-modify-write, as in the W tier) and emitted at
-// C_row_ptr[i] + (keys of the row before the part), sorted by the warp
-// bucket sort when requested.  B-row segments of a part: galloping search
-// from where the previous part's segment ended.
+// table (plain fp64 read-modify-write; lanes sharing a key in a round found
+// with __match_any_sync) and emitted at C_row_ptr[i] + (keys before the part)
+// -- sorted by the warp bucket sort when requested.  Segments and the flat
+// product list as in the block parts, per warp.
 // ---------------------------------------------------------------------------
 constexpr int kWPartT = 2 * kWPartKeys;
-constexpr size_t kWPartSmemPerWarp = size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * 8;
+constexpr size_t kWPartSmemPerWarp = size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * kSegBytes + 8;
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
@@ -553,13 +650,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
     const int32_t *__restrict__ part_n, unsigned long long *row_counter) {
   extern __shared__ double s_dyn_f64[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *vals = s_dyn_f64 + w * kWPartT;
-  uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * kWPartT) + w * kWPartT;
-  uint32_t *cnt = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * kWPartT) + WARPS * kWPartT +
-                  w * kWPartT;
-  int32_t *sa = reinterpret_cast<int32_t *>(cnt + (WARPS - w) * kWPartT) +
-                w * 2 * kWPartMaxEntries;
-  int32_t *sbv = sa + kWPartMaxEntries;
+  char *base = reinterpret_cast<char *>(s_dyn_f64) + size_t(w) * kWPartSmemPerWarp;
+  double *vals = reinterpret_cast<double *>(base);
+  uint32_t *keys = reinterpret_cast<uint32_t *>(vals + kWPartT);
+  uint32_t *cnt = keys + kWPartT;
+  Segs sg = segs_at(cnt + kWPartT, kWPartMaxEntries);
   while (true) {
     long long r = 0;
     if (lane == 0) r = (long long)atomicAdd(row_counter, 1ull);
@@ -572,53 +667,50 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
     const int na = (int)(A.rp[i + 1] - as);
     const int np = -part_n[i];
     const int2 *pr = parts + part_off[i];
-    int32_t *sb = sa, *se = sbv;
-    for (int j = lane; j < na; j += 32) sb[j] = 0;
-    const bool seq = flop[i] >= int64_t(kSeqMinLen) * na * np;
+    for (int j = lane; j < na; j += 32) {
+      sg.sb[j] = 0;
+      sg.a[j] = __ldg(A.val + as + j);
+    }
     __syncwarp();
     for (int p = 0; p < np; ++p) {
-      const int2 P = pr[p];
+      const int2 Pp = pr[p];
       const int64_t hi = p + 1 < np ? int64_t(pr[p + 1].x) : B.ncols;
-      const int cntp = (p + 1 < np ? pr[p + 1].y : nnz) - P.y;
+      const int cntp = (p + 1 < np ? pr[p + 1].y : nnz) - Pp.y;
       const int logT = num_log2(cntp);
       const int T = 1 << logT;
       for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
-      for (int j = lane; j < na; j += 32) {
-        const int k = __ldg(A.col + as + j);
-        const int64_t bs = __ldg(B.rp + k);
-        const int len = (int)(__ldg(B.rp + k + 1) - bs);
-        se[j] = p + 1 == np ? len : gallop_lb(B.col + bs, sb[j], len, hi);
+      int carry = 0;
+      for (int j0 = 0; j0 < na; j0 += 32) {  // segment ends, exclusive prefix of lengths
+        const int j = j0 + lane;
+        int L = 0;
+        if (j < na) {
+          const int k = __ldg(A.col + as + j);
+          const int64_t bs0 = __ldg(B.rp + k);
+          const int len = (int)(__ldg(B.rp + k + 1) - bs0);
+          const int e = p + 1 == np ? len : gallop_lb(B.col + bs0, sg.sb[j], len, hi);
+          sg.se[j] = e;
+          sg.sabs[j] = bs0 + sg.sb[j];
+          L = e - sg.sb[j];
+        }
+        const int incl = warp_incl_scan(L);
+        if (j < na) sg.pre[j] = carry + incl - L;
+        carry += __shfl_sync(kFull, incl, 31);
       }
+      if (lane == 0) sg.pre[na] = carry;
       __syncwarp();
-      auto entry = [&](int64_t j) {
-        const int k = __ldg(A.col + as + j);
-        Entry en;
-        en.bs = __ldg(B.rp + k) + sb[j];
-        en.len = se[j] - sb[j];
-        en.a = __ldg(A.val + as + j);
-        return en;
-      };
-      if (seq) {
-        for_entries<true, true>(B, na, 0, 1, entry, [&](bool act, uint32_t c, double v) {
-          if (act) vals[num_probe(keys, c, logT)] += v;  // c_ij <- c_ij + value (l.8)
-          __syncwarp();
-        });
-      } else {
-        for_entries<false, true>(B, na, 0, 1, entry, [&](bool act, uint32_t c, double v) {
-          uint32_t slot = 0;
-          if (act) slot = num_probe(keys, c, logT);
-          const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
-          if (act) {
-            if (__popc(grp) == 1) vals[slot] += v;
-            else atomicAdd(vals + slot, v);
-          }
-          __syncwarp();
-        });
-      }
-      warp_emit(keys, vals, cnt, T, logT, cntp, rp0 + P.y, c_col, c_val, sorted);
-      int32_t *t = sb;
-      sb = se;
-      se = t;
+      const int P = carry;
+      for_part_rounds(B, sg, na, P, 0, (P + 31) >> 5, [&](bool act, uint32_t c, double v) {
+        uint32_t slot = 0;
+        if (act) slot = num_probe(keys, c, logT);
+        const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
+        if (act) {
+          if (__popc(grp) == 1) vals[slot] += v;  // c_ij <- c_ij + value (l.8)
+          else atomicAdd(vals + slot, v);
+        }
+        __syncwarp();
+      });
+      warp_emit(keys, vals, cnt, T, logT, cntp, rp0 + Pp.y, c_col, c_val, sorted);
+      for (int j = lane; j < na; j += 32) sg.sb[j] = sg.se[j];
       __syncwarp();
     }
   }

@@ -105,7 +105,7 @@ constexpr int kMaxPartsPerRow = 512;  // >= kBitmapMaxCols / kPartKeys + kBitmap
 // Rows with few a_ik are cut into small WARP parts instead (one warp per
 // part, warp-private table): rank cuts every kWPartKeys keys.
 constexpr int kWPartKeys = 256;
-constexpr int kWPartMaxEntries = 128;
+constexpr int kWPartMaxEntries = 64;
 
 
 __device__ __forceinline__ int num_log2(int64_t nnz) {

@@ -281,7 +281,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_part<1024>, kPartSmem) == SPG_OK &&
-         set_smem(c, k_num_wpart<8>, 8 * kWPartSmemPerWarp) == SPG_OK &&
+         set_smem(c, k_num_wpart<4>, 4 * kWPartSmemPerWarp) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
   if (!ok) {
@@ -538,15 +538,15 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   const int32_t *rows = (const int32_t *)c->rows_num.p;
   const int64_t *flop = (const int64_t *)c->flop.p;
   // G-tier slab: keys + vals of lowest 2^n >= 2 * max nnz(c_i) per block
-  int64_t g_grid = 0, slabT = 0, seg_stride = 0;
+  int64_t g_grid = 0, slabT = 0, seg_cap = 0;
   const bool use_parts = c->plan_parts && h.b_unsorted == 0 && h.parts_overflow == 0;
   if (h.num_count[NB_G]) {
     g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
     if (use_parts) {
       SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));
       if ((int64_t)h.max_arow > kSegSmem) {
-        seg_stride = 2 * (int64_t)h.max_arow;
-        if ((st = buf_ensure(c, c->seg, size_t(g_grid) * size_t(seg_stride) * 4, s)) != SPG_OK)
+        seg_cap = (int64_t)h.max_arow + 1;
+        if ((st = buf_ensure(c, c->seg, size_t(g_grid) * size_t(seg_cap) * kSegBytes, s)) != SPG_OK)
           return st;
       }
     } else {
@@ -596,11 +596,11 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
         }
       SPG_LAUNCHED(c, "k_num_block");
     } else if (bin == NB_GW) {  // warp parts
-      const int64_t grid = std::min<int64_t>(ceil_div(n, 8), int64_t(c->num_sms) * 3);
+      const int64_t grid = std::min<int64_t>(ceil_div(n, 4), int64_t(c->num_sms) * 5);
       SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter_w, 0, 8, ss));
       {
-        ProfScope _ps(c, ss, "k_num_wpart<8>");
-        k_num_wpart<8><<<(unsigned)grid, 256, 8 * kWPartSmemPerWarp, ss>>>(
+        ProfScope _ps(c, ss, "k_num_wpart<4>");
+        k_num_wpart<4><<<(unsigned)grid, 128, 4 * kWPartSmemPerWarp, ss>>>(
             rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
             (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p,
             &((PlanInfo *)c->info.p)->row_counter_w);
@@ -611,8 +611,8 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
         ProfScope _ps(c, ss, "k_num_part<1024>");
         k_num_part<1024><<<(unsigned)g_grid, 1024, kPartSmem, ss>>>(
             rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
-            (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p, (int32_t *)c->seg.p,
-            seg_stride, &((PlanInfo *)c->info.p)->row_counter);
+            (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p, (char *)c->seg.p,
+            seg_cap, &((PlanInfo *)c->info.p)->row_counter);
       }
       SPG_LAUNCHED(c, "k_num_part");
     } else {  // NB_G
