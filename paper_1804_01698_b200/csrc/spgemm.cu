@@ -545,7 +545,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
     if (use_parts) {
       SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));
       if ((int64_t)h.max_arow > kSegSmem) {
-        seg_cap = (int64_t)h.max_arow + 1;
+        seg_cap = ((int64_t)h.max_arow + 8) & ~int64_t(7);  // keeps every block's int64 arrays aligned
         if ((st = buf_ensure(c, c->seg, size_t(g_grid) * size_t(seg_cap) * kSegBytes, s)) != SPG_OK)
           return st;
       }
