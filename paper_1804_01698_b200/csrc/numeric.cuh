@@ -9,7 +9,13 @@
 
 namespace spg {
 
-// Probe for key c, inserting it if absent; returns its slot.
+// Shared-memory tables: chunked probing (probe_chunk).
+__device__ __forceinline__ uint32_t num_probe_smem(uint32_t *keys, uint32_t c, int logT) {
+  bool isnew = false;
+  return probe_chunk(keys, c, logT, &isnew);
+}
+
+// Probe for key c, inserting it if absent; returns its slot (global tables).
 __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int logT) {
   const uint32_t mask = (1u << logT) - 1u;
   uint32_t h = hash_slot(c, logT);
@@ -188,13 +194,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
     if (use_seq(flop[i], ae - as)) {
       // keys of a round are distinct: plain read-modify-write of the value
       for_row<true, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
-        if (act) vals[num_probe(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
+        if (act) vals[num_probe_smem(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
         __syncwarp();
       });
     } else {
       for_row<false, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         uint32_t slot = 0;
-        if (act) slot = num_probe(keys, c, logT);
+        if (act) slot = num_probe_smem(keys, c, logT);
         const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
         if (act) {
           if (__popc(grp) == 1) vals[slot] += v;   // c_ij <- c_ij + value (l.8)
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
       auto acc = [&](bool act, uint32_t c, double v) {
-        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
+        if (act) atomicAdd(vals + num_probe_smem(keys, c, logT), v);
       };
       if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc);
       else for_row<false, true>(A, B, as, ae, w, NW, acc);
@@ -613,7 +619,11 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
       const int R = (P + 31) >> 5;
       for_part_rounds(B, sg, na, P, (int)((int64_t)R * w / NW), (int)((int64_t)R * (w + 1) / NW),
                       [&](bool act, uint32_t c, double v) {
-                        if (act) atomicAdd(vals + num_probe(keys, c, logT), v);  // c_ij += value
+#ifdef SPG_EXPERIMENT_NOATOMIC
+                        if (act) vals[num_probe_smem(keys, c, logT)] += v;  // timing experiment only
+#else
+                        if (act) atomicAdd(vals + num_probe_smem(keys, c, logT), v);  // c_ij += value
+#endif
                       });
       __syncthreads();
       if (!sorted) {
@@ -701,7 +711,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
       const int P = carry;
       for_part_rounds(B, sg, na, P, 0, (P + 31) >> 5, [&](bool act, uint32_t c, double v) {
         uint32_t slot = 0;
-        if (act) slot = num_probe(keys, c, logT);
+        if (act) slot = num_probe_smem(keys, c, logT);
         const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
         if (act) {
           if (__popc(grp) == 1) vals[slot] += v;  // c_ij <- c_ij + value (l.8)

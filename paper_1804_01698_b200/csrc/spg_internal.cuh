@@ -136,6 +136,51 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t c, int logT) {
   return (c * kHashMul) >> (32 - logT);
 }
 
+// ---------------------------------------------------------------------------
+// HashVector-style probing of SHARED-memory tables (§4.2.2, P:329-338:
+// "the hash indicates the identifier of target chunk in hash table"; compare
+// the key against the whole chunk; "new element is pushed ... in order from
+// the beginning" of the chunk; "when the chunk is occupied with other keys,
+// the next chunk is to be checked in accordance with linear probing").  A
+// chunk is kChunk = 4 consecutive 32-bit slots read with one 128-bit shared
+// load, so a lane resolves most keys in one step and the warp's divergent
+// probe loop is short.
+// ---------------------------------------------------------------------------
+constexpr int kChunkLog = 2;
+
+__device__ __forceinline__ uint4 lds_volatile_v4(const uint32_t *p) {
+  uint4 r;
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(a));
+  return r;
+}
+
+// Find or insert key c in smem table keys[0, 2^logT); returns the slot and
+// sets *isnew when this call inserted c.
+__device__ __forceinline__ uint32_t probe_chunk(uint32_t *keys, uint32_t c, int logT,
+                                                bool *isnew) {
+  const uint32_t cmask = (1u << (logT - kChunkLog)) - 1u;
+  uint32_t ch = (c * kHashMul) >> (32 - (logT - kChunkLog));
+  while (true) {
+    const uint32_t b = ch << kChunkLog;
+    const uint4 k = lds_volatile_v4(keys + b);
+    if (k.x == c) return b;
+    if (k.y == c) return b + 1;
+    if (k.z == c) return b + 2;
+    if (k.w == c) return b + 3;
+    const int e = k.x == kEmpty ? 0 : k.y == kEmpty ? 1 : k.z == kEmpty ? 2 : k.w == kEmpty ? 3 : 4;
+    if (e < 4) {
+      const uint32_t old = atomicCAS(keys + b + e, kEmpty, c);
+      if (old == kEmpty) { *isnew = true; return b + e; }
+      if (old == c) return b + e;
+      continue;  // lost the slot to another key: re-read this chunk
+    }
+    ch = (ch + 1u) & cmask;  // chunk full: next chunk (linear probing)
+  }
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
 template <typename T>

@@ -28,6 +28,13 @@ __device__ __forceinline__ int sym_insert(uint32_t *tab, uint32_t c, int logT) {
   }
 }
 
+// Same, for a shared-memory table (chunked probing).
+__device__ __forceinline__ int sym_insert_smem(uint32_t *tab, uint32_t c, int logT) {
+  bool isnew = false;
+  probe_chunk(tab, c, logT, &isnew);
+  return isnew ? 1 : 0;
+}
+
 // Bitmap variant for very long rows: column c -> bit c of an ncols-bit set.
 __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
   const uint32_t bit = 1u << (c & 31u);
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) cnt += sym_insert(tab, c, logT);
+      if (act) cnt += sym_insert_smem(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, 0, 1, ins);
     else for_row<false, false>(A, B, as, ae, 0, 1, ins);
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) cnt += sym_insert(tab, c, logT);
+      if (act) cnt += sym_insert_smem(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
     else for_row<false, false>(A, B, as, ae, w, NW, ins);
