@@ -649,7 +649,8 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
 // product list as in the block parts, per warp.
 // ---------------------------------------------------------------------------
 constexpr int kWPartT = 2 * kWPartKeys;
-constexpr size_t kWPartSmemPerWarp = size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * kSegBytes + 8;
+constexpr size_t kWPartSmemPerWarp =  // multiple of 16 B: 128-bit chunk loads stay aligned
+    (size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * kSegBytes + 8 + 15) & ~size_t(15);
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
