@@ -368,6 +368,67 @@ __device__ __forceinline__ int block_rank_emit(const uint32_t *keys, const doubl
   return tot;
 }
 
+// Emit of a part's table from its insertion list slot_of[0, n): unsorted =
+// list order (coalesced stores); sorted = bitmap rank over [cbase, cbase +
+// nbits), nbits <= 32 * words of bm.
+__device__ __forceinline__ void block_list_emit(const uint32_t *keys, const double *vals,
+                                                const uint16_t *slot_of, int n, int64_t cbase,
+                                                int64_t nbits, uint32_t *bm, uint16_t *wpre,
+                                                int *gpre, int *s_tot, int64_t out_base,
+                                                int32_t *__restrict__ c_col,
+                                                double *__restrict__ c_val, int sorted) {
+  if (!sorted) {
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+      const int s = slot_of[p];
+      c_col[out_base + p] = (int32_t)keys[s];
+      c_val[out_base + p] = vals[s];
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int nwords = (int)((nbits + 31) >> 5);
+  for (int q = threadIdx.x; q < nwords; q += blockDim.x) bm[q] = 0u;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const uint32_t off = (uint32_t)(int64_t(keys[slot_of[p]]) - cbase);
+    atomicOr(bm + (off >> 5), 1u << (off & 31u));
+  }
+  __syncthreads();
+  const int ngroups = (nwords + kRankGroup - 1) / kRankGroup;
+  for (int g = w; g < ngroups; g += NW) {
+    const int w0 = g * kRankGroup + 2 * lane;
+    const int c0 = w0 < nwords ? __popc(bm[w0]) : 0;
+    const int c1 = w0 + 1 < nwords ? __popc(bm[w0 + 1]) : 0;
+    const int incl = warp_incl_scan(c0 + c1);
+    const int ex = incl - c0 - c1;
+    if (w0 < nwords) wpre[w0] = (uint16_t)ex;
+    if (w0 + 1 < nwords) wpre[w0 + 1] = (uint16_t)(ex + c0);
+    if (lane == 31) gpre[g] = incl;
+  }
+  __syncthreads();
+  if (w == 0) {
+    int carry = 0;
+    for (int g0 = 0; g0 < ngroups; g0 += 32) {
+      const int g = g0 + lane;
+      const int v = g < ngroups ? gpre[g] : 0;
+      const int incl = warp_incl_scan(v);
+      if (g < ngroups) gpre[g] = carry + incl - v;
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const int s = slot_of[p];
+    const uint32_t k = keys[s];
+    const uint32_t off = (uint32_t)(int64_t(k) - cbase);
+    const uint32_t wd = off >> 5;
+    const int pos = gpre[wd / kRankGroup] + wpre[wd] + __popc(bm[wd] & ((1u << (off & 31u)) - 1u));
+    c_col[out_base + pos] = (int32_t)k;
+    c_val[out_base + pos] = vals[s];
+  }
+  (void)s_tot;
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restrict__ rows,
                                                         int64_t nrows, DevCSR A, DevCSR B,
@@ -435,7 +496,7 @@ constexpr int kSegBytes = 28;                       // sb, se, pre (int32), sabs
 constexpr int kPartRankWords = int(kPartWidth / 32);
 constexpr size_t kPartSmem = size_t(kPartT) * 12 + size_t(kSegSmem) * kSegBytes + 16 +
                              size_t(kPartRankWords) * 6 +
-                             size_t(kPartRankWords / kRankGroup) * 4;
+                             size_t(kPartRankWords / kRankGroup) * 4 + size_t(kPartKeys) * 2;
 
 // first q in [s, len) with col[q] >= hi (col sorted), searching from s
 __device__ __forceinline__ int gallop_lb(const int32_t *__restrict__ col, int s, int len,
@@ -559,6 +620,8 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
   uint32_t *bm = reinterpret_cast<uint32_t *>(seg_smem + size_t(kSegSmem) * kSegBytes + 16);
   uint16_t *wpre = reinterpret_cast<uint16_t *>(bm + kPartRankWords);
   int *gpre = reinterpret_cast<int *>(wpre + kPartRankWords);
+  uint16_t *slot_of = reinterpret_cast<uint16_t *>(gpre + kPartRankWords / kRankGroup);
+  const int lane = threadIdx.x & 31;
   while (true) {
     if (threadIdx.x == 0) s_row = (long long)atomicAdd(row_counter, 1ull);
     __syncthreads();
@@ -597,10 +660,11 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
         const int64_t bs0 = __ldg(B.rp + k);
         const int e = p + 1 == np ? len : gallop_lb(B.col + bs0, sg.sb[j], len, hi);
         sg.se[j] = e;
+        sg.sabs[j] = bs0 + sg.sb[j];  // absolute segment start for this part
         mine += e - sg.sb[j];
       }
       int P;
-      int ex = block_excl_scan_int(mine, s_warp, &P);
+      int ex = block_excl_scan_int(mine, s_warp, &P);  // (contains the barriers)
       for (int j = threadIdx.x * per; j < na && j < (threadIdx.x + 1) * per; ++j) {
         sg.pre[j] = ex;
         ex += sg.se[j] - sg.sb[j];
@@ -610,30 +674,30 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
         s_cnt = 0;
       }
       __syncthreads();
-      // absolute segment starts for this part
-      for (int j = threadIdx.x; j < na; j += THREADS) {
-        const int k = __ldg(A.col + as + j);
-        sg.sabs[j] = __ldg(B.rp + k) + sg.sb[j];
-      }
-      __syncthreads();
       const int R = (P + 31) >> 5;
+      // accumulate; newly inserted keys are appended to the insertion list
       for_part_rounds(B, sg, na, P, (int)((int64_t)R * w / NW), (int)((int64_t)R * (w + 1) / NW),
                       [&](bool act, uint32_t c, double v) {
-#ifdef SPG_EXPERIMENT_NOATOMIC
-                        if (act) vals[num_probe_smem(keys, c, logT)] += v;  // timing experiment only
-#else
-                        if (act) atomicAdd(vals + num_probe_smem(keys, c, logT), v);  // c_ij += value
-#endif
+                        bool isnew = false;
+                        uint32_t slot = 0;
+                        if (act) {
+                          slot = probe_chunk(keys, c, logT, &isnew);
+                          atomicAdd(vals + slot, v);  // c_ij <- c_ij + value (l.8)
+                        }
+                        const unsigned m = __ballot_sync(kFull, isnew);
+                        if (m) {
+                          const int leader = __ffs(m) - 1;
+                          int base = 0;
+                          if (lane == leader) base = atomicAdd(&s_cnt, __popc(m));
+                          base = __shfl_sync(kFull, base, leader);
+                          if (isnew) slot_of[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)slot;
+                        }
                       });
-      __syncthreads();
-      if (!sorted) {
-        block_emit_unsorted(keys, vals, T, rp0 + Pp.y, c_col, c_val, &s_cnt);
-      } else {
-        const int64_t width = (hi - Pp.x) < kPartWidth ? (hi - Pp.x) : kPartWidth;
-        block_rank_emit(keys, vals, T, Pp.x, width, bm, wpre, gpre, &s_cnt, rp0 + Pp.y, c_col,
-                        c_val);
-      }
       for (int j = threadIdx.x; j < na; j += THREADS) sg.sb[j] = sg.se[j];
+      __syncthreads();
+      const int64_t width = (hi - Pp.x) < kPartWidth ? (hi - Pp.x) : kPartWidth;
+      block_list_emit(keys, vals, slot_of, cnt, Pp.x, width, bm, wpre, gpre, &s_cnt, rp0 + Pp.y,
+                      c_col, c_val, sorted);
       __syncthreads();
     }
   }
