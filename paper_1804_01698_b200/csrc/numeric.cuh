@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // over [lo, lo + kPartWidth), when sorted.  No global atomics.
 // ---------------------------------------------------------------------------
 constexpr int kPartT = 2 * kPartKeys;               // table slots (load <= 1/2)
-constexpr int kSegSmem = 256;                       // a_ik whose segments live in smem
+constexpr int kSegSmem = 1024;                      // a_ik whose segments live in smem
 constexpr int kSegBytes = 28;                       // sb, se, pre (int32), sabs (int64), a (f64)
 constexpr int kPartRankWords = int(kPartWidth / 32);
 constexpr size_t kPartSmem = size_t(kPartT) * 12 + size_t(kSegSmem) * kSegBytes + 16 +

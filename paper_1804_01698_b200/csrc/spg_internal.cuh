@@ -83,7 +83,7 @@ __device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {
 // Rows whose table would exceed 8192 slots use the smem BITMAP tier when the
 // column space fits one (it also cuts the row into column-range parts for the
 // numeric phase); otherwise the larger smem hash tables / global hash.
-constexpr int64_t kBitmapMaxCols = int64_t(196 * 1024) * 8;  // 196 KB of bits
+constexpr int64_t kBitmapMaxCols = int64_t(200 * 1024) * 8;  // 200 KB of bits
 
 __device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols) {
   if (flop == 0) return SB_SKIP;
@@ -98,11 +98,10 @@ __device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols) {
 
 // Column-range parts of a long row (numeric G tier): at most kPartKeys keys
 // and at most kPartWidth columns each.
-constexpr int kPartKeys = 1024;
-constexpr int kPartWidthLog = 16;
+constexpr int kPartKeys = 4096;
+constexpr int kPartWidthLog = 18;
 constexpr int64_t kPartWidth = int64_t(1) << kPartWidthLog;
-constexpr int kMaxRankCuts = int(kBitmapMaxCols / kPartKeys) + 2;
-constexpr int kMaxWidthCuts = int(kBitmapMaxCols / kPartWidth) + 2;
+constexpr int kMaxPartsPerRow = 512;  // >= kBitmapMaxCols / kPartKeys + kBitmapMaxCols / kPartWidth + 2
 // Rows with few a_ik are cut into small WARP parts instead (one warp per
 // part, warp-private table): rank cuts every kWPartKeys keys.
 constexpr int kWPartKeys = 256;

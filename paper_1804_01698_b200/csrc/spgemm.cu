@@ -280,7 +280,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_block<512>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
-         set_smem(c, k_num_part<256>, kPartSmem) == SPG_OK &&
+         set_smem(c, k_num_part<1024>, kPartSmem) == SPG_OK &&
          set_smem(c, k_num_wpart<4>, 4 * kWPartSmemPerWarp) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
@@ -543,7 +543,6 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   if (h.num_count[NB_G]) {
     g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
     if (use_parts) {
-      g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms) * 4);
       SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));
       if ((int64_t)h.max_arow > kSegSmem) {
         seg_cap = ((int64_t)h.max_arow + 8) & ~int64_t(7);  // keeps every block's int64 arrays aligned
@@ -609,8 +608,8 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       SPG_LAUNCHED(c, "k_num_wpart");
     } else if (use_parts) {  // NB_G with column-range parts
       {
-        ProfScope _ps(c, ss, "k_num_part<256>");
-        k_num_part<256><<<(unsigned)g_grid, 256, kPartSmem, ss>>>(
+        ProfScope _ps(c, ss, "k_num_part<1024>");
+        k_num_part<1024><<<(unsigned)g_grid, 1024, kPartSmem, ss>>>(
             rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
             (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p, (char *)c->seg.p,
             seg_cap, &((PlanInfo *)c->info.p)->row_counter);

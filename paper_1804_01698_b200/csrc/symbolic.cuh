@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt;
   __shared__ int s_warp[THREADS / 32];
-  __shared__ int2 s_rank[kMaxRankCuts];    // rank cuts (col, cum)
-  __shared__ int2 s_width[kMaxWidthCuts];  // width cuts (col, cum)
+  __shared__ int2 s_rank[kMaxPartsPerRow];   // rank cuts (col, cum)
+  __shared__ int2 s_width[kMaxPartsPerRow];  // width cuts (col, cum)
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwords = (int)((B.ncols + 31) >> 5);
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
         const int pc = __popc(word);
         if (q > 0 && ((int64_t(q) * 32) & (kPartWidth - 1)) == 0) {  // width cut
           const int k = (int)((int64_t(q) * 32) >> kPartWidthLog);
-          if (k < kMaxWidthCuts) s_width[k] = make_int2(q * 32, cum);
+          if (k < kMaxPartsPerRow) s_width[k] = make_int2(q * 32, cum);
         }
         int nextR = ((cum + kPartKeys - 1) / kPartKeys) * kPartKeys;  // rank cuts
         if (nextR == 0) nextR = kPartKeys;
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
           uint32_t wv = word;
           for (int t = 0; t < nextR - cum; ++t) wv &= wv - 1;  // drop lower set bits
           const int k = nextR / kPartKeys;
-          if (k < kMaxRankCuts) s_rank[k] = make_int2(q * 32 + __ffs(wv) - 1, nextR);
+          if (k < kMaxPartsPerRow) s_rank[k] = make_int2(q * 32 + __ffs(wv) - 1, nextR);
           nextR += kPartKeys;
         }
         cum += pc;
@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       __syncthreads();
       if (threadIdx.x == 0) {
         // merge rank cuts [1, nrk) and width cuts [1, nwd) by column
-        const int nrk = min((nnz - 1) / kPartKeys + 1, kMaxRankCuts);
-        const int nwd = min((int)((B.ncols - 1) >> kPartWidthLog) + 1, kMaxWidthCuts);
+        const int nrk = min((nnz - 1) / kPartKeys + 1, kMaxPartsPerRow);
+        const int nwd = min((int)((B.ncols - 1) >> kPartWidthLog) + 1, kMaxPartsPerRow);
         int np = 0;
         int64_t base = 0;
         for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts, pass 1 writes
