@@ -194,13 +194,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
     if (use_seq(flop[i], ae - as)) {
       // keys of a round are distinct: plain read-modify-write of the value
       for_row<true, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
-        if (act) vals[num_probe_smem(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
+        if (act) vals[num_probe(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
         __syncwarp();
       });
     } else {
       for_row<false, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         uint32_t slot = 0;
-        if (act) slot = num_probe_smem(keys, c, logT);
+        if (act) slot = num_probe(keys, c, logT);
         const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
         if (act) {
           if (__popc(grp) == 1) vals[slot] += v;   // c_ij <- c_ij + value (l.8)

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) cnt += sym_insert_smem(tab, c, logT);
+      if (act) cnt += sym_insert(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, 0, 1, ins);
     else for_row<false, false>(A, B, as, ae, 0, 1, ins);
