@@ -26,6 +26,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# C of the large configs is >100 GB: avoid caching-allocator fragmentation
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 DEFAULT_CONFIG = "c2_stencil64"   # BASELINE.json configs[1]
 L2_FLUSH_BYTES = 256 << 20
@@ -159,7 +161,7 @@ def kernel_bytes(name: str, a_nnz_row, flop_row, c_nnz_row, m, nnzA, ncols, krow
     if name in SYM_KERNEL_BIN:
         sel = np.isin(bin_of_rows_sym(flop_row, ncols), SYM_KERNEL_BIN[name])
         return float((16 + 4 * a_nnz_row[sel] + 4 * flop_row[sel]).sum())
-    if name == "k_flop_bin":
+    if name == "k_flop_nz":
         return float(8 * (m + 1) + 4 * nnzA + 8 * m + 8 * (krows + 1))
     return None
 

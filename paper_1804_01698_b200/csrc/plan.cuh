@@ -6,71 +6,121 @@
 namespace spg {
 
 // ---------------------------------------------------------------------------
-// a1 + a2 counts.  flop[i] = sum_{j in A_i} nnz(B_{col_j})
-// (Fig:load_balance l.1-6; "non-trivial scalar multiplications",
-// P:137).  G lanes cooperate on one row (G in {4,8,16,32}); also counts rows
-// per symbolic bin, the total / max flop and the longest B row touched.
+// a1, nonzero-parallel form (balanced whatever the row lengths): every thread
+// owns kFlopRun consecutive stored a_ik, finds the row of the first one by a
+// binary search of A.rp inside its block's row range, sums nnz(b_k*) along
+// its run, and adds each row's partial sum with a segmented warp reduction
+// + one atomicAdd per row segment.  flop[] must be zeroed first.
 // ---------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(256) k_flop_bin(DevCSR A, const int64_t *__restrict__ b_rp,
-                                                  int64_t ncols, int64_t *__restrict__ flop,
-                                                  PlanInfo *info, int count_bins) {
-  __shared__ unsigned s_bins[kMaxBins];
-  __shared__ unsigned long long s_sum, s_max, s_maxb;
-  if (threadIdx.x < kMaxBins) s_bins[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { s_sum = 0; s_max = 0; s_maxb = 0; }
-  __syncthreads();
+constexpr int kFlopRun = 8;
+constexpr int kFlopThreads = 256;
+constexpr int kFlopTile = kFlopRun * kFlopThreads;
+
+__device__ __forceinline__ int64_t row_of(const int64_t *__restrict__ rp, int64_t lo, int64_t hi,
+                                          int64_t j) {
+  // last r in [lo, hi] with rp[r] <= j
+  while (hi - lo > 0) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (__ldg(rp + mid) <= j) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_t *__restrict__ b_rp,
+                                                          unsigned long long *__restrict__ flop,
+                                                          PlanInfo *info) {
+  __shared__ long long s_r[2];
+  __shared__ unsigned long long s_maxb;
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  constexpr int kRowsPerWarp = 32 / G;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  unsigned long long my_sum = 0, my_max = 0, my_maxb = 0, my_maxa = 0;
-  for (int64_t base = warp * kRowsPerWarp; base < A.nrows; base += nwarps * kRowsPerWarp) {
-    const int64_t i = base + lane / G;
-    if (i < A.nrows) {  // uniform inside the G-lane group
-      const int64_t s = A.rp[i], e = A.rp[i + 1];
-      int64_t f = 0, mb = 0;
-      if (gl == 0) my_maxa = (unsigned long long)(e - s) > my_maxa ? (unsigned long long)(e - s) : my_maxa;
-      for (int64_t j = s + gl; j < e; j += G) {
-        const int k = __ldg(A.col + j);
-        const int64_t len = __ldg(b_rp + k + 1) - __ldg(b_rp + k);
-        f += len;
-        mb = len > mb ? len : mb;
-      }
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) f += __shfl_xor_sync(gmask, f, o, G);
-      my_maxb = (unsigned long long)mb > my_maxb ? (unsigned long long)mb : my_maxb;
-      if (gl == 0) {
-        flop[i] = f;
-        my_sum += (unsigned long long)f;
-        my_max = (unsigned long long)f > my_max ? (unsigned long long)f : my_max;
-        if (count_bins) atomicAdd(&s_bins[sym_bin(f, ncols)], 1u);
-      }
+  const int64_t base = A.rp[0], nz = A.rp[A.nrows] - base;
+  unsigned long long maxb = 0;
+  if (threadIdx.x == 0) s_maxb = 0;
+  for (int64_t t0 = int64_t(blockIdx.x) * kFlopTile; t0 < nz; t0 += int64_t(gridDim.x) * kFlopTile) {
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : min<int64_t>(kFlopTile, nz - t0) - 1);
+      s_r[threadIdx.x] = row_of(A.rp, 0, A.nrows - 1, j);
     }
+    __syncthreads();
+    const int64_t rlo = s_r[0], rhi = s_r[1];
+    const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
+    const int64_t jend = base + nz;
+    int64_t r = j0 < jend ? row_of(A.rp, rlo, rhi, j0) : rhi;
+    int64_t rend = __ldg(A.rp + r + 1);
+    unsigned long long acc = 0;
+    // walk the run; flush acc at each row boundary (all but the last segment)
+    for (int u = 0; u < kFlopRun; ++u) {
+      const int64_t j = j0 + u;
+      if (j >= jend) break;
+      while (j >= rend) {
+        if (acc) atomicAdd(flop + r, acc);
+        acc = 0;
+        ++r;
+        rend = __ldg(A.rp + r + 1);
+      }
+      const int k = __ldg(A.col + j);
+      const unsigned long long len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
+      acc += len;
+      maxb = len > maxb ? len : maxb;
+    }
+    // last segment: lanes holding the same row combine before the atomic
+    const unsigned long long key = (unsigned long long)r;
+    const unsigned grp = __match_any_sync(kFull, j0 < jend ? key : ~0ull);
+    const int leader = __ffs(grp) - 1;
+    // segmented suffix sum inside the group (groups are contiguous lane ranges
+    // because rows are nondecreasing across lanes): after the step with offset
+    // o, lane i holds the sum over lanes [i, i + 2o) of its group
+    unsigned long long sum = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_down_sync(kFull, sum, o);
+      if (lane + o < 32 && ((grp >> (lane + o)) & 1u)) sum += v;
+    }
+    if (lane == leader && j0 < jend && sum) atomicAdd(flop + r, sum);
   }
-  my_sum = warp_sum(my_sum);
-#pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    unsigned long long t = __shfl_xor_sync(kFull, my_max, o);
-    my_max = t > my_max ? t : my_max;
-    t = __shfl_xor_sync(kFull, my_maxb, o);
-    my_maxb = t > my_maxb ? t : my_maxb;
-    t = __shfl_xor_sync(kFull, my_maxa, o);
-    my_maxa = t > my_maxa ? t : my_maxa;
+    const unsigned long long t = __shfl_xor_sync(kFull, maxb, o);
+    maxb = t > maxb ? t : maxb;
   }
-  if (lane == 0) {
-    atomicAdd(&s_sum, my_sum);
-    atomicMax(&s_max, my_max);
-    atomicMax(&s_maxb, my_maxb);
-    if (my_maxa) atomicMax(&info->max_arow, my_maxa);
+  if (lane == 0) atomicMax(&s_maxb, maxb);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&info->max_brow, s_maxb);
+}
+
+// Per-row pass after k_flop_nz: symbolic bin counts, flop total / max, longest a_i.
+__global__ void __launch_bounds__(256) k_flop_stats(DevCSR A, int64_t ncols,
+                                                    const int64_t *__restrict__ flop,
+                                                    PlanInfo *info, int count_bins) {
+  __shared__ unsigned s_bins[kMaxBins];
+  __shared__ unsigned long long s_sum, s_max, s_maxa;
+  if (threadIdx.x < kMaxBins) s_bins[threadIdx.x] = 0;
+  if (threadIdx.x == 0) { s_sum = 0; s_max = 0; s_maxa = 0; }
+  __syncthreads();
+  unsigned long long sum = 0, mx = 0, mxa = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < A.nrows;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = flop[i], na = A.rp[i + 1] - A.rp[i];
+    sum += (unsigned long long)f;
+    mx = (unsigned long long)f > mx ? (unsigned long long)f : mx;
+    mxa = (unsigned long long)na > mxa ? (unsigned long long)na : mxa;
+    if (count_bins) atomicAdd(&s_bins[sym_bin(f, ncols, na)], 1u);
+  }
+  sum = warp_sum(sum);
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long t = __shfl_xor_sync(kFull, mx, o);
+    mx = t > mx ? t : mx;
+    t = __shfl_xor_sync(kFull, mxa, o);
+    mxa = t > mxa ? t : mxa;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_sum, sum);
+    atomicMax(&s_max, mx);
+    atomicMax(&s_maxa, mxa);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_sum) atomicAdd(&info->flop_total, s_sum);
     atomicMax(&info->max_flop, s_max);
-    atomicMax(&info->max_brow, s_maxb);
+    atomicMax(&info->max_arow, s_maxa);
   }
   if (count_bins && threadIdx.x < kMaxBins && s_bins[threadIdx.x])
     atomicAdd(&info->sym_count[threadIdx.x], (unsigned long long)s_bins[threadIdx.x]);
@@ -82,6 +132,7 @@ __global__ void __launch_bounds__(256) k_flop_bin(DevCSR A, const int64_t *__res
 // mode 1 = numeric bins from nnz(c_i) = C_rp[i+1] - C_rp[i].
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *__restrict__ key,
+                                                     const int64_t *__restrict__ arp,
                                                      int64_t ncols, int mode, PlanInfo *info,
                                                      int32_t *__restrict__ rows_out,
                                                      int64_t *__restrict__ row_nnz,
@@ -95,10 +146,10 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
   unsigned local = 0;
   if (i < m) {
     if (mode == 0) {
-      b = sym_bin(key[i], ncols);
+      b = sym_bin(key[i], ncols, arp[i + 1] - arp[i]);
       if (b == SB_SKIP) row_nnz[i] = 0;
     } else {
-      b = num_bin_row(key[i + 1] - key[i], part_n, i);
+      b = num_bin_row(key[i + 1] - key[i], arp[i + 1] - arp[i], part_n, i);
     }
     if (b != 0) local = atomicAdd(&s_cnt[b], 1u);
   }
@@ -188,7 +239,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partials(int64_t *__restr
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict__ data, int64_t n,
                                                             const int64_t *__restrict__ partial,
                                                             PlanInfo *info,
-                                                            const int32_t *__restrict__ part_n) {
+                                                            const int32_t *__restrict__ part_n,
+                                                            const int64_t *__restrict__ arp) {
   __shared__ long long s_warp[33];
   __shared__ unsigned s_bins[kMaxBins];
   __shared__ unsigned long long s_max;
@@ -208,7 +260,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < kScanItems; ++t)
-    if (base + t < n && v[t] > 0) atomicAdd(&s_bins[num_bin_row(v[t], part_n, base + t)], 1u);
+    if (arp && base + t < n && v[t] > 0)
+      atomicAdd(&s_bins[num_bin_row(v[t], arp[base + t + 1] - arp[base + t], part_n, base + t)], 1u);
   long long tot;
   long long ex = block_excl_scan_1024(s, s_warp, &tot) + partial[blockIdx.x];
 #pragma unroll

@@ -85,9 +85,14 @@ __device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {
 // numeric phase); otherwise the larger smem hash tables / global hash.
 constexpr int64_t kBitmapMaxCols = int64_t(200 * 1024) * 8;  // 200 KB of bits
 
-__device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols) {
+// Rows with more than kWarpMaxEntries a_ik go to a block tier even when their
+// table is small: one warp would walk all their a_ik alone.
+constexpr int64_t kWarpMaxEntries = 512;
+
+__device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols, int64_t na) {
   if (flop == 0) return SB_SKIP;
   int n = sym_log2_gpu(flop, ncols);
+  if (na > kWarpMaxEntries && n <= 10) return SB_B2K;
   if (n <= 7) return SB_W128;
   if (n <= 10) return SB_W1024;
   if (n <= 13) return SB_B2K + (n - 11);
@@ -113,9 +118,10 @@ __device__ __forceinline__ int num_log2(int64_t nnz) {
   return n < kMinLogT ? kMinLogT : n;
 }
 
-__device__ __forceinline__ int num_bin(int64_t nnz) {
+__device__ __forceinline__ int num_bin(int64_t nnz, int64_t na) {
   if (nnz == 0) return NB_SKIP;
   int n = num_log2(nnz);
+  if (na > kWarpMaxEntries && n <= 10) return NB_B2K;
   if (n <= 8) return NB_W256;
   if (n <= 10) return NB_W1024;
   if (n <= 14) return NB_B2K + (n - 11);
@@ -123,8 +129,9 @@ __device__ __forceinline__ int num_bin(int64_t nnz) {
 }
 
 // numeric bin of a row, with the part kind of long rows (part_n < 0: warp parts)
-__device__ __forceinline__ int num_bin_row(int64_t nnz, const int32_t *part_n, int64_t i) {
-  const int b = num_bin(nnz);
+__device__ __forceinline__ int num_bin_row(int64_t nnz, int64_t na, const int32_t *part_n,
+                                           int64_t i) {
+  const int b = num_bin(nnz, na);
   if (b == NB_G && part_n != nullptr && part_n[i] < 0) return NB_GW;
   return b;
 }

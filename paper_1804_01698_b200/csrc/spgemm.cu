@@ -173,7 +173,8 @@ spg_status set_smem(spg_ctx *c, K kernel, size_t bytes) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// a1 (+ a2 counts): per-row flop with a lane-group size matched to nnz/row.
+// a1 (+ a2 counts): per-row flop, nonzero-parallel (balanced whatever the row
+// lengths), then a per-row pass for bins / totals.
 spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count_bins,
                        cudaStream_t s) {
   const int64_t m = A->nrows;
@@ -181,22 +182,25 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
   PlanInfo *info = (PlanInfo *)c->info.p;
   int64_t *flop = (int64_t *)c->flop.p;
   DevCSR a = dev(A);
-  // lane group size: host does not know nnz(A) without a read; use the
-  // caller-independent choice G = 8 (rows of R-MAT/ER/stencil average 8-30).
-  constexpr int G = 8;
-  const int64_t rows_per_block = 256 / G;
-  int64_t grid = std::min<int64_t>(ceil_div(m, rows_per_block), int64_t(c->num_sms) * 16);
+  SPG_CUDA(c, cudaMemsetAsync(flop, 0, size_t(m) * 8, s));
   {
-    ProfScope _ps(c, s, "k_flop_bin");
-    k_flop_bin<G><<<(unsigned)grid, 256, 0, s>>>(a, B->row_ptr, B->ncols, flop, info, count_bins);
+    ProfScope _ps(c, s, "k_flop_nz");
+    k_flop_nz<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
+        a, B->row_ptr, (unsigned long long *)flop, info);
   }
-  SPG_LAUNCHED(c, "k_flop_bin");
+  SPG_LAUNCHED(c, "k_flop_nz");
+  {
+    ProfScope _ps(c, s, "k_flop_stats");
+    const int64_t grid = std::min<int64_t>(ceil_div(m, 256), int64_t(c->num_sms) * 8);
+    k_flop_stats<<<(unsigned)grid, 256, 0, s>>>(a, B->ncols, flop, info, count_bins);
+  }
+  SPG_LAUNCHED(c, "k_flop_stats");
   return SPG_OK;
 }
 
 // scan of data[0..n) in place (int64), numeric-bin counting in the last pass
 spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
-                       const int32_t *part_n = nullptr) {
+                       const int32_t *part_n = nullptr, const int64_t *arp = nullptr) {
   if (n == 0) return SPG_OK;
   const int64_t nb = ceil_div(n, kScanTile);
   SPG_CUDA(c, cudaGetLastError());
@@ -216,7 +220,7 @@ spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
   {
     ProfScope _ps(c, s, "k_scan_down");
     k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p,
-                                                      part_n);
+                                                      part_n, arp);
   }
   SPG_LAUNCHED(c, "k_scan_down");
   return SPG_OK;
@@ -395,7 +399,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     if ((st = launch_flop(c, A, B, 1, s)) != SPG_OK) return st;
     {
       ProfScope _ps(c, s, "k_bin_scatter_sym");
-      k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, B->ncols, 0, info,
+      k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, A->row_ptr, B->ncols, 0, info,
                                                                (int32_t *)c->rows_sym.p, row_nnz, nullptr);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(sym)");
@@ -495,11 +499,11 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   }
   // a4: C_row_ptr = exclusive scan of row nnz (+ numeric bin counts)
   const int32_t *pn = c->plan_parts ? (const int32_t *)c->part_n.p : nullptr;
-  if ((st = launch_scan(c, row_nnz, m, s, pn)) != SPG_OK) return st;
+  if ((st = launch_scan(c, row_nnz, m, s, pn, A->row_ptr)) != SPG_OK) return st;
   if (m > 0) {
     {
       ProfScope _ps(c, s, "k_bin_scatter_num");
-      k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, 0, 1, info,
+      k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, A->row_ptr, 0, 1, info,
                                                                (int32_t *)c->rows_num.p, nullptr, pn);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(num)");
