@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
   for (int64_t t0 = int64_t(blockIdx.x) * kFlopTile; t0 < nz; t0 += int64_t(gridDim.x) * kFlopTile) {
     __syncthreads();
     if (threadIdx.x < 2) {
-      const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : min<int64_t>(kFlopTile, nz - t0) - 1);
+      const int64_t tl = (nz - t0) < kFlopTile ? (nz - t0) : kFlopTile;
+      const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : tl - 1);
       s_r[threadIdx.x] = row_of(A.rp, 0, A.nrows - 1, j);
     }
     __syncthreads();
