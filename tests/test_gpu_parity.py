@@ -277,12 +277,20 @@ def test_c3_full_size_sampled(spg, ctx):
         # row sums: C*1 vs A*(B*1) computed on the host from A, B (fp64)
         rp = C.row_ptr
         rs = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
-        rows_idx = torch.repeat_interleave(torch.arange(A.nrows, device="cuda"), rp.diff())
-        rs.index_add_(0, rows_idx, C.val)
+        rp_h = rp.cpu().numpy()
+        r0 = 0
+        while r0 < A.nrows:  # row blocks of <= 2^28 entries (C3's C has 9.7e9)
+            r1 = int(np.searchsorted(rp_h, rp_h[r0] + (1 << 28), side="right")) - 1
+            r1 = min(max(r1, r0 + 1), A.nrows)
+            lens = rp[r0 + 1:r1 + 1] - rp[r0:r1]
+            idx = torch.repeat_interleave(torch.arange(r0, r1, device="cuda"), lens)
+            rs.index_add_(0, idx, C.val[int(rp_h[r0]):int(rp_h[r1])])
+            del idx
+            r0 = r1
         bsum = np.bincount(np.repeat(np.arange(B.nrows), np.diff(B.row_ptr)), weights=B.val,
                            minlength=B.nrows)
         ref = np.bincount(np.repeat(np.arange(A.nrows), np.diff(A.row_ptr)),
                           weights=A.val * bsum[A.col], minlength=A.nrows)
         np.testing.assert_allclose(rs.cpu().numpy(), ref, rtol=1e-11, atol=1e-300)
-        del C, rs, rows_idx
+        del C, rs
         torch.cuda.empty_cache()
