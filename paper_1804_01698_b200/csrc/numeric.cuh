@@ -132,15 +132,14 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
     uint32_t *grp = keys + (T >> 1);                                  // free half
     for (int e = lane; e < nnz; e += 32) loc[e] = atomicAdd(cnt + ((keys[e] - mn) >> sh), 1u);
     __syncwarp();
-    // 3. exclusive scan of the bucket counts (lane owns T/32 consecutive)
-    const int per = T >> 5;
-    int run = 0;
-    for (int q = 0; q < per; ++q) run += (int)cnt[lane * per + q];
-    int ex = warp_incl_scan(run) - run;
-    for (int q = 0; q < per; ++q) {
-      const int v = (int)cnt[lane * per + q];
-      cnt[lane * per + q] = (uint32_t)ex;
-      ex += v;
+    // 3. exclusive scan of the bucket counts, 32 consecutive buckets per step
+    //    (lane l reads bucket q + l: conflict-free)
+    int carry = 0;
+    for (int q = 0; q < T; q += 32) {
+      const int v = (int)cnt[q + lane];
+      const int incl = warp_incl_scan(v);
+      cnt[q + lane] = (uint32_t)(carry + incl - v);
+      carry += __shfl_sync(kFull, incl, 31);
     }
     __syncwarp();
     // 4. group keys by bucket, 5. rank inside the bucket and store
@@ -193,12 +192,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restri
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     if (use_seq(flop[i], ae - as)) {
       // keys of a round are distinct: plain read-modify-write of the value
-      for_row<true, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
+      for_row<true, true, 2>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         if (act) vals[num_probe(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
         __syncwarp();
       });
     } else {
-      for_row<false, true>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
+      for_row<false, true, 2>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         uint32_t slot = 0;
         if (act) slot = num_probe(keys, c, logT);
         const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));

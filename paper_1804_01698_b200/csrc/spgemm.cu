@@ -276,7 +276,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
   }
   ok = ok && cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
   if (ok) {
-    const size_t s_num_w1024 = size_t(4) * 1024 * 16;
+    const size_t s_num_w1024 = 4 * 1024 * 16;
     const size_t s_num_b = size_t(16384) * 12;
     ok = set_smem(c, k_num_warp<1024, 4>, s_num_w1024) == SPG_OK &&
          set_smem(c, k_num_block<512>, s_num_b) == SPG_OK &&

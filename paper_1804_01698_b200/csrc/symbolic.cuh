@@ -62,7 +62,7 @@ struct Entry {
   double a;
 };
 
-template <bool kSeq, bool kVal, typename EF, typename F>
+template <bool kSeq, bool kVal, int kDepth, typename EF, typename F>
 __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w, int NW,
                                             EF &&entry, F &&f) {
   const int lane = lane_id();
@@ -78,41 +78,40 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
     if (cb + lane < nent) en = entry(cb + lane);
     if (kSeq && own_chunks && __all_sync(kFull, en.len <= 32)) {
       // this warp owns the chunk and every B row fits one round: one round per
-      // nonempty entry, the gathers of the next round issued before this one
-      // is hashed (software pipeline)
+      // nonempty entry.  Rolling software pipeline over kDepth register slots
+      // (deep for the block / bitmap tiers, 1 for the occupancy-bound warp tiers):
+      // slot d holds the gathered (b_kj, a_ik) of a round; right after a
+      // round is hashed its slot is refilled with the round kDepth ahead, so
+      // kDepth independent gathers stay in flight per lane.
       unsigned pend = __ballot_sync(kFull, en.len > 0);
-      if (!pend) continue;
-      int j = __ffs(pend) - 1;
-      pend &= pend - 1;
-      int L = __shfl_sync(kFull, en.len, j);
-      double aj = kVal ? shfl_f64(en.a, j) : 0.0;
-      int64_t jbs = shfl_i64(en.bs, j);
-      bool act = lane < L;
-      uint32_t c = act ? (uint32_t)__ldg(B.col + jbs + lane) : 0u;
-      double bv = (kVal && act) ? __ldg(B.val + jbs + lane) : 0.0;
-      while (true) {
-        const bool more = pend != 0;
-        int nL = 0;
-        double na = 0.0;
-        uint32_t nc = 0u;
-        double nbv = 0.0;
-        if (more) {
-          const int nj = __ffs(pend) - 1;
+      int sl[kDepth];
+      uint32_t sc[kDepth];
+      double sb[kDepth], sa[kDepth];
+      auto fill = [&](int d) {
+        sl[d] = 0;
+        if (pend) {  // warp-uniform
+          const int j = __ffs(pend) - 1;
           pend &= pend - 1;
-          nL = __shfl_sync(kFull, en.len, nj);
-          if (kVal) na = shfl_f64(en.a, nj);
-          const int64_t nbs = shfl_i64(en.bs, nj);
-          if (lane < nL) {
-            nc = (uint32_t)__ldg(B.col + nbs + lane);
-            if (kVal) nbv = __ldg(B.val + nbs + lane);
+          sl[d] = __shfl_sync(kFull, en.len, j);
+          if (kVal) sa[d] = shfl_f64(en.a, j);
+          const int64_t bs = shfl_i64(en.bs, j);
+          if (lane < sl[d]) {
+            sc[d] = (uint32_t)__ldg(B.col + bs + lane);
+            if (kVal) sb[d] = __ldg(B.val + bs + lane);
           }
         }
-        f(act, c, aj * bv);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
-        if (!more) break;
-        act = lane < nL;
-        c = nc;
-        bv = nbv;
-        aj = na;
+      };
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) fill(d);
+      bool more = sl[0] > 0;
+      while (more) {
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+          if (sl[d] == 0) { more = false; break; }  // rounds are slotted in order
+          const bool act = lane < sl[d];
+          f(act, act ? sc[d] : 0u, (kVal && act) ? sa[d] * sb[d] : 0.0);  // a_ik * b_kj (l.5)
+          fill(d);
+        }
       }
       continue;
     }
@@ -208,10 +207,10 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
 }
 
 // All products of row [as, ae) of A.
-template <bool kSeq, bool kVal, typename F>
+template <bool kSeq, bool kVal, int kDepth = (kVal ? 4 : 8), typename F>
 __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_t as,
                                         int64_t ae, int w, int NW, F &&f) {
-  for_entries<kSeq, kVal>(
+  for_entries<kSeq, kVal, kDepth>(
       B, ae - as, w, NW,
       [&](int64_t j) {
         const int k = __ldg(A.col + as + j);
@@ -254,8 +253,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     auto ins = [&](bool act, uint32_t c, double) {
       if (act) cnt += sym_insert(tab, c, logT);
     };
-    if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, 0, 1, ins);
-    else for_row<false, false>(A, B, as, ae, 0, 1, ins);
+    if (use_seq(flop[i], ae - as)) for_row<true, false, 2>(A, B, as, ae, 0, 1, ins);
+    else for_row<false, false, 2>(A, B, as, ae, 0, 1, ins);
     cnt = warp_sum(cnt);
     if (lane == 0) row_nnz[i] = cnt;
     __syncwarp();
@@ -297,6 +296,47 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
   }
 }
 
+// Block-wide walk of bitmap words bm[0, nwords) in order with the exclusive
+// prefix popcount of each word: f(q, word, cum) for every word q.  Warp w owns
+// a contiguous range of 32-word chunks; lane l reads word chunk + l, so every
+// shared load is conflict-free.  Two passes: warp totals, then the walk.
+// Contains barriers (all threads must call it).
+template <typename F>
+__device__ __forceinline__ void bitmap_prefix_walk(const uint32_t *bm, int nwords, int *s_warp,
+                                                   F &&f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int nchunks = (nwords + 31) >> 5;
+  const int cper = (nchunks + NW - 1) / NW;
+  const int q0 = w * cper * 32, q1 = min(nwords, (w + 1) * cper * 32);
+  int mine = 0;
+  for (int q = q0 + lane; q < q1; q += 32) mine += __popc(bm[q]);
+  mine = warp_sum(mine);
+  if (lane == 0) s_warp[w] = mine;
+  __syncthreads();
+  if (w == 0) {
+    const int v = lane < NW ? s_warp[lane] : 0;
+    const int vi = warp_incl_scan(v);
+    if (lane < NW) s_warp[lane] = vi - v;
+  }
+  __syncthreads();
+  int carry = s_warp[w];
+  for (int c0 = q0; c0 < q1; c0 += 32) {
+    const int q = c0 + lane;
+    const uint32_t word = q < q1 ? bm[q] : 0u;
+    const int pc = __popc(word);
+    const int incl = warp_incl_scan(pc);
+    if (q < q1) f(q, word, carry + incl - pc);
+    carry += __shfl_sync(kFull, incl, 31);
+  }
+  __syncthreads();
+}
+
+// column of the n-th (0-based) set bit of word q
+__device__ __forceinline__ int nth_bit_col(int q, uint32_t word, int n) {
+  for (int t = 0; t < n; ++t) word &= word - 1;  // drop the n lower set bits
+  return q * 32 + __ffs(word) - 1;
+}
+
 // ---------------------------------------------------------------------------
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
@@ -317,6 +357,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt;
   __shared__ int s_warp[THREADS / 32];
+  __shared__ int s_base;
   __shared__ int2 s_rank[kMaxPartsPerRow];   // rank cuts (col, cum)
   __shared__ int2 s_width[kMaxPartsPerRow];  // width cuts (col, cum)
   constexpr int NW = THREADS / 32;
@@ -349,83 +390,39 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
         const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
         if (base + np > parts_cap) {
           atomicAdd(&info->parts_overflow, 1ull);
-          s_warp[0] = -1;
+          s_base = -1;
         } else {
-          s_warp[0] = (int)base;
+          s_base = (int)base;
           part_off[i] = (int32_t)base;
           part_n[i] = -np;
           parts[base] = make_int2(0, 0);
         }
       }
       __syncthreads();
-      const int base = s_warp[0];
-      __syncthreads();
+      const int base = s_base;
       if (base >= 0) {
-        const int per = (nwords + THREADS - 1) / THREADS;
-        const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
-        int mine = 0;
-        for (int q = w0; q < w1; ++q) mine += __popc(bm[q]);
-        const int incl = warp_incl_scan(mine);
-        if (lane == 31) s_warp[w] = incl;
-        __syncthreads();
-        if (w == 0) {
-          const int v = lane < NW ? s_warp[lane] : 0;
-          const int vi = warp_incl_scan(v);
-          if (lane < NW) s_warp[lane] = vi - v;
-        }
-        __syncthreads();
-        int cum = s_warp[w] + incl - mine;
-        for (int q = w0; q < w1; ++q) {
-          const uint32_t word = bm[q];
-          const int pc = __popc(word);
-          int nextR = ((cum + kWPartKeys - 1) / kWPartKeys) * kWPartKeys;
-          if (nextR == 0) nextR = kWPartKeys;
-          while (nextR < cum + pc) {
-            uint32_t wv = word;
-            for (int t = 0; t < nextR - cum; ++t) wv &= wv - 1;
-            parts[base + nextR / kWPartKeys] = make_int2(q * 32 + __ffs(wv) - 1, nextR);
-            nextR += kWPartKeys;
-          }
-          cum += pc;
-        }
+        bitmap_prefix_walk(bm, nwords, s_warp, [&](int q, uint32_t word, int cum) {
+          int r = ((cum + kWPartKeys - 1) / kWPartKeys) * kWPartKeys;
+          if (r == 0) r = kWPartKeys;
+          if (r < cum + __popc(word))  // at most one cut per word (kWPartKeys >= 32)
+            parts[base + r / kWPartKeys] = make_int2(nth_bit_col(q, word, r - cum), r);
+        });
       } else if (threadIdx.x == 0) {
         part_n[i] = 0;
       }
     } else if (want_parts && !wkind && nnz > kPartKeys) {
-      // each thread owns a contiguous range of words; block scan of popcounts
-      const int per = (nwords + THREADS - 1) / THREADS;
-      const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
-      int mine = 0;
-      for (int q = w0; q < w1; ++q) mine += __popc(bm[q]);
-      const int incl = warp_incl_scan(mine);
-      if (lane == 31) s_warp[w] = incl;
-      __syncthreads();
-      if (w == 0) {
-        const int v = lane < NW ? s_warp[lane] : 0;
-        const int vi = warp_incl_scan(v);
-        if (lane < NW) s_warp[lane] = vi - v;
-      }
-      __syncthreads();
-      int cum = s_warp[w] + incl - mine;  // keys before word w0
-      for (int q = w0; q < w1; ++q) {
-        const uint32_t word = bm[q];
-        const int pc = __popc(word);
+      bitmap_prefix_walk(bm, nwords, s_warp, [&](int q, uint32_t word, int cum) {
         if (q > 0 && ((int64_t(q) * 32) & (kPartWidth - 1)) == 0) {  // width cut
           const int k = (int)((int64_t(q) * 32) >> kPartWidthLog);
           if (k < kMaxPartsPerRow) s_width[k] = make_int2(q * 32, cum);
         }
-        int nextR = ((cum + kPartKeys - 1) / kPartKeys) * kPartKeys;  // rank cuts
-        if (nextR == 0) nextR = kPartKeys;
-        while (nextR < cum + pc) {
-          uint32_t wv = word;
-          for (int t = 0; t < nextR - cum; ++t) wv &= wv - 1;  // drop lower set bits
-          const int k = nextR / kPartKeys;
-          if (k < kMaxPartsPerRow) s_rank[k] = make_int2(q * 32 + __ffs(wv) - 1, nextR);
-          nextR += kPartKeys;
+        int r = ((cum + kPartKeys - 1) / kPartKeys) * kPartKeys;  // rank cut (at most one per word)
+        if (r == 0) r = kPartKeys;
+        if (r < cum + __popc(word)) {
+          const int k = r / kPartKeys;
+          if (k < kMaxPartsPerRow) s_rank[k] = make_int2(nth_bit_col(q, word, r - cum), r);
         }
-        cum += pc;
-      }
-      __syncthreads();
+      });
       if (threadIdx.x == 0) {
         // merge rank cuts [1, nrk) and width cuts [1, nwd) by column
         const int nrk = min((nnz - 1) / kPartKeys + 1, kMaxPartsPerRow);

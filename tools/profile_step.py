@@ -16,10 +16,14 @@ ap.add_argument("--scale", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--sorted", type=int, default=1)
 ap.add_argument("--records", action="store_true")
+ap.add_argument("--rows", default=None, help="r0:r1 row-range view of A")
 a = ap.parse_args()
 A, B, _ = synth.workload(a.config, a.scale)
 dA = spg.DeviceCSR.from_host(A)
 dB = dA if B is A else spg.DeviceCSR.from_host(B)
+if a.rows:
+    r0, r1 = (int(x) for x in a.rows.split(":"))
+    dA = dA.rows(r0, r1)
 ctx = spg.Context()
 from paper_1804_01698_b200 import _lib  # noqa: E402
 for _ in range(a.reps):
