@@ -99,6 +99,14 @@ spg_status spg_profile_reset(spg_ctx *ctx);
 int64_t spg_profile_count(spg_ctx *ctx);
 spg_status spg_profile_record(spg_ctx *ctx, int64_t idx, const char **name, float *ms);
 
+/* Measurement aid: 16 int64 kernel counters of the last call (host out),
+ * filled only when the environment variable SPG_TUNE has bit 8 set at ctx
+ * creation (per-phase clock64 sums of the column-part kernel: [0] parts,
+ * [1] init+segment search, [2] scan, [3] accumulate, [4] emit clocks,
+ * [5] products, [6] entries).  Zeroed by spg_symbolic.  Synchronizes
+ * `stream`. */
+spg_status spg_debug_counters(spg_ctx *ctx, int64_t *out, void *stream);
+
 /* Phase 1 -- symbolic (Fig:hash_spgemm l.1-14 and "Symbolic(rpts_C, A, B)",
  * P:292-310; hashing P:283, "In symbolic phase, it is enough to insert keys",
  * P:285).  Steps, all on the GPU: per-row flop (Fig:load_balance l.1-6),

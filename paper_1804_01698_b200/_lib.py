@@ -21,7 +21,8 @@ STATUS = {0: "SPG_OK", 1: "SPG_ERR_INVALID_ARG", 2: "SPG_ERR_DIM_MISMATCH",
 EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_count",
            "spg_symbolic", "spg_numeric", "spg_get_info", "spg_plan_export",
            "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
-           "spg_profile_reset", "spg_profile_count", "spg_profile_record")
+           "spg_profile_reset", "spg_profile_count", "spg_profile_record",
+           "spg_debug_counters")
 
 
 class spg_csr(ct.Structure):
@@ -74,6 +75,7 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_profile_count.argtypes = [vp]
     lib.spg_profile_count.restype = i64
     lib.spg_profile_record.argtypes = [vp, i64, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_float)]
+    lib.spg_debug_counters.argtypes = [vp, i64p, vp]
     for name in EXPORTS:
         if name not in ("spg_last_error", "spg_launch_count", "spg_profile_count"):
             getattr(lib, name).restype = ct.c_int
@@ -168,3 +170,9 @@ def spg_profile_records(ctx: int) -> list[tuple[str, float]]:
         _check(ctx, "spg_profile_record", lib.spg_profile_record(ctx, i, ct.byref(name), ct.byref(ms)))
         out.append((name.value.decode(), float(ms.value)))
     return out
+
+
+def spg_debug_counters(ctx: int, stream: int = 0) -> list[int]:
+    out = (ct.c_int64 * 16)()
+    _check(ctx, "spg_debug_counters", load().spg_debug_counters(ctx, out, stream))
+    return list(out)

@@ -30,44 +30,27 @@ __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int lo
   }
 }
 
-// Warp-cooperative bitonic sort of P (power of two) (key, val) pairs in smem.
-__device__ __forceinline__ void warp_bitonic(uint32_t *keys, double *vals, int P) {
+// Lanes of a round holding the same key c combine their values into the
+// lowest such lane; returns true for the lanes that then hold a key to apply
+// (active, first of their key).  Summation order inside a round is free
+// (reading R4).
+__device__ __forceinline__ bool warp_combine(bool act, uint32_t c, double &v) {
   const int lane = lane_id();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < (P >> 1); t += 32) {
-        const int i0 = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-        const int i1 = i0 + j;
-        const bool up = (i0 & k) == 0;
-        const uint32_t a = keys[i0], b = keys[i1];
-        if ((a > b) == up) {
-          keys[i0] = b; keys[i1] = a;
-          const double va = vals[i0];
-          vals[i0] = vals[i1]; vals[i1] = va;
-        }
+  const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
+  const int leader = __ffs(grp) - 1;
+  const int gmax = (int)__reduce_max_sync(kFull, (unsigned)__popc(grp));
+  if (gmax > 1) {
+    unsigned rem = lane == leader ? grp & ~(1u << lane) : 0u;
+    for (int it = 1; it < gmax; ++it) {
+      const int src = rem ? __ffs(rem) - 1 : lane;
+      const double o = __shfl_sync(kFull, v, src);
+      if (rem) {
+        v += o;
+        rem &= rem - 1;
       }
-      __syncwarp();
     }
   }
-}
-
-__device__ __forceinline__ void block_bitonic(uint32_t *keys, double *vals, int P) {
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
-        const int i0 = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-        const int i1 = i0 + j;
-        const bool up = (i0 & k) == 0;
-        const uint32_t a = keys[i0], b = keys[i1];
-        if ((a > b) == up) {
-          keys[i0] = b; keys[i1] = a;
-          const double va = vals[i0];
-          vals[i0] = vals[i1]; vals[i1] = va;
-        }
-      }
-      __syncthreads();
-    }
-  }
+  return act && lane == leader;
 }
 
 // Warp emit of a warp-private table keys/vals[0, T) holding nnz keys to
@@ -235,10 +218,98 @@ __device__ __forceinline__ void block_emit_unsorted(const uint32_t *keys, const 
   }
 }
 
+__device__ __forceinline__ int block_excl_scan_int(int v, int *s_warp, int *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int incl = warp_incl_scan(v);
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int x = lane < NW ? s_warp[lane] : 0;
+    const int xi = warp_incl_scan(x);
+    if (lane < NW) s_warp[lane] = xi - x;
+    if (lane == 31) s_warp[32] = xi;
+  }
+  __syncthreads();
+  const int r = s_warp[w] + incl - v;
+  *total = s_warp[32];
+  __syncthreads();
+  return r;
+}
+
+// a7 for a block-shared table: the row's nnz <= T/2 (key, value)
+// pairs sit compacted in keys/vals[0, nnz); store them to C at rp0 in
+// ascending column order by a bucket (counting) sort: T/2 buckets monotone in
+// the column, b(c) = (c - min) >> sh; position = bucket offset + rank among
+// the few keys of the bucket.  Scratch: keys[T/2, T) (bucket counters) and
+// vals[T/2, T) (per-key rank in bucket, keys grouped by bucket); s_red[66].
+__device__ __forceinline__ void block_bucket_sort_store(const uint32_t *keys, const double *vals,
+                                                        int T, int nnz, int64_t rp0,
+                                                        int32_t *__restrict__ c_col,
+                                                        double *__restrict__ c_val, int *s_red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int NB = T >> 1;
+  uint32_t *cnt = const_cast<uint32_t *>(keys) + NB;
+  uint32_t *loc = reinterpret_cast<uint32_t *>(const_cast<double *>(vals) + NB);
+  uint32_t *grp = loc + NB;
+  unsigned mn = 0xFFFFFFFFu, mx = 0u;
+  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+    const unsigned k = keys[e];
+    mn = k < mn ? k : mn;
+    mx = k > mx ? k : mx;
+  }
+  mn = __reduce_min_sync(kFull, mn);
+  mx = __reduce_max_sync(kFull, mx);
+  if (lane == 0) { s_red[w] = (int)mn; s_red[32 + w] = (int)mx; }
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) cnt[b] = 0u;
+  __syncthreads();
+  if (w == 0) {
+    unsigned a = lane < NW ? (unsigned)s_red[lane] : 0xFFFFFFFFu;
+    unsigned z = lane < NW ? (unsigned)s_red[32 + lane] : 0u;
+    a = __reduce_min_sync(kFull, a);
+    z = __reduce_max_sync(kFull, z);
+    if (lane == 0) { s_red[64] = (int)a; s_red[65] = (int)z; }
+  }
+  __syncthreads();
+  mn = (unsigned)s_red[64];
+  mx = (unsigned)s_red[65];
+  int sh = log2_ceil64(uint64_t(mx - mn) + 1) - (log2_ceil64(uint64_t(NB)));
+  sh = sh < 0 ? 0 : sh;
+  for (int e = threadIdx.x; e < nnz; e += blockDim.x) loc[e] = atomicAdd(cnt + ((keys[e] - mn) >> sh), 1u);
+  __syncthreads();
+  // exclusive scan of cnt[0, NB): thread owns a contiguous range
+  const int per = (NB + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(NB, (int)threadIdx.x * per), b1 = min(NB, b0 + per);
+  int mine = 0;
+  for (int b = b0; b < b1; ++b) mine += (int)cnt[b];
+  int tot;
+  int ex = block_excl_scan_int(mine, s_red, &tot);
+  for (int b = b0; b < b1; ++b) {
+    const int v = (int)cnt[b];
+    cnt[b] = (uint32_t)ex;
+    ex += v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+    const uint32_t k = keys[e];
+    grp[cnt[(k - mn) >> sh] + loc[e]] = k;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+    const uint32_t k = keys[e];
+    const uint32_t b = (k - mn) >> sh;
+    const int lo = (int)cnt[b];
+    const int hi = (int)b + 1 < NB ? (int)cnt[b + 1] : nnz;
+    int rnk = 0;
+    for (int q = lo; q < hi; ++q) rnk += grp[q] < k;
+    c_col[rp0 + lo + rnk] = (int32_t)k;
+    c_val[rp0 + lo + rnk] = vals[e];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // B tier: one block per row, keys/vals of T slots in dynamic smem, shared by
 // the block (atomic CAS for keys, atomic fp64 add for values).  Sorted output:
-// emit unordered into C, reload the row into smem, bitonic sort, store.
+// emit unordered into C, reload the row into smem, bucket-sort it into C (a7).
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict__ rows,
@@ -250,6 +321,7 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
                                                        int tmax) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_cnt;
+  __shared__ int s_red[66];
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5;
   double *vals = s_dyn_f64;
@@ -266,27 +338,24 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
       auto acc = [&](bool act, uint32_t c, double v) {
-        if (act) atomicAdd(vals + num_probe_smem(keys, c, logT), v);
+        if (act) atomicAdd(vals + num_probe_smem(keys, c, logT), v);  // c_ij <- c_ij + value (l.8)
+      };
+      auto acc_comb = [&](bool act, uint32_t c, double v) {  // keys may repeat in a round
+        if (warp_combine(act, c, v)) atomicAdd(vals + num_probe_smem(keys, c, logT), v);
       };
       if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc);
-      else for_row<false, true>(A, B, as, ae, w, NW, acc);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc_comb);
     }
     __syncthreads();
     block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
     if (sorted) {
       __syncthreads();
-      int P = 1;
-      while (P < nnz) P <<= 1;
-      for (int s = threadIdx.x; s < P; s += THREADS) {
-        if (s < nnz) { keys[s] = (uint32_t)c_col[rp0 + s]; vals[s] = c_val[rp0 + s]; }
-        else keys[s] = kEmpty;
+      for (int s = threadIdx.x; s < nnz; s += THREADS) {
+        keys[s] = (uint32_t)c_col[rp0 + s];
+        vals[s] = c_val[rp0 + s];
       }
       __syncthreads();
-      block_bitonic(keys, vals, P);
-      for (int s = threadIdx.x; s < nnz; s += THREADS) {
-        c_col[rp0 + s] = (int32_t)keys[s];
-        c_val[rp0 + s] = vals[s];
-      }
+      block_bucket_sort_store(keys, vals, T, nnz, rp0, c_col, c_val, s_red);
     }
     __syncthreads();
   }
@@ -491,100 +560,224 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // ---------------------------------------------------------------------------
 constexpr int kPartT = 2 * kPartKeys;               // table slots (load <= 1/2)
 constexpr int kSegSmem = 1024;                      // a_ik whose segments live in smem
-constexpr int kSegBytes = 28;                       // sb, se, pre (int32), sabs (int64), a (f64)
+constexpr int kSegBytes = 32;                       // pos, rend (int64), a (f64), nx, pre (int32)
 constexpr int kPartRankWords = int(kPartWidth / 32);
 constexpr size_t kPartSmem = size_t(kPartT) * 12 + size_t(kSegSmem) * kSegBytes + 16 +
                              size_t(kPartRankWords) * 6 +
                              size_t(kPartRankWords / kRankGroup) * 4 + size_t(kPartKeys) * 2;
 
-// first q in [s, len) with col[q] >= hi (col sorted), searching from s
-__device__ __forceinline__ int gallop_lb(const int32_t *__restrict__ col, int s, int len,
-                                         int64_t hi) {
-  if (s >= len || int64_t(__ldg(col + s)) >= hi) return s;
-  int lo = s, step = 1;  // invariant: col[lo] < hi
-  while (lo + step < len && int64_t(__ldg(col + lo + step)) < hi) {
-    lo += step;
-    step <<= 1;
-  }
-  int a = lo + 1, b = min(lo + step, len);
-  while (a < b) {
-    const int m = (a + b) >> 1;
-    if (int64_t(__ldg(col + m)) < hi) a = m + 1; else b = m;
-  }
-  return a;
-}
-
-// Per-entry segment arrays of a part (smem or global scratch).
+// Per-entry state of a row walked part by part (smem, or per-block global
+// scratch for rows with many a_ik).  Entry j = the row's j-th a_ik; its B row
+// occupies [B.rp[k], B.rp[k+1]) = [.., rend[j]).
 struct Segs {
-  int32_t *sb, *se, *pre;  // begin / end offsets in the B row; exclusive prefix of lengths
-  int64_t *sabs;           // absolute position of the segment start in B.col / B.val
-  double *a;               // a_ik
+  int64_t *pos;   // absolute start of the current part's segment in B.col / B.val
+  int64_t *rend;  // absolute end of the B row
+  double *a;      // a_ik
+  int32_t *nx;    // length of the current part's segment
+  int32_t *pre;   // exclusive prefix of nx over j (na + 1 entries)
 };
 
 __device__ __forceinline__ Segs segs_at(void *base, int cap) {
   Segs g;
-  g.sabs = reinterpret_cast<int64_t *>(base);
-  g.a = reinterpret_cast<double *>(g.sabs + cap);
-  g.sb = reinterpret_cast<int32_t *>(g.a + cap);
-  g.se = g.sb + cap;
-  g.pre = g.se + cap;  // cap + 1 entries
+  g.pos = reinterpret_cast<int64_t *>(base);
+  g.rend = g.pos + cap;
+  g.a = reinterpret_cast<double *>(g.rend + cap);
+  g.nx = reinterpret_cast<int32_t *>(g.a + cap);
+  g.pre = g.nx + cap;  // cap + 1 entries
   return g;
+}
+
+// Entry state at the start of row [as, as + na): one pass, cached for all parts.
+__device__ __forceinline__ void seg_init(const DevCSR &A, const DevCSR &B, int64_t as, int na,
+                                         const Segs &sg, int tid, int nth) {
+  for (int j = tid; j < na; j += nth) {
+    const int k = __ldg(A.col + as + j);
+    sg.pos[j] = __ldg(B.rp + k);
+    sg.rend[j] = __ldg(B.rp + k + 1);
+    sg.a[j] = __ldg(A.val + as + j);
+    sg.nx[j] = 0;
+  }
+}
+
+// first q in [s, r) with col[q] >= hi (col sorted), given col[s-1] < hi
+__device__ __forceinline__ int64_t gallop_abs(const int32_t *__restrict__ col, int64_t s,
+                                              int64_t r, int64_t hi) {
+  if (s >= r || int64_t(__ldg(col + s)) >= hi) return s;
+  int64_t lo = s, step = 1;  // invariant: col[lo] < hi
+  while (lo + step < r && int64_t(__ldg(col + lo + step)) < hi) {
+    lo += step;
+    step <<= 1;
+  }
+  int64_t x = lo + 1, y = lo + step < r ? lo + step : r;
+  while (x < y) {
+    const int64_t m = (x + y) >> 1;
+    if (int64_t(__ldg(col + m)) < hi) x = m + 1; else y = m;
+  }
+  return x;
+}
+
+// Segment ends of one part [lo, hi) for all entries of a team of nth threads
+// (a block or one warp): nx[j] = (first q >= pos[j] in the B row with
+// col[q] >= hi) - pos[j]; the last part takes the rest of every B row.
+// Latency-tolerant (the searches are chains of dependent loads):
+//  - few entries: G = 2^g lanes per entry run a G-ary search (one ballot per
+//    step narrows the range G+1 times: ~log_{G+1}(len) dependent loads);
+//  - many entries: a thread takes 4 entries at a time and reads 4 consecutive
+//    columns of each (16 independent loads in flight), which settles the short
+//    segments of long rows at once; longer ones gallop on.
+__device__ __forceinline__ void seg_search(const int32_t *__restrict__ bcol, const Segs &sg, int na,
+                                           int64_t hi, bool last, int tid, int nth) {
+  // every entry first moves past the previous part's segment (pos += nx)
+  if (last) {
+    for (int j = tid; j < na; j += nth) {
+      const int64_t p = sg.pos[j] + sg.nx[j];
+      sg.pos[j] = p;
+      sg.nx[j] = (int)(sg.rend[j] - p);
+    }
+    return;
+  }
+  int G = 1;
+  while (G < 32 && int64_t(G) * 2 * na <= nth) G <<= 1;
+  if (G >= 4) {
+    const int lane = tid & 31;
+    const int gb = lane & ~(G - 1), gl = lane & (G - 1);
+    const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << gb);
+    const int ngroups = nth / G;
+    for (int j = tid / G; j < na; j += ngroups) {  // same j sequence for the whole group
+      const int64_t p0 = sg.pos[j] + sg.nx[j];
+      int64_t lo = p0, up = sg.rend[j];  // the answer lies in [lo, up]
+      while (up > lo) {
+        const int64_t len = up - lo;
+        if (len <= G) {
+          const bool ge = gl < len && int64_t(__ldg(bcol + lo + gl)) >= hi;
+          const unsigned b = __ballot_sync(gmask, ge) >> gb;
+          lo = b ? lo + __ffs(b) - 1 : up;
+          break;
+        }
+        const int64_t q = lo + (len * (gl + 1)) / (G + 1);  // strictly increasing in gl
+        const bool ge = int64_t(__ldg(bcol + q)) >= hi;
+        const unsigned b = (__ballot_sync(gmask, ge) >> gb) & (G == 32 ? kFull : ((1u << G) - 1u));
+        const int f = b ? __ffs(b) - 1 : G;  // first probe >= hi
+        const int64_t nlo = f > 0 ? lo + (len * f) / (G + 1) + 1 : lo;
+        if (f < G) up = lo + (len * (f + 1)) / (G + 1);
+        lo = nlo;
+      }
+      __syncwarp(gmask);
+      if (gl == 0) {
+        sg.pos[j] = p0;
+        sg.nx[j] = (int)(lo - p0);
+      }
+    }
+    return;
+  }
+  for (int j0 = tid; j0 < na; j0 += 4 * nth) {
+    int64_t p[4], r[4];
+    int32_t c[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * nth;
+      p[u] = j < na ? sg.pos[j] + sg.nx[j] : 0;
+      r[u] = j < na ? sg.rend[j] : 0;
+#pragma unroll
+      for (int d = 0; d < 4; ++d)
+        c[u][d] = p[u] + d < r[u] ? __ldg(bcol + p[u] + d) : INT32_MAX;  // INT32_MAX >= any hi
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * nth;
+      if (j >= na) continue;
+      int d = 0;
+#pragma unroll
+      for (int t = 3; t >= 0; --t)
+        if (int64_t(c[u][t]) >= hi) d = t;
+      int64_t e;
+      if (int64_t(c[u][0]) >= hi) e = p[u];
+      else if (int64_t(c[u][3]) >= hi) e = p[u] + d;
+      else e = gallop_abs(bcol, p[u] + 4, r[u], hi);
+      sg.pos[j] = p[u];
+      sg.nx[j] = (int)(e - p[u]);
+    }
+  }
+}
+
+// Number of lanes whose (nondecreasing across lanes) value wv is <= x: 0..32.
+__device__ __forceinline__ int count_le(int wv, int x) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const int v = __shfl_sync(kFull, wv, pos + s - 1);
+    if (v <= x) pos += s;
+  }
+  const int last = __shfl_sync(kFull, wv, 31);  // (all lanes shuffle)
+  if (pos == 31 && last <= x) pos = 32;
+  return pos;
+}
+
+// Owner entry of product x (x < P): the last j with pre[j] <= x, searched
+// from entry jb (pre[jb] <= every product of the round) in windows of 32
+// boundaries pre[jb+1 .. jb+32] loaded by the warp at once.  All lanes call.
+__device__ __forceinline__ int part_owner(const int32_t *__restrict__ pre, int na, int jb, int x,
+                                          bool act) {
+  const int lane = lane_id();
+  int own = act ? -1 : 0;
+  while (true) {
+    const int e = jb + 1 + lane;
+    const int wv = e <= na ? pre[e] : INT32_MAX;
+    const int c = count_le(wv, x);
+    if (own < 0 && c < 32) own = jb + c;
+    if (__all_sync(kFull, own >= 0)) break;
+    jb += 32;
+  }
+  return own;
 }
 
 // Flat enumeration of the products of one part: product p (0 <= p < P) lies
 // in the segment of entry j with pre[j] <= p < pre[j+1].  Rounds [g0, g1) of
-// 32 consecutive products; each lane keeps its owner entry j and advances it
-// (products of a lane increase by 32 per round).  Two rounds in flight.
-template <typename F>
+// 32 consecutive products, owners found by part_owner windows.
+constexpr int kPartChunk = 8;  // rounds a warp takes at a time in the block-part kernel
+constexpr int kWalkMinEntries = 512;
+constexpr int kWalkU = 2;  // entries a thread walks at once  // rows with >= this many a_ik: entry walk per part
+
+template <int kD = 4, typename F>
 __device__ __forceinline__ void for_part_rounds(const DevCSR &B, const Segs &sg, int na, int P,
                                                 int g0, int g1, F &&f) {
   if (g0 >= g1) return;
   const int lane = lane_id();
-  int p = g0 * 32 + lane;
-  int lo = 0, hi = na;  // owner: last j with pre[j] <= p
-  while (hi - lo > 1) {
-    const int m = (lo + hi) >> 1;
-    if (sg.pre[m] <= p) lo = m; else hi = m;
-  }
-  int j = lo;
-  for (int g = g0; g < g1; g += 2, p += 64) {
-    const bool act0 = p < P;
-    const bool act1 = (g + 1 < g1) && (p + 32 < P);
-    uint32_t c0 = 0u, c1 = 0u;
-    double v0 = 0.0, v1 = 0.0;
-    if (act0) {
-      while (j + 1 < na && sg.pre[j + 1] <= p) ++j;
-      const int64_t q = sg.sabs[j] + (p - sg.pre[j]);
-      c0 = (uint32_t)__ldg(B.col + q);
-      v0 = sg.a[j] * __ldg(B.val + q);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+  int jb;  // owner of the next round's first product (warp-uniform)
+  {
+    const int x = g0 * 32;
+    int lo = 0, hi = na;  // last j with pre[j] <= x
+    while (hi - lo > 1) {
+      const int m = (lo + hi) >> 1;
+      if (sg.pre[m] <= x) lo = m; else hi = m;
     }
-    if (act1) {
-      while (j + 1 < na && sg.pre[j + 1] <= p + 32) ++j;
-      const int64_t q = sg.sabs[j] + (p + 32 - sg.pre[j]);
-      c1 = (uint32_t)__ldg(B.col + q);
-      v1 = sg.a[j] * __ldg(B.val + q);
+    jb = lo;
+  }
+  // batches of kD rounds: owners and gather addresses of all kD rounds first,
+  // then the kD gathers (independent loads in flight), then the kD updates
+  for (int g = g0; g < g1; g += kD) {
+    uint32_t c[kD];
+    double v[kD];
+    bool act[kD];
+    int64_t q[kD];
+    double a[kD];
+#pragma unroll
+    for (int d = 0; d < kD; ++d) {
+      const int x = (g + d) * 32 + lane;
+      act[d] = (g + d < g1) && x < P;
+      const int j = part_owner(sg.pre, na, jb, x, act[d]);
+      jb = __shfl_sync(kFull, act[d] ? j : jb, 31);
+      q[d] = act[d] ? sg.pos[j] + (x - sg.pre[j]) : 0;
+      a[d] = act[d] ? sg.a[j] : 0.0;
     }
-    f(act0, c0, v0);
-    f(act1, c1, v1);
+#pragma unroll
+    for (int d = 0; d < kD; ++d) {
+      c[d] = act[d] ? (uint32_t)__ldg(B.col + q[d]) : 0u;
+      v[d] = act[d] ? __ldg(B.val + q[d]) : 0.0;
+    }
+#pragma unroll
+    for (int d = 0; d < kD; ++d) f(act[d], c[d], a[d] * v[d]);  // a_ik * b_kj (Fig:code_spgemm l.5)
   }
-}
-
-__device__ __forceinline__ int block_excl_scan_int(int v, int *s_warp, int *total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
-  const int incl = warp_incl_scan(v);
-  if (lane == 31) s_warp[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    const int x = lane < NW ? s_warp[lane] : 0;
-    const int xi = warp_incl_scan(x);
-    if (lane < NW) s_warp[lane] = xi - x;
-    if (lane == 31) s_warp[32] = xi;
-  }
-  __syncthreads();
-  const int r = s_warp[w] + incl - v;
-  *total = s_warp[32];
-  __syncthreads();
-  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -606,13 +799,11 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
     int32_t *__restrict__ c_col, double *__restrict__ c_val, int sorted,
     const int2 *__restrict__ parts, const int32_t *__restrict__ part_off,
     const int32_t *__restrict__ part_n, char *__restrict__ seg_scratch, int64_t seg_cap,
-    unsigned long long *row_counter) {
+    unsigned long long *row_counter, int tune, unsigned long long *dbg) {
   extern __shared__ double s_dyn_f64[];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_round;
   __shared__ int s_warp[33];
   __shared__ long long s_row;
-  constexpr int NW = THREADS / 32;
-  const int w = threadIdx.x >> 5;
   double *vals = s_dyn_f64;
   uint32_t *keys = reinterpret_cast<uint32_t *>(vals + kPartT);
   char *seg_smem = reinterpret_cast<char *>(keys + kPartT);
@@ -636,68 +827,159 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
     Segs sg = na <= kSegSmem ? segs_at(seg_smem, kSegSmem)
                              : segs_at(seg_scratch + int64_t(blockIdx.x) * seg_cap * kSegBytes,
                                        (int)seg_cap);
-    for (int j = threadIdx.x; j < na; j += THREADS) {
-      sg.sb[j] = 0;
-      const int k = __ldg(A.col + as + j);
-      sg.sabs[j] = __ldg(B.rp + k);  // B row start (the segment offset is added per part)
-      sg.a[j] = __ldg(A.val + as + j);
-    }
-    __syncthreads();
+    seg_init(A, B, as, na, sg, threadIdx.x, THREADS);
     const int per = (na + THREADS - 1) / THREADS;  // entries per thread for the scan
+    const bool walk = na >= kWalkMinEntries && (tune & 4);  // (entry walk: measurement only)
     for (int p = 0; p < np; ++p) {
       const int2 Pp = pr[p];
       const int64_t hi = p + 1 < np ? int64_t(pr[p + 1].x) : B.ncols;
       const int cnt = (p + 1 < np ? pr[p + 1].y : nnz) - Pp.y;
       const int logT = num_log2(cnt);
       const int T = 1 << logT;
+      const bool instr = (tune & 8) && threadIdx.x == 0;
+      const long long t0 = instr ? clock64() : 0;
       for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
-      // segment ends and lengths (thread owns entries [t*per, t*per + per))
-      int mine = 0;
-      for (int j = threadIdx.x * per; j < na && j < (threadIdx.x + 1) * per; ++j) {
-        const int k = __ldg(A.col + as + j);
-        const int len = (int)(__ldg(B.rp + k + 1) - __ldg(B.rp + k));
-        const int64_t bs0 = __ldg(B.rp + k);
-        const int e = p + 1 == np ? len : gallop_lb(B.col + bs0, sg.sb[j], len, hi);
-        sg.se[j] = e;
-        sg.sabs[j] = bs0 + sg.sb[j];  // absolute segment start for this part
-        mine += e - sg.sb[j];
+      if (threadIdx.x == 0) {
+        s_cnt = 0;
+        s_round = 0;
       }
+      __syncthreads();  // seg_init / the previous part's pos update are visible
+      long long t1 = 0, t2 = 0;
+      if (walk) {
+        // entry walk (rows with many a_ik: short segments per part): thread
+        // per entry, kWalkU entries at a time, 4 columns read ahead each; the
+        // products c < hi of the B row are applied in place and pos[j] moves
+        // past them.  No search, scan or owner lookup.
+        t1 = t2 = instr ? clock64() : 0;
+        auto ins = [&](uint32_t c, double v) {
+          bool isnew = false;
+          const uint32_t slot = probe_chunk(keys, c, logT, &isnew);
+          atomicAdd(vals + slot, v);  // c_ij <- c_ij + value (l.8)
+          if (isnew) slot_of[atomicAdd(&s_cnt, 1)] = (uint16_t)slot;
+        };
+        for (int j0 = threadIdx.x; j0 < na; j0 += kWalkU * THREADS) {
+          int64_t q[kWalkU], r[kWalkU];
+          double aa[kWalkU];
+          bool live[kWalkU];
+#pragma unroll
+          for (int u = 0; u < kWalkU; ++u) {
+            const int j = j0 + u * THREADS;
+            live[u] = j < na;
+            q[u] = live[u] ? sg.pos[j] : 0;
+            r[u] = live[u] ? sg.rend[j] : 0;
+            aa[u] = live[u] ? sg.a[j] : 0.0;
+          }
+          while (true) {
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < kWalkU; ++u) any |= live[u];
+            if (!any) break;
+            int32_t c[kWalkU][4];
+#pragma unroll
+            for (int u = 0; u < kWalkU; ++u)
+#pragma unroll
+              for (int d = 0; d < 4; ++d)
+                c[u][d] = (live[u] && q[u] + d < r[u]) ? __ldg(B.col + q[u] + d) : INT32_MAX;
+#pragma unroll
+            for (int u = 0; u < kWalkU; ++u) {
+              if (!live[u]) continue;
+              int n = 0;
+#pragma unroll
+              for (int d = 0; d < 4; ++d) n += int64_t(c[u][d]) < hi;  // sorted: a prefix
+              double v[4];
+#pragma unroll
+              for (int d = 0; d < 4; ++d) v[d] = d < n ? __ldg(B.val + q[u] + d) : 0.0;
+#pragma unroll
+              for (int d = 0; d < 4; ++d)
+                if (d < n) ins((uint32_t)c[u][d], aa[u] * v[d]);  // a_ik * b_kj (l.5)
+              q[u] += n;
+              if (n < 4) {
+                live[u] = false;
+                sg.pos[j0 + u * THREADS] = q[u];
+              }
+            }
+          }
+        }
+      } else {
+      seg_search(B.col, sg, na, hi, p + 1 == np, threadIdx.x, THREADS);
+      __syncthreads();
+      t1 = instr ? clock64() : 0;
+      // exclusive prefix of the segment lengths (thread owns entries [t*per, t*per + per))
+      const int jlo = min(na, threadIdx.x * per), jhi = min(na, jlo + per);
+      int mine = 0;
+      for (int j = jlo; j < jhi; ++j) mine += sg.nx[j];
       int P;
       int ex = block_excl_scan_int(mine, s_warp, &P);  // (contains the barriers)
-      for (int j = threadIdx.x * per; j < na && j < (threadIdx.x + 1) * per; ++j) {
-        sg.pre[j] = ex;
-        ex += sg.se[j] - sg.sb[j];
+      for (int j = jlo; j < jhi; j += 8) {  // nx loads batched ahead of the pre stores
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = j + u < jhi ? sg.nx[j + u] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j + u < jhi) {
+            sg.pre[j + u] = ex;
+            ex += v[u];
+          }
       }
-      if (threadIdx.x == 0) {
-        sg.pre[na] = P;
-        s_cnt = 0;
-      }
+      if (threadIdx.x == 0) sg.pre[na] = P;
       __syncthreads();
+      t2 = instr ? clock64() : 0;
       const int R = (P + 31) >> 5;
-      // accumulate; newly inserted keys are appended to the insertion list
-      for_part_rounds(B, sg, na, P, (int)((int64_t)R * w / NW), (int)((int64_t)R * (w + 1) / NW),
-                      [&](bool act, uint32_t c, double v) {
-                        bool isnew = false;
-                        uint32_t slot = 0;
-                        if (act) {
-                          slot = probe_chunk(keys, c, logT, &isnew);
-                          atomicAdd(vals + slot, v);  // c_ij <- c_ij + value (l.8)
-                        }
-                        const unsigned m = __ballot_sync(kFull, isnew);
-                        if (m) {
-                          const int leader = __ffs(m) - 1;
-                          int base = 0;
-                          if (lane == leader) base = atomicAdd(&s_cnt, __popc(m));
-                          base = __shfl_sync(kFull, base, leader);
-                          if (isnew) slot_of[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)slot;
-                        }
-                      });
-      for (int j = threadIdx.x; j < na; j += THREADS) sg.sb[j] = sg.se[j];
-      __syncthreads();
+      // accumulate: flat rounds of 32 products, equal contiguous ranges of
+      // rounds per warp (SPG_TUNE bit 2: chunks from a shared counter; bit 1:
+      // combine equal keys of a round first); newly inserted keys are
+      // appended to the insertion list
+      const bool comb = (tune & 1) != 0;
+      auto acc = [&](bool act, uint32_t c, double v) {
+        const bool lead = comb ? warp_combine(act, c, v) : act;
+        bool isnew = false;
+        uint32_t slot = 0;
+        if (lead) {
+          slot = probe_chunk(keys, c, logT, &isnew);
+          if (tune & 48) {  // measurement only (wrong values): 16 racy add, 32 no add
+            if (tune & 16) vals[slot] += v;
+          } else {
+            atomicAdd(vals + slot, v);  // c_ij <- c_ij + value (l.8)
+          }
+        }
+        const unsigned m = __ballot_sync(kFull, isnew);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(&s_cnt, __popc(m));
+          base = __shfl_sync(kFull, base, leader);
+          if (isnew) slot_of[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)slot;
+        }
+      };
+      if (!(tune & 2)) {
+        const int w = threadIdx.x >> 5, NW = THREADS / 32;
+        for_part_rounds(B, sg, na, P, (int)((int64_t)R * w / NW), (int)((int64_t)R * (w + 1) / NW), acc);
+      } else {
+        while (true) {
+          int g0 = 0;
+          if (lane == 0) g0 = atomicAdd(&s_round, kPartChunk);
+          g0 = __shfl_sync(kFull, g0, 0);
+          if (g0 >= R) break;
+          for_part_rounds(B, sg, na, P, g0, min(g0 + kPartChunk, R), acc);
+        }
+      }
+      }
+      __syncthreads();  // every warp is done reading this part's segments
+      long long t3 = instr ? clock64() : 0;
       const int64_t width = (hi - Pp.x) < kPartWidth ? (hi - Pp.x) : kPartWidth;
       block_list_emit(keys, vals, slot_of, cnt, Pp.x, width, bm, wpre, gpre, &s_cnt, rp0 + Pp.y,
                       c_col, c_val, sorted);
       __syncthreads();
+      if (instr) {
+        const long long t4 = clock64();
+        atomicAdd(dbg + 0, 1ull);                              // parts
+        atomicAdd(dbg + 1, (unsigned long long)(t1 - t0));     // init + segment search
+        atomicAdd(dbg + 2, (unsigned long long)(t2 - t1));     // scan
+        atomicAdd(dbg + 3, (unsigned long long)(t3 - t2));     // accumulate
+        atomicAdd(dbg + 4, (unsigned long long)(t4 - t3));     // emit
+        atomicAdd(dbg + 5, (unsigned long long)walk);          // parts walked
+        atomicAdd(dbg + 6, (unsigned long long)na);            // entries walked
+      }
     }
   }
 }
@@ -713,7 +995,7 @@ __global__ void __launch_bounds__(THREADS) k_num_part(
 // ---------------------------------------------------------------------------
 constexpr int kWPartT = 2 * kWPartKeys;
 constexpr size_t kWPartSmemPerWarp =  // multiple of 16 B: 128-bit chunk loads stay aligned
-    (size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * kSegBytes + 8 + 15) & ~size_t(15);
+    (size_t(kWPartT) * 16 + size_t(kWPartMaxEntries) * kSegBytes + 16 + 15) & ~size_t(15);
 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
@@ -741,10 +1023,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
     const int na = (int)(A.rp[i + 1] - as);
     const int np = -part_n[i];
     const int2 *pr = parts + part_off[i];
-    for (int j = lane; j < na; j += 32) {
-      sg.sb[j] = 0;
-      sg.a[j] = __ldg(A.val + as + j);
-    }
+    seg_init(A, B, as, na, sg, lane, 32);
     __syncwarp();
     for (int p = 0; p < np; ++p) {
       const int2 Pp = pr[p];
@@ -753,19 +1032,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
       const int logT = num_log2(cntp);
       const int T = 1 << logT;
       for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
+      seg_search(B.col, sg, na, hi, p + 1 == np, lane, 32);
+      __syncwarp();
       int carry = 0;
-      for (int j0 = 0; j0 < na; j0 += 32) {  // segment ends, exclusive prefix of lengths
+      for (int j0 = 0; j0 < na; j0 += 32) {  // exclusive prefix of the segment lengths
         const int j = j0 + lane;
-        int L = 0;
-        if (j < na) {
-          const int k = __ldg(A.col + as + j);
-          const int64_t bs0 = __ldg(B.rp + k);
-          const int len = (int)(__ldg(B.rp + k + 1) - bs0);
-          const int e = p + 1 == np ? len : gallop_lb(B.col + bs0, sg.sb[j], len, hi);
-          sg.se[j] = e;
-          sg.sabs[j] = bs0 + sg.sb[j];
-          L = e - sg.sb[j];
-        }
+        const int L = j < na ? sg.nx[j] : 0;
         const int incl = warp_incl_scan(L);
         if (j < na) sg.pre[j] = carry + incl - L;
         carry += __shfl_sync(kFull, incl, 31);
@@ -784,7 +1056,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_num_wpart(
         __syncwarp();
       });
       warp_emit(keys, vals, cnt, T, logT, cntp, rp0 + Pp.y, c_col, c_val, sorted);
-      for (int j = lane; j < na; j += 32) sg.sb[j] = sg.se[j];
       __syncwarp();
     }
   }

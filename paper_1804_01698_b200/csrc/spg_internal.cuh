@@ -50,6 +50,7 @@ struct PlanInfo {
   unsigned long long parts_overflow;
   unsigned long long row_counter;   // dynamic row queue of the numeric G tier
   unsigned long long row_counter_w; // dynamic row queue of the warp-part tier
+  unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)
 };
 
 __host__ __device__ __forceinline__ int log2_ceil64(uint64_t x) {  // smallest n: 2^n >= x

@@ -46,6 +46,7 @@ struct spg_ctx {
   cudaEvent_t ev_join[kSubStreams] = {};
   int64_t launches = 0;
   int serial = 0;  // SPG_SERIAL_BINS=1: all bins on the caller's stream (diagnosis)
+  int tune = 0;    // SPG_TUNE=<bits>: kernel variant switches for A/B measurements (default 0)
   // optional per-launch timing (events on the stream each kernel runs on)
   int profiling = 0;
   struct Rec { const char *name; cudaEvent_t a, b; };
@@ -264,6 +265,8 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
   {
     const char *e = getenv("SPG_SERIAL_BINS");
     c->serial = (e && e[0] == '1') ? 1 : 0;
+    const char *t = getenv("SPG_TUNE");
+    c->tune = t ? atoi(t) : 0;
   }
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) c->num_sms = v;
@@ -616,7 +619,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
         k_num_part<1024><<<(unsigned)g_grid, 1024, kPartSmem, ss>>>(
             rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
             (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p, (char *)c->seg.p,
-            seg_cap, &((PlanInfo *)c->info.p)->row_counter);
+            seg_cap, &((PlanInfo *)c->info.p)->row_counter, c->tune, ((PlanInfo *)c->info.p)->dbg);
       }
       SPG_LAUNCHED(c, "k_num_part");
     } else {  // NB_G
@@ -631,6 +634,15 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
     }
   }
   return join(c, s);
+}
+
+spg_status spg_debug_counters(spg_ctx *c, int64_t *out, void *stream) {
+  if (!c || !out) return SPG_ERR_INVALID_ARG;
+  if (!c->info.p) return fail(c, SPG_ERR_STATE, "no plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaMemcpyAsync(out, ((PlanInfo *)c->info.p)->dbg, 16 * 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  return SPG_OK;
 }
 
 spg_status spg_plan_export(spg_ctx *c, int64_t *flop_out, int64_t *tsize_out, void *stream) {

@@ -36,5 +36,6 @@ for _ in range(a.reps):
         _lib.spg_profile_enable(ctx.handle, False)
         print([(n, round(t, 3)) for n, t in _lib.spg_profile_records(ctx.handle)], flush=True)
         print(ctx.info(), flush=True)
+        print("dbg", _lib.spg_debug_counters(ctx.handle), flush=True)
     del C
 print("ok", ctx.info()["nnz_total"], ctx.launches)
