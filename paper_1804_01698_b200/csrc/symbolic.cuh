@@ -78,12 +78,50 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
     if (cb + lane < nent) en = entry(cb + lane);
     if (kSeq && own_chunks && __all_sync(kFull, en.len <= 32)) {
       // this warp owns the chunk and every B row fits one round: one round per
-      // nonempty entry.  Rolling software pipeline over kDepth register slots
-      // (deep for the block / bitmap tiers, 1 for the occupancy-bound warp tiers):
-      // slot d holds the gathered (b_kj, a_ik) of a round; right after a
-      // round is hashed its slot is refilled with the round kDepth ahead, so
-      // kDepth independent gathers stay in flight per lane.
+      // nonempty entry.  kDepth <= 2 (warp tiers, occupancy-bound): one round
+      // ahead.  Deeper (block / bitmap tiers): rolling software pipeline over
+      // kDepth register slots -- slot d holds the gathered (b_kj, a_ik) of a
+      // round; right after a round is hashed its slot is refilled with the
+      // round kDepth ahead, so kDepth independent gathers stay in flight.
       unsigned pend = __ballot_sync(kFull, en.len > 0);
+      if constexpr (kDepth <= 2) {
+        // one round ahead: the gathers of the next round are issued before
+        // this one is hashed
+        if (!pend) continue;
+        int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        int L = __shfl_sync(kFull, en.len, j);
+        double aj = kVal ? shfl_f64(en.a, j) : 0.0;
+        int64_t jbs = shfl_i64(en.bs, j);
+        bool act = lane < L;
+        uint32_t c = act ? (uint32_t)__ldg(B.col + jbs + lane) : 0u;
+        double bv = (kVal && act) ? __ldg(B.val + jbs + lane) : 0.0;
+        while (true) {
+          const bool more = pend != 0;
+          int nL = 0;
+          double na = 0.0;
+          uint32_t nc = 0u;
+          double nbv = 0.0;
+          if (more) {
+            const int nj = __ffs(pend) - 1;
+            pend &= pend - 1;
+            nL = __shfl_sync(kFull, en.len, nj);
+            if (kVal) na = shfl_f64(en.a, nj);
+            const int64_t nbs = shfl_i64(en.bs, nj);
+            if (lane < nL) {
+              nc = (uint32_t)__ldg(B.col + nbs + lane);
+              if (kVal) nbv = __ldg(B.val + nbs + lane);
+            }
+          }
+          f(act, c, aj * bv);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+          if (!more) break;
+          act = lane < nL;
+          c = nc;
+          bv = nbv;
+          aj = na;
+        }
+        continue;
+      }
       int sl[kDepth];
       uint32_t sc[kDepth];
       double sb[kDepth], sa[kDepth];
