@@ -136,8 +136,7 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
                                                      const int64_t *__restrict__ arp,
                                                      int64_t ncols, int mode, PlanInfo *info,
                                                      int32_t *__restrict__ rows_out,
-                                                     int64_t *__restrict__ row_nnz,
-                                                     const int32_t *__restrict__ part_n) {
+                                                     int64_t *__restrict__ row_nnz) {
   __shared__ unsigned s_cnt[kMaxBins];
   __shared__ unsigned long long s_base[kMaxBins];
   if (threadIdx.x < kMaxBins) s_cnt[threadIdx.x] = 0;
@@ -150,7 +149,7 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
       b = sym_bin(key[i], ncols, arp[i + 1] - arp[i]);
       if (b == SB_SKIP) row_nnz[i] = 0;
     } else {
-      b = num_bin_row(key[i + 1] - key[i], arp[i + 1] - arp[i], part_n, i);
+      b = num_bin(key[i + 1] - key[i], arp[i + 1] - arp[i]);
     }
     if (b != 0) local = atomicAdd(&s_cnt[b], 1u);
   }
@@ -240,7 +239,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partials(int64_t *__restr
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict__ data, int64_t n,
                                                             const int64_t *__restrict__ partial,
                                                             PlanInfo *info,
-                                                            const int32_t *__restrict__ part_n,
                                                             const int64_t *__restrict__ arp) {
   __shared__ long long s_warp[33];
   __shared__ unsigned s_bins[kMaxBins];
@@ -262,7 +260,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
 #pragma unroll
   for (int t = 0; t < kScanItems; ++t)
     if (arp && base + t < n && v[t] > 0)
-      atomicAdd(&s_bins[num_bin_row(v[t], arp[base + t + 1] - arp[base + t], part_n, base + t)], 1u);
+      atomicAdd(&s_bins[num_bin(v[t], arp[base + t + 1] - arp[base + t])], 1u);
   long long tot;
   long long ex = block_excl_scan_1024(s, s_warp, &tot) + partial[blockIdx.x];
 #pragma unroll
@@ -294,6 +292,35 @@ __global__ void __launch_bounds__(256) k_check_sorted(DevCSR B, PlanInfo *info) 
     bad = __any_sync(kFull, bad);
   }
   if (bad && lane == 0) atomicOr(&info->b_unsorted, 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// Column-tile offsets of B (long-row tier): toff[k*(ntiles+1) + t] = absolute
+// position of the first entry of B row k with column >= t*kTileCols (B.rp[k+1]
+// if none); needs strictly increasing rows.  Warp per row: lane l looks at
+// entry q and fills the tiles that begin after the previous entry's column and
+// at or before its own.  Positions fit int32 (checked by the host).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_tile_offsets(DevCSR B, int ntiles, int32_t *__restrict__ toff) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t k = warp; k < B.nrows; k += nwarps) {
+    const int64_t s = B.rp[k], e = B.rp[k + 1];
+    int32_t *o = toff + k * (ntiles + 1);
+    int prev_tile = -1;  // tile of the entry before this chunk's first (-1: none)
+    for (int64_t q0 = s; q0 < e; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const int tc = q < e ? (__ldg(B.col + q) >> kTileLog) : ntiles;
+      int tp = __shfl_up_sync(kFull, tc, 1);
+      if (lane == 0) tp = prev_tile;
+      if (q < e)
+        for (int t = tp + 1; t <= tc; ++t) o[t] = (int32_t)q;
+      const int lastlane = (e - q0) < 32 ? int(e - q0) - 1 : 31;
+      prev_tile = __shfl_sync(kFull, tc, lastlane);
+    }
+    for (int t = prev_tile + 1 + lane; t <= ntiles; t += 32) o[t] = (int32_t)e;  // after the last entry
+  }
 }
 
 // ---------------------------------------------------------------------------

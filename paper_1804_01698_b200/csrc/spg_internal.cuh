@@ -20,8 +20,7 @@ constexpr int64_t kMaxBRow = int64_t(1) << 26;  // 32 rows * 2^26 < 2^31 per chu
 // (load <= 1/2, reading R6).
 enum SymBin { SB_SKIP = 0, SB_W128, SB_W1024, SB_B2K, SB_B4K, SB_B8K, SB_B16K, SB_B32K,
               SB_G, SB_BM, SB_COUNT };
-enum NumBin { NB_SKIP = 0, NB_W256, NB_W1024, NB_B2K, NB_B4K, NB_B8K, NB_B16K, NB_G, NB_GW,
-              NB_COUNT };
+enum NumBin { NB_SKIP = 0, NB_W256, NB_W1024, NB_B2K, NB_B4K, NB_B8K, NB_B16K, NB_G, NB_COUNT };
 constexpr int kMaxBins = 12;
 
 struct DevCSR {
@@ -48,8 +47,8 @@ struct PlanInfo {
   unsigned long long b_unsorted;  // 1 if some B row is not strictly increasing
   unsigned long long parts_used;  // bump allocator of the parts buffer
   unsigned long long parts_overflow;
-  unsigned long long row_counter;   // dynamic row queue of the numeric G tier
-  unsigned long long row_counter_w; // dynamic row queue of the warp-part tier
+  unsigned long long row_counter;   // dynamic work queue of the numeric G tier
+  unsigned long long b_end;         // B.row_ptr[B.nrows] (tile offsets are int32 positions)
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)
 };
 
@@ -102,17 +101,17 @@ __device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols, int64_t na) 
   return SB_G;
 }
 
-// Column-range parts of a long row (numeric G tier): at most kPartKeys keys
-// and at most kPartWidth columns each.
-constexpr int kPartKeys = 4096;
-constexpr int kPartWidthLog = 18;
-constexpr int64_t kPartWidth = int64_t(1) << kPartWidthLog;
-constexpr int kMaxPartsPerRow = 512;  // >= kBitmapMaxCols / kPartKeys + kBitmapMaxCols / kPartWidth + 2
-// Rows with few a_ik are cut into small WARP parts instead (one warp per
-// part, warp-private table): rank cuts every kWPartKeys keys.
-constexpr int kWPartKeys = 256;
-constexpr int kWPartMaxEntries = 64;
-
+// Column tiles of the long-row tier (numeric G tier, B rows sorted): every B
+// row is cut at multiples of kTileCols columns (tile offsets built once per
+// multiply, k_tile_offsets), and a long row of C is cut into PARTS = runs of
+// consecutive tiles holding <= kTPartKeys keys (smem hash table) or one tile
+// holding more (dense smem window).  Rows with nnz(c_i) > kPartMinKeys get
+// parts (the numeric G bin).
+constexpr int kTileLog = 13;
+constexpr int kTileCols = 1 << kTileLog;
+constexpr int kTPartKeys = 2048;
+constexpr int kPartMinKeys = 8192;
+constexpr int kMaxTiles = 256;  // >= kBitmapMaxCols / kTileCols + 1
 
 __device__ __forceinline__ int num_log2(int64_t nnz) {
   int n = log2_ceil64(uint64_t(2 * nnz));
@@ -127,14 +126,6 @@ __device__ __forceinline__ int num_bin(int64_t nnz, int64_t na) {
   if (n <= 10) return NB_W1024;
   if (n <= 14) return NB_B2K + (n - 11);
   return NB_G;
-}
-
-// numeric bin of a row, with the part kind of long rows (part_n < 0: warp parts)
-__device__ __forceinline__ int num_bin_row(int64_t nnz, int64_t na, const int32_t *part_n,
-                                           int64_t i) {
-  const int b = num_bin(nnz, na);
-  if (b == NB_G && part_n != nullptr && part_n[i] < 0) return NB_GW;
-  return b;
 }
 
 // Fibonacci hashing: HIGH bits of col*H (reading R5 of DESIGN.md; the paper's

@@ -38,7 +38,7 @@ struct spg_ctx {
   void *user = nullptr;
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
-  Buf parts, part_off, part_n, seg;  // column-range parts of long rows (BM tier)
+  Buf parts, part_row, part_n, toff;  // column-tile parts of long rows (BM tier), B tile offsets
   bool plan_parts = false;           // parts were produced for the numeric G tier
   PlanInfo *host_info = nullptr;  // pinned
   cudaStream_t sub[kSubStreams] = {};
@@ -201,7 +201,7 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
 
 // scan of data[0..n) in place (int64), numeric-bin counting in the last pass
 spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
-                       const int32_t *part_n = nullptr, const int64_t *arp = nullptr) {
+                       const int64_t *arp = nullptr) {
   if (n == 0) return SPG_OK;
   const int64_t nb = ceil_div(n, kScanTile);
   SPG_CUDA(c, cudaGetLastError());
@@ -220,8 +220,7 @@ spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
   SPG_LAUNCHED(c, "k_scan_partials");
   {
     ProfScope _ps(c, s, "k_scan_down");
-    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p,
-                                                      part_n, arp);
+    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p, arp);
   }
   SPG_LAUNCHED(c, "k_scan_down");
   return SPG_OK;
@@ -287,8 +286,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_block<512>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
-         set_smem(c, k_num_part<1024>, kPartSmem) == SPG_OK &&
-         set_smem(c, k_num_wpart<4>, 4 * kWPartSmemPerWarp) == SPG_OK &&
+         set_smem(c, k_num_tpart<512>, kTPartSmem) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
   if (!ok) {
@@ -304,7 +302,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
   if (!c) return SPG_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
   Buf *bufs[] = {&c->flop,  &c->rows_sym, &c->rows_num, &c->partial, &c->slab,
-                 &c->info,  &c->scratch,  &c->parts,    &c->part_off, &c->part_n, &c->seg};
+                 &c->info,  &c->scratch,  &c->parts,    &c->part_row, &c->part_n, &c->toff};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {
@@ -395,6 +393,8 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   PlanInfo *info = (PlanInfo *)c->info.p;
   SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
   SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, sizeof(int64_t), s));
+  if (B->nrows > 0)
+    SPG_CUDA(c, cudaMemcpyAsync(&info->b_end, B->row_ptr + B->nrows, 8, cudaMemcpyDeviceToDevice, s));
   int64_t *row_nnz = C_row_ptr + 1;
   int64_t *flop = (int64_t *)c->flop.p;
   if (m > 0 && B->nrows > 0) {
@@ -403,7 +403,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     {
       ProfScope _ps(c, s, "k_bin_scatter_sym");
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, A->row_ptr, B->ncols, 0, info,
-                                                               (int32_t *)c->rows_sym.p, row_nnz, nullptr);
+                                                               (int32_t *)c->rows_sym.p, row_nnz);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(sym)");
     if ((st = read_info(c, s)) != SPG_OK) return st;
@@ -421,10 +421,12 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         k_check_sorted<<<(unsigned)std::max<int64_t>(gridc, 1), 256, 0, s>>>(dev(B), info);
       }
       SPG_LAUNCHED(c, "k_check_sorted");
-      const int64_t nwd = (B->ncols + kPartWidth - 1) / kPartWidth;
-      parts_cap = (int64_t)(h.flop_total / kWPartKeys) + (int64_t)h.sym_count[SB_BM] * (nwd + 2) + 16;
+      // parts per row <= 2 nnz / kTPartKeys + 1 (consecutive parts hold > kTPartKeys keys)
+      parts_cap = (int64_t)(2 * h.flop_total / kTPartKeys) + (int64_t)h.sym_count[SB_BM] + 16;
+      const int64_t ntiles = (B->ncols + kTileCols - 1) / kTileCols;
+      parts_cap = std::min<int64_t>(parts_cap, (int64_t)h.sym_count[SB_BM] * ntiles + 16);
       if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * sizeof(int2), s)) != SPG_OK) return st;
-      if ((st = buf_ensure(c, c->part_off, size_t(m) * 4, s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->part_row, size_t(parts_cap) * 4, s)) != SPG_OK) return st;
       if ((st = buf_ensure(c, c->part_n, size_t(m) * 4, s)) != SPG_OK) return st;
       parts = (int2 *)c->parts.p;
       c->plan_parts = true;
@@ -473,7 +475,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
           k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(
-              rb, n, a, b, flop, row_nnz, info, parts, parts_cap, (int32_t *)c->part_off.p,
+              rb, n, a, b, flop, row_nnz, info, parts, parts_cap, (int32_t *)c->part_row.p,
               (int32_t *)c->part_n.p);
         }
         SPG_LAUNCHED(c, "k_sym_bitmap");
@@ -501,13 +503,12 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     SPG_CUDA(c, cudaMemsetAsync(row_nnz, 0, size_t(m) * 8, s));
   }
   // a4: C_row_ptr = exclusive scan of row nnz (+ numeric bin counts)
-  const int32_t *pn = c->plan_parts ? (const int32_t *)c->part_n.p : nullptr;
-  if ((st = launch_scan(c, row_nnz, m, s, pn, A->row_ptr)) != SPG_OK) return st;
+  if ((st = launch_scan(c, row_nnz, m, s, A->row_ptr)) != SPG_OK) return st;
   if (m > 0) {
     {
       ProfScope _ps(c, s, "k_bin_scatter_num");
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, A->row_ptr, 0, 1, info,
-                                                               (int32_t *)c->rows_num.p, nullptr, pn);
+                                                               (int32_t *)c->rows_num.p, nullptr);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(num)");
   }
@@ -544,19 +545,27 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   DevCSR a = dev(A), b = dev(B);
   const int32_t *rows = (const int32_t *)c->rows_num.p;
   const int64_t *flop = (const int64_t *)c->flop.p;
-  // G-tier slab: keys + vals of lowest 2^n >= 2 * max nnz(c_i) per block
-  int64_t g_grid = 0, slabT = 0, seg_cap = 0;
+  // G tier: column-tile parts (B sorted, parts cut by the symbolic) or the
+  // global-hash fallback (slab: keys + vals of lowest 2^n >= 2 max nnz(c_i) per block)
+  int64_t g_grid = 0, slabT = 0, ntiles = 0;
   const bool use_parts = c->plan_parts && h.b_unsorted == 0 && h.parts_overflow == 0;
   if (h.num_count[NB_G]) {
-    g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
     if (use_parts) {
+      ntiles = (B->ncols + kTileCols - 1) / kTileCols;
+      if (h.b_end >= (unsigned long long)INT32_MAX)
+        return fail(c, SPG_ERR_OVERFLOW, "tile offsets need B.row_ptr[nrows] < 2^31");
+      if ((st = buf_ensure(c, c->toff, size_t(B->nrows) * size_t(ntiles + 1) * 4, s)) != SPG_OK)
+        return st;
       SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));
-      if ((int64_t)h.max_arow > kSegSmem) {
-        seg_cap = ((int64_t)h.max_arow + 8) & ~int64_t(7);  // keeps every block's int64 arrays aligned
-        if ((st = buf_ensure(c, c->seg, size_t(g_grid) * size_t(seg_cap) * kSegBytes, s)) != SPG_OK)
-          return st;
+      {
+        ProfScope _ps(c, s, "k_tile_offsets");
+        const int64_t grid = std::min<int64_t>(ceil_div(B->nrows, 8), int64_t(c->num_sms) * 16);
+        k_tile_offsets<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, s>>>(b, (int)ntiles,
+                                                                          (int32_t *)c->toff.p);
       }
+      SPG_LAUNCHED(c, "k_tile_offsets");
     } else {
+      g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
       int lg = log2_ceil64(2 * h.max_nnz);
       slabT = int64_t(1) << std::max(lg, kMinLogT);
       if ((st = buf_ensure(c, c->slab, size_t(g_grid) * size_t(slabT) * 12, s)) != SPG_OK) return st;
@@ -602,26 +611,16 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
           k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
         }
       SPG_LAUNCHED(c, "k_num_block");
-    } else if (bin == NB_GW) {  // warp parts
-      const int64_t grid = std::min<int64_t>(ceil_div(n, 4), int64_t(c->num_sms) * 5);
-      SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter_w, 0, 8, ss));
+    } else if (use_parts) {  // NB_G: column-tile parts, independent work items
       {
-        ProfScope _ps(c, ss, "k_num_wpart<4>");
-        k_num_wpart<4><<<(unsigned)grid, 128, 4 * kWPartSmemPerWarp, ss>>>(
-            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
-            (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p,
-            &((PlanInfo *)c->info.p)->row_counter_w);
+        ProfScope _ps(c, ss, "k_num_tpart<512>");
+        k_num_tpart<512><<<(unsigned)(2 * c->num_sms), 512, kTPartSmem, ss>>>(
+            a, b, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
+            (const int32_t *)c->part_row.p, (int64_t)h.parts_used, (const int32_t *)c->toff.p,
+            (int)ntiles, &((PlanInfo *)c->info.p)->row_counter, c->tune,
+            ((PlanInfo *)c->info.p)->dbg);
       }
-      SPG_LAUNCHED(c, "k_num_wpart");
-    } else if (use_parts) {  // NB_G with column-range parts
-      {
-        ProfScope _ps(c, ss, "k_num_part<1024>");
-        k_num_part<1024><<<(unsigned)g_grid, 1024, kPartSmem, ss>>>(
-            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
-            (const int32_t *)c->part_off.p, (const int32_t *)c->part_n.p, (char *)c->seg.p,
-            seg_cap, &((PlanInfo *)c->info.p)->row_counter, c->tune, ((PlanInfo *)c->info.p)->dbg);
-      }
-      SPG_LAUNCHED(c, "k_num_part");
+      SPG_LAUNCHED(c, "k_num_tpart");
     } else {  // NB_G
       uint32_t *sk = (uint32_t *)c->slab.p;
       double *sv = (double *)((char *)c->slab.p + size_t(g_grid) * size_t(slabT) * 4);

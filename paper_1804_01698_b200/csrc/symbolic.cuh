@@ -378,10 +378,10 @@ __device__ __forceinline__ int nth_bit_col(int q, uint32_t word, int n) {
 // ---------------------------------------------------------------------------
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
-// sorted it also cuts rows with nnz > kPartKeys into column-range parts for the
-// numeric G tier: cuts at every kPartKeys-th key (rank cuts) and at every
-// multiple of kPartWidth (width cuts); part = (first column, keys of the row
-// before it); ranges holding no key are merged into the previous part.
+// sorted it also cuts rows with nnz > kPartMinKeys into column-tile parts for
+// the numeric G tier (spg_internal.cuh): part = (first column = first tile *
+// kTileCols, keys of the row before it), its row id in part_row, the row's
+// part count in part_n.
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restrict__ rows,
@@ -390,17 +390,17 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         int64_t *__restrict__ row_nnz,
                                                         PlanInfo *info, int2 *__restrict__ parts,
                                                         int64_t parts_cap,
-                                                        int32_t *__restrict__ part_off,
+                                                        int32_t *__restrict__ part_row,
                                                         int32_t *__restrict__ part_n) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt;
   __shared__ int s_warp[THREADS / 32];
-  __shared__ int s_base;
-  __shared__ int2 s_rank[kMaxPartsPerRow];   // rank cuts (col, cum)
-  __shared__ int2 s_width[kMaxPartsPerRow];  // width cuts (col, cum)
+  __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
+  __shared__ int s_cut[kMaxTiles];       // first tile of each part
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwords = (int)((B.ncols + 31) >> 5);
+  const int ntiles = (int)((B.ncols + kTileCols - 1) >> kTileLog);
   uint32_t *bm = s_dyn_u32;
   const bool want_parts = parts != nullptr && info->b_unsorted == 0;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
@@ -420,85 +420,40 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     __syncthreads();
     const int nnz = s_cnt;
     if (threadIdx.x == 0) row_nnz[i] = nnz;
-    const bool wkind = (ae - as) <= kWPartMaxEntries;  // few a_ik: warp parts
-    if (want_parts && wkind && nnz > kWPartKeys) {
-      // warp parts: rank cuts only, part k = (column of the key of rank k*kWPartKeys, k*kWPartKeys)
-      const int np = (nnz + kWPartKeys - 1) / kWPartKeys;
+    if (want_parts && nnz > kPartMinKeys) {
+      // keys before each column tile (from the prefix popcounts of the bitmap)
+      bitmap_prefix_walk(bm, nwords, s_warp, [&](int q, uint32_t, int cum) {
+        if ((q & (kTileCols / 32 - 1)) == 0) s_tile[q >> (kTileLog - 5)] = cum;
+      });
       if (threadIdx.x == 0) {
+        s_tile[ntiles] = nnz;
+        // parts: greedy runs of consecutive tiles holding <= kTPartKeys keys;
+        // a tile holding more stands alone (dense window in the numeric phase)
+        int np = 0, start = 0, acc = 0;
+        for (int t = 0; t < ntiles; ++t) {
+          const int c = s_tile[t + 1] - s_tile[t];
+          if (acc > 0 && acc + c > kTPartKeys) {
+            s_cut[np++] = start;
+            start = t;
+            acc = 0;
+          }
+          acc += c;
+        }
+        s_cut[np++] = start;
         const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
         if (base + np > parts_cap) {
           atomicAdd(&info->parts_overflow, 1ull);
-          s_base = -1;
+          part_n[i] = 0;
         } else {
-          s_base = (int)base;
-          part_off[i] = (int32_t)base;
-          part_n[i] = -np;
-          parts[base] = make_int2(0, 0);
-        }
-      }
-      __syncthreads();
-      const int base = s_base;
-      if (base >= 0) {
-        bitmap_prefix_walk(bm, nwords, s_warp, [&](int q, uint32_t word, int cum) {
-          int r = ((cum + kWPartKeys - 1) / kWPartKeys) * kWPartKeys;
-          if (r == 0) r = kWPartKeys;
-          if (r < cum + __popc(word))  // at most one cut per word (kWPartKeys >= 32)
-            parts[base + r / kWPartKeys] = make_int2(nth_bit_col(q, word, r - cum), r);
-        });
-      } else if (threadIdx.x == 0) {
-        part_n[i] = 0;
-      }
-    } else if (want_parts && !wkind && nnz > kPartKeys) {
-      bitmap_prefix_walk(bm, nwords, s_warp, [&](int q, uint32_t word, int cum) {
-        if (q > 0 && ((int64_t(q) * 32) & (kPartWidth - 1)) == 0) {  // width cut
-          const int k = (int)((int64_t(q) * 32) >> kPartWidthLog);
-          if (k < kMaxPartsPerRow) s_width[k] = make_int2(q * 32, cum);
-        }
-        int r = ((cum + kPartKeys - 1) / kPartKeys) * kPartKeys;  // rank cut (at most one per word)
-        if (r == 0) r = kPartKeys;
-        if (r < cum + __popc(word)) {
-          const int k = r / kPartKeys;
-          if (k < kMaxPartsPerRow) s_rank[k] = make_int2(nth_bit_col(q, word, r - cum), r);
-        }
-      });
-      if (threadIdx.x == 0) {
-        // merge rank cuts [1, nrk) and width cuts [1, nwd) by column
-        const int nrk = min((nnz - 1) / kPartKeys + 1, kMaxPartsPerRow);
-        const int nwd = min((int)((B.ncols - 1) >> kPartWidthLog) + 1, kMaxPartsPerRow);
-        int np = 0;
-        int64_t base = 0;
-        for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts, pass 1 writes
-          if (pass == 1) {
-            base = (int64_t)atomicAdd(&info->parts_used, (unsigned long long)np);
-            if (base + np > parts_cap) {
-              atomicAdd(&info->parts_overflow, 1ull);
-              part_n[i] = 0;
-              break;
-            }
-            part_off[i] = (int32_t)base;
-            part_n[i] = np;
+          for (int p = 0; p < np; ++p) {
+            parts[base + p] = make_int2(s_cut[p] << kTileLog, s_tile[s_cut[p]]);
+            part_row[base + p] = i;
           }
-          np = 0;
-          int a = 1, b = 1;
-          int2 cur = make_int2(0, 0);
-          while (a < nrk || b < nwd) {
-            int2 nx;
-            if (a < nrk && (b >= nwd || s_rank[a].x <= s_width[b].x)) nx = s_rank[a++];
-            else nx = s_width[b++];
-            if (nx.y > cur.y) {  // [cur, nx) holds keys: emit it
-              if (pass == 1) parts[base + np] = cur;
-              ++np;
-            }
-            cur = nx;  // an empty range [cur, nx) is merged into its neighbours
-          }
-          if (nnz > cur.y) {
-            if (pass == 1) parts[base + np] = cur;
-            ++np;
-          }
+          part_n[i] = np;
         }
       }
     } else if (threadIdx.x == 0 && part_n != nullptr) {
-      part_n[i] = 0;  // a single part: the whole row
+      part_n[i] = 0;  // no parts: a B-tier row
     }
     __syncthreads();
   }
