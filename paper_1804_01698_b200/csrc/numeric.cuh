@@ -107,6 +107,51 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
     }
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
+    if (nnz <= 128 && mx - mn < (1u << 25)) {
+      // <= 128 keys within 2^25 columns: bitonic sort in registers of packed
+      // (column - min) << 7 | index, 4 per lane (element e = 4 lane + r)
+      uint32_t pk[4];
+      const uint4 kk = reinterpret_cast<const uint4 *>(keys)[lane];  // keys[4 lane .. 4 lane + 3]
+      const uint32_t kr[4] = {kk.x, kk.y, kk.z, kk.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = 4 * lane + r;
+        pk[r] = e < nnz ? ((kr[r] - mn) << 7) | (uint32_t)e : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          if (j >= 4) {  // partner: same r in lane ^ (j / 4)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const uint32_t o = __shfl_xor_sync(kFull, pk[r], j >> 2);
+              const int e = 4 * lane + r;
+              const bool keepmin = ((e & j) == 0) == ((e & k) == 0);
+              pk[r] = keepmin ? min(pk[r], o) : max(pk[r], o);
+            }
+          } else {  // partner: register r ^ j of this lane
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              if (r & j) continue;
+              const int e = 4 * lane + r;
+              const uint32_t a = pk[r], b = pk[r | j];
+              const bool up = (e & k) == 0;
+              if ((a > b) == up) { pk[r] = b; pk[r | j] = a; }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = 4 * lane + r;
+        if (e < nnz) {
+          c_col[rp0 + e] = (int32_t)(mn + (pk[r] >> 7));
+          c_val[rp0 + e] = vals[pk[r] & 127u];
+        }
+      }
+      return;
+    }
     int sh = log2_ceil64(uint64_t(mx - mn) + 1) - logT;
     sh = sh < 0 ? 0 : sh;
     for (int b = lane; b < T; b += 32) cnt[b] = 0u;
@@ -151,14 +196,14 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
 // plain read-modify-write; lanes that share a key in a round (found with
 // __match_any_sync) use the atomic add.  Rounds are separated by __syncwarp.
 // ---------------------------------------------------------------------------
-template <int TMAX, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_num_warp(const int32_t *__restrict__ rows,
+template <int TMAX, int WARPS, int SORTED>
+__global__ void __launch_bounds__(WARPS * 32, 40 / WARPS) k_num_warp(const int32_t *__restrict__ rows,
                                                          int64_t nrows, DevCSR A, DevCSR B,
                                                          const int64_t *__restrict__ flop,
                                                          const int64_t *__restrict__ c_rp,
                                                          int32_t *__restrict__ c_col,
-                                                         double *__restrict__ c_val,
-                                                         int sorted) {
+                                                         double *__restrict__ c_val) {
+  constexpr int sorted = SORTED;  // (separate instantiations: the sorted emit costs registers)
   extern __shared__ double s_dyn_f64[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *vals = s_dyn_f64 + w * TMAX;

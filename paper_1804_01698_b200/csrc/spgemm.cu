@@ -280,7 +280,8 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
   if (ok) {
     const size_t s_num_w1024 = 4 * 1024 * 16;
     const size_t s_num_b = size_t(16384) * 12;
-    ok = set_smem(c, k_num_warp<1024, 4>, s_num_w1024) == SPG_OK &&
+    ok = set_smem(c, k_num_warp<1024, 4, 0>, s_num_w1024) == SPG_OK &&
+         set_smem(c, k_num_warp<1024, 4, 1>, s_num_w1024) == SPG_OK &&
          set_smem(c, k_num_block<512>, s_num_b) == SPG_OK &&
          set_smem(c, k_num_block<1024>, s_num_b) == SPG_OK &&
          set_smem(c, k_sym_block<512>, size_t(32768) * 4) == SPG_OK &&
@@ -583,16 +584,24 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
       {
         ProfScope _ps(c, ss, "k_num_warp<256>");
-        k_num_warp<256, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 16, ss>>>(
-            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted);
+        if (sorted)
+          k_num_warp<256, kWarps, 1><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 16, ss>>>(
+              rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val);
+        else
+          k_num_warp<256, kWarps, 0><<<(unsigned)grid, kWarps * 32, kWarps * 256 * 16, ss>>>(
+              rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val);
       }
       SPG_LAUNCHED(c, "k_num_warp<256>");
     } else if (bin == NB_W1024) {
       const int64_t grid = std::min<int64_t>(ceil_div(n, 4), int64_t(c->num_sms) * 32);
       {
         ProfScope _ps(c, ss, "k_num_warp<1024>");
-        k_num_warp<1024, 4><<<(unsigned)grid, 4 * 32, 4 * 1024 * 16, ss>>>(
-            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted);
+        if (sorted)
+          k_num_warp<1024, 4, 1><<<(unsigned)grid, 4 * 32, 4 * 1024 * 16, ss>>>(
+              rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val);
+        else
+          k_num_warp<1024, 4, 0><<<(unsigned)grid, 4 * 32, 4 * 1024 * 16, ss>>>(
+              rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val);
       }
       SPG_LAUNCHED(c, "k_num_warp<1024>");
     } else if (bin >= NB_B2K && bin <= NB_B16K) {
