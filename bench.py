@@ -313,8 +313,10 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
     def step(sorted_out):
-        if tri:
-            return spg.triangle_count(Aloc, dB, dG, sorted=sorted_out, ctx=ctx) if r1 > r0 else 0
+        if sorted_out == "fused":  # C5 variant: mask fused into the product (C never formed)
+            return spg.masked_sum(Aloc, dB, dG, r0, ctx) if r1 > r0 else 0.0
+        if tri:  # rows [r0, r1) of C = L*U, masked by the same rows of G, in row blocks
+            return spg.triangle_count_rows(dA, dB, dG, r0, r1, sorted=sorted_out, ctx=ctx)
         C = spg.spgemm(Aloc, dB, sorted=sorted_out, ctx=ctx)
         return C
 
@@ -335,7 +337,7 @@ def run_ours(args):
             ev[i][0].record(s)
             out = step(sorted_out)
             ev[i][1].record(s)
-            if i == k - 1 and out is not None and not isinstance(out, int):
+            if i == k - 1 and out is not None and not isinstance(out, (int, float)):
                 last = out.row_ptr               # keep only the final row_ptr (C can be >100 GB)
             del out
         torch.cuda.synchronize()
@@ -362,6 +364,10 @@ def run_ours(args):
         step(False)
     ms_sorted, launches, recs, Cs = timed(True, args.steps, profile=True)
     ms_unsorted, _, _, _ = timed(False, args.steps)
+    ms_fused = None
+    if tri:
+        step("fused")
+        ms_fused, _, _, _ = timed("fused", args.steps)
     clk = clocks.stop()
 
     gflops = lambda ms: 2.0 * flop_total / (ms * 1e-3) / 1e9  # noqa: E731
@@ -422,7 +428,11 @@ def run_ours(args):
                        "parallelism": f"rows x {world} (flop-balanced, B broadcast)",
                        "l2": "flushed between steps (256 MiB write outside the step events)"},
             "variants": {"sorted": {"value": gflops(ms_sorted), "ms_per_step": ms_sorted},
-                         "unsorted": {"value": gflops(ms_unsorted), "ms_per_step": ms_unsorted}},
+                         "unsorted": {"value": gflops(ms_unsorted), "ms_per_step": ms_unsorted},
+                         **({"fused_mask": {"value": gflops(ms_fused), "ms_per_step": ms_fused,
+                                            "note": "sum(L*U o G) with the mask fused into the "
+                                                    "product (SURVEY 8(f) row 1); C not formed"}}
+                            if ms_fused is not None else {})},
             "minimal_bytes_model": mb,
             "hbm_roofline_frac_step": (mb / (ms_sorted * 1e-3) / 1e9 / measured_peak()[0]) if mb else None,
             "gpu_launches": launches,

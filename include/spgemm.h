@@ -168,6 +168,20 @@ spg_status spg_rows_to_parts(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
 spg_status spg_mask_sum(spg_ctx *ctx, const spg_csr *C, const spg_csr *G,
                         int64_t g_row_begin, int64_t *sum, void *stream);
 
+/* Fused mask-and-sum (triangle counting, Sec 5.6 P:602-605;
+ * SURVEY.md §8(f) row 1):  *sum = sum over (i, j) in pattern(G) of (A*B)(i, j)
+ * for the rows of A, where row i of A is row g_row_begin + i of G -- computed
+ * WITHOUT forming C: the columns of G's row i are the keys of the hash set
+ * (bitmap for long G rows) that every product of Gustavson's row i probes;
+ * matching products are summed in fp64 (exact for integer-valued inputs below
+ * 2^53, e.g. the triangle count's L*U with values 1.0: triangles = *sum / 2).
+ *   A, B : device CSR, values required; A.ncols == B.nrows; any column order.
+ *   G    : device CSR pattern (values unused), G.ncols == B.ncols, rows
+ *          strictly increasing when B.ncols > kBitmapMaxCols (binary search).
+ *   sum  : host out.  Synchronizes `stream`. */
+spg_status spg_masked_sum(spg_ctx *ctx, const spg_csr *A, const spg_csr *B, const spg_csr *G,
+                          int64_t g_row_begin, double *sum, void *stream);
+
 /* Validation of the CSR invariants (untimed): row_ptr nondecreasing, columns
  * in [0, ncols); with check_sorted != 0 also strictly increasing columns per
  * row (which implies uniqueness).  Returns SPG_OK or SPG_ERR_INDEX_RANGE /

@@ -22,7 +22,7 @@ EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_co
            "spg_symbolic", "spg_numeric", "spg_get_info", "spg_plan_export",
            "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
-           "spg_debug_counters")
+           "spg_debug_counters", "spg_masked_sum")
 
 
 class spg_csr(ct.Structure):
@@ -76,6 +76,7 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_profile_count.restype = i64
     lib.spg_profile_record.argtypes = [vp, i64, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_float)]
     lib.spg_debug_counters.argtypes = [vp, i64p, vp]
+    lib.spg_masked_sum.argtypes = [vp, csrp, csrp, csrp, i64, ct.POINTER(ct.c_double), vp]
     for name in EXPORTS:
         if name not in ("spg_last_error", "spg_launch_count", "spg_profile_count"):
             getattr(lib, name).restype = ct.c_int
@@ -176,3 +177,12 @@ def spg_debug_counters(ctx: int, stream: int = 0) -> list[int]:
     out = (ct.c_int64 * 16)()
     _check(ctx, "spg_debug_counters", load().spg_debug_counters(ctx, out, stream))
     return list(out)
+
+
+def spg_masked_sum(ctx: int, A: spg_csr, B: spg_csr, G: spg_csr, g_row_begin: int,
+                   stream: int) -> float:
+    out = ct.c_double(0.0)
+    _check(ctx, "spg_masked_sum",
+           load().spg_masked_sum(ctx, ct.byref(A), ct.byref(B), ct.byref(G), g_row_begin,
+                                 ct.byref(out), stream))
+    return out.value

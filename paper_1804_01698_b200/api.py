@@ -161,6 +161,25 @@ def mask_sum(C: DeviceCSR, G: DeviceCSR, g_row_begin: int = 0, ctx: Context | No
     return _lib.spg_mask_sum(ctx.handle, C.c(), G.c(), g_row_begin, _stream())
 
 
+def masked_sum(A: DeviceCSR, B: DeviceCSR, G: DeviceCSR, g_row_begin: int = 0,
+               ctx: Context | None = None) -> float:
+    """sum over (i,j) in pattern(G) of (A*B)(i,j), without forming A*B
+    (fused mask)."""
+    ctx = ctx or default_context()
+    return _lib.spg_masked_sum(ctx.handle, A.c(), B.c(), G.c(), g_row_begin, _stream())
+
+
+def triangle_count_fused(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR,
+                         ctx: Context | None = None) -> int:
+    """Triangles = sum(L*U o G)/2 with the mask fused into the product (C is
+    never formed); values must be 1.0 (BASELINE config 5)."""
+    s = masked_sum(L, U, G, 0, ctx)
+    t = int(round(s))
+    if t != s or t % 2:
+        raise RuntimeError(f"masked sum {s!r} is not an even integer")
+    return t // 2
+
+
 def validate(M: DeviceCSR, check_sorted: bool = False, ctx: Context | None = None) -> None:
     ctx = ctx or default_context()
     _lib.spg_validate(ctx.handle, M.c(), check_sorted, _stream())

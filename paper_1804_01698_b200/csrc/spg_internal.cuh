@@ -49,6 +49,8 @@ struct PlanInfo {
   unsigned long long parts_overflow;
   unsigned long long row_counter;   // dynamic work queue of the numeric G tier
   unsigned long long b_end;         // B.row_ptr[B.nrows] (tile offsets are int32 positions)
+  unsigned long long mask_ctr[2];   // row queues of the fused mask-and-sum kernels
+  double mask_acc;                  // their fp64 sum
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)
 };
 

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "masked.cuh"
 #include "numeric.cuh"
 #include "plan.cuh"
 #include "spg_internal.cuh"
@@ -288,6 +289,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
          set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_tpart<512>, kTPartSmem) == SPG_OK &&
+         set_smem(c, k_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
   if (!ok) {
@@ -735,6 +737,45 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
   SPG_CUDA(c, cudaStreamSynchronize(s));
   h = c->host_info->mask_sum;
   *sum = (int64_t)h;
+  return SPG_OK;
+}
+
+spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const spg_csr *G,
+                          int64_t g_row_begin, double *sum, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", true)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", true)) != SPG_OK) return st;
+  if ((st = check_csr(c, G, "G", false)) != SPG_OK) return st;
+  if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
+  if (G->ncols != B->ncols) return fail(c, SPG_ERR_DIM_MISMATCH, "G.ncols != B.ncols");
+  if (!sum || g_row_begin < 0 || g_row_begin + A->nrows > G->nrows)
+    return fail(c, SPG_ERR_INVALID_ARG, "bad mask row range or NULL sum");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 3 * 8, s));  // both queues and the sum
+  if (A->nrows > 0 && B->nrows > 0) {
+    DevCSR a = dev(A), b = dev(B), g = dev(G);
+    {
+      ProfScope _ps(c, s, "k_mask_sum_warp<8>");
+      k_mask_sum_warp<kWarps><<<(unsigned)(c->num_sms * 8), kWarps * 32, 0, s>>>(
+          a, b, g, g_row_begin, &info->mask_ctr[0], &info->mask_acc);
+    }
+    SPG_LAUNCHED(c, "k_mask_sum_warp");
+    const int use_bitmap = B->ncols <= kBitmapMaxCols ? 1 : 0;
+    const size_t smem = use_bitmap ? size_t((B->ncols + 31) / 32) * 4 : 0;
+    {
+      ProfScope _ps(c, s, "k_mask_sum_block<1024>");
+      k_mask_sum_block<1024><<<(unsigned)c->num_sms, 1024, smem, s>>>(
+          a, b, g, g_row_begin, &info->mask_ctr[1], &info->mask_acc, use_bitmap);
+    }
+    SPG_LAUNCHED(c, "k_mask_sum_block");
+  }
+  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  *sum = c->host_info->mask_acc;
   return SPG_OK;
 }
 

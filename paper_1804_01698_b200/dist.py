@@ -93,14 +93,20 @@ def spgemm_dist(A, B, sorted: bool = True, group=None, ctx: Context | None = Non
     return DistBlock(C, r0, r1, sum(counts[:rank]), sum(counts), offs)
 
 
-def triangle_count_dist(L, U, G, group=None, ctx: Context | None = None) -> int:
+def triangle_count_dist(L, U, G, group=None, ctx: Context | None = None,
+                        fused: bool = False) -> int:
     """Triangle count of BASELINE config 5 over the ranks: each rank counts
-    sum(C o G) on its flop-balanced row block of C = L*U, then all_reduce(SUM)."""
-    from .api import triangle_count_rows
+    sum(C o G) on its flop-balanced row block of C = L*U, then all_reduce(SUM).
+    fused=True sums the masked products without forming C (spg_masked_sum)."""
+    from .api import masked_sum, triangle_count_rows
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     offs, _ = partition_rows(L, U, world, ctx)
     r0, r1 = offs[rank], offs[rank + 1]
-    part = triangle_count_rows(L, U, G, r0, r1, ctx=ctx)
+    if fused:
+        s = masked_sum(L.rows(r0, r1), U, G, r0, ctx) if r1 > r0 else 0.0
+        part = int(round(s))
+    else:
+        part = triangle_count_rows(L, U, G, r0, r1, ctx=ctx)
     t = torch.tensor([part], dtype=torch.int64, device=L.row_ptr.device)
     dist.all_reduce(t, group=group)
     total = int(t.item())

@@ -50,4 +50,6 @@ def test_triangles_dist_nccl_world1(pg):
     from paper_1804_01698_b200 import dist as sdist
     L, U, ex = synth.workload("c5_triangle", scale=11)
     dL, dU, dG = (spg.DeviceCSR.from_host(x) for x in (L, U, ex["G"]))
-    assert sdist.triangle_count_dist(dL, dU, dG) == oracle.triangle_count(L, U, ex["G"])
+    want = oracle.triangle_count(L, U, ex["G"])
+    assert sdist.triangle_count_dist(dL, dU, dG) == want
+    assert sdist.triangle_count_dist(dL, dU, dG, fused=True) == want

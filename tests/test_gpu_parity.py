@@ -219,6 +219,56 @@ def test_triangles_complete_graph(spg, ctx):
     assert spg.triangle_count(dL, dU, dG, ctx=ctx) == n * (n - 1) * (n - 2) // 6
 
 
+# ------------------------------------------------------------------ fused mask
+@pytest.mark.parametrize("scale", [10, 14])
+def test_c5_triangles_fused(spg, ctx, scale):
+    """Fused mask-and-sum (C never formed) vs the oracle's triangle count;
+    scale 14 has G rows above the warp tier (bitmap tier)."""
+    L, U, ex = synth.workload("c5_triangle", scale=scale)
+    G = ex["G"]
+    want = oracle.triangle_count(L, U, G)
+    dL, dU, dG = (spg.DeviceCSR.from_host(x) for x in (L, U, G))
+    assert spg.triangle_count_fused(dL, dU, dG, ctx=ctx) == want
+    if scale == 14:
+        assert int(np.diff(G.row_ptr).max()) > 256  # both tiers ran
+
+
+def test_triangles_fused_complete_graph(spg, ctx):
+    for n in (3, 60, 700):  # 700: G rows of 699 > the warp tier
+        G = synth.complete_graph(n)
+        L, U = synth.tril_strict(G), synth.triu_strict(G)
+        dL, dU, dG = (spg.DeviceCSR.from_host(x) for x in (L, U, G))
+        assert spg.triangle_count_fused(dL, dU, dG, ctx=ctx) == n * (n - 1) * (n - 2) // 6
+
+
+@pytest.mark.parametrize("ncols", [5000, 2_000_000])
+def test_masked_sum_random_values(spg, ctx, ncols):
+    """General values: sum over pattern(G) of (A*B) vs the oracle's C and
+    mask_sum; ncols 2M > the bitmap limit (binary-search tier)."""
+    rng = np.random.default_rng(ncols)
+    m, k = 300, 400
+    A = synth.random_sparse(m, k, 0.05, 11, 0.0, 1.0)
+    B = synth.random_sparse(k, ncols, min(0.5, 3000.0 / ncols), 12, 0.0, 1.0)
+    o_rp, o_col, o_val = oracle.spgemm(A, B)
+    # G: half of C's pattern per row plus random extra columns; some rows long
+    rows, cols = [], []
+    for i in range(m):
+        ci = o_col[o_rp[i]:o_rp[i + 1]]
+        keep = ci[rng.random(len(ci)) < 0.5]
+        extra = rng.integers(0, ncols, size=int(rng.integers(0, 600 if i % 7 == 0 else 40)))
+        cc = np.unique(np.r_[keep, extra]).astype(np.int64)
+        rows.append(np.full(len(cc), i)); cols.append(cc)
+    G = synth.from_coo(m, ncols, np.concatenate(rows), np.concatenate(cols))
+    want = 0.0
+    for i in range(m):  # oracle-side mask sum in fp64 (canonical order)
+        ci, vi = o_col[o_rp[i]:o_rp[i + 1]], o_val[o_rp[i]:o_rp[i + 1]]
+        g = G.col[G.row_ptr[i]:G.row_ptr[i + 1]]
+        want += float(vi[np.isin(ci, g)].sum())
+    dA, dB, dG = (spg.DeviceCSR.from_host(x) for x in (A, B, G))
+    got = spg.masked_sum(dA, dB, dG, 0, ctx)
+    assert abs(got - want) <= 1e-12 * abs(want), (got, want)
+
+
 def test_validate(spg, ctx):
     from paper_1804_01698_b200 import _lib
     A = synth.random_sparse(50, 40, 0.2, 1)
