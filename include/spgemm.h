@@ -120,7 +120,9 @@ spg_status spg_debug_counters(spg_ctx *ctx, int64_t *out, void *stream);
  *   nnz_C       : host out, nnz(C) = C_row_ptr[A.nrows].
  *   flop_total  : host out (may be NULL), sum of per-row flop.
  * Blocks the calling thread for two small device->host reads (bin counts,
- * then nnz and numeric bin counts).  Keeps the plan (flop, bins) in ctx for
+ * then nnz and numeric bin counts); one more when most a_ik hit empty rows
+ * of B (then the plan runs on A' = the useful a_ik of A, kept in ctx, e.g.
+ * a tall-skinny frontier B).  Keeps the plan (flop, bins) in ctx for
  * spg_numeric. */
 spg_status spg_symbolic(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
                         int64_t *C_row_ptr, int64_t *nnz_C, int64_t *flop_total,

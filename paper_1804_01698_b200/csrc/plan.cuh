@@ -26,44 +26,82 @@ __device__ __forceinline__ int64_t row_of(const int64_t *__restrict__ rp, int64_
   return lo;
 }
 
+// last r' in [r, hi] with rp[r'] <= j, given rp[r] <= j (galloping: cheap
+// when few rows lie between, logarithmic across long runs of empty rows)
+__device__ __forceinline__ int64_t advance_row(const int64_t *__restrict__ rp, int64_t r, int64_t hi,
+                                               int64_t j) {
+  if (r >= hi || __ldg(rp + r + 1) > j) return r;
+  int64_t lo = r + 1, step = 1;  // invariant: rp[lo] <= j
+  while (lo + step <= hi && __ldg(rp + lo + step) <= j) {
+    lo += step;
+    step <<= 1;
+  }
+  int64_t up = lo + step <= hi ? lo + step - 1 : hi;  // answer in [lo, up]
+  while (up > lo) {
+    const int64_t m = lo + (up - lo + 1) / 2;
+    if (__ldg(rp + m) <= j) lo = m; else up = m - 1;
+  }
+  return lo;
+}
+
+// Rows of the first and last entries of the tile of kFlopTile consecutive
+// a_ik starting at t0 (threads 0 and 1) into s_r[0..1].
+__device__ __forceinline__ void tile_rows(const DevCSR &A, int64_t base, int64_t t0, int64_t nz,
+                                          long long *s_r) {
+  if (threadIdx.x < 2) {
+    const int64_t tl = (nz - t0) < kFlopTile ? (nz - t0) : kFlopTile;
+    const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : tl - 1);
+    s_r[threadIdx.x] = row_of(A.rp, 0, A.nrows - 1, j);
+  }
+}
+
 __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_t *__restrict__ b_rp,
+                                                          int64_t b_nrows,
+                                                          const uint32_t *__restrict__ b_nonempty,
                                                           unsigned long long *__restrict__ flop,
-                                                          PlanInfo *info) {
+                                                          PlanInfo *info,
+                                                          unsigned long long *__restrict__ useful_row) {
   __shared__ long long s_r[2];
-  __shared__ unsigned long long s_maxb;
+  __shared__ unsigned long long s_maxb, s_useful;
   const int lane = threadIdx.x & 31;
   const int64_t base = A.rp[0], nz = A.rp[A.nrows] - base;
-  unsigned long long maxb = 0;
-  if (threadIdx.x == 0) s_maxb = 0;
+  // mostly-empty B (e.g. a tall-skinny frontier): test the nonempty-row bitmap
+  // before gathering B.rp (decided on the device: no host round trip)
+  const bool use_bm = b_nonempty != nullptr && 2 * (int64_t)info->b_empty > b_nrows;
+  unsigned long long maxb = 0, useful = 0;
+  if (threadIdx.x == 0) { s_maxb = 0; s_useful = 0; }
   for (int64_t t0 = int64_t(blockIdx.x) * kFlopTile; t0 < nz; t0 += int64_t(gridDim.x) * kFlopTile) {
     __syncthreads();
-    if (threadIdx.x < 2) {
-      const int64_t tl = (nz - t0) < kFlopTile ? (nz - t0) : kFlopTile;
-      const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : tl - 1);
-      s_r[threadIdx.x] = row_of(A.rp, 0, A.nrows - 1, j);
-    }
+    tile_rows(A, base, t0, nz, s_r);
     __syncthreads();
     const int64_t rlo = s_r[0], rhi = s_r[1];
     const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
     const int64_t jend = base + nz;
     int64_t r = j0 < jend ? row_of(A.rp, rlo, rhi, j0) : rhi;
     int64_t rend = __ldg(A.rp + r + 1);
-    unsigned long long acc = 0;
+    unsigned long long acc = 0, acc_u = 0;
     // walk the run; flush acc at each row boundary (all but the last segment)
     for (int u = 0; u < kFlopRun; ++u) {
       const int64_t j = j0 + u;
       if (j >= jend) break;
-      while (j >= rend) {
+      if (j >= rend) {
         if (acc) atomicAdd(flop + r, acc);
+        if (use_bm && useful_row && acc_u) atomicAdd(useful_row + r, acc_u);
         acc = 0;
-        ++r;
+        acc_u = 0;
+        r = advance_row(A.rp, r + 1, rhi, j);
         rend = __ldg(A.rp + r + 1);
       }
       const int k = __ldg(A.col + j);
-      const unsigned long long len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
+      unsigned long long len = 0;
+      if (!use_bm || ((__ldg(b_nonempty + (k >> 5)) >> (k & 31)) & 1u))
+        len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
       acc += len;
+      acc_u += len > 0;
+      useful += len > 0;
       maxb = len > maxb ? len : maxb;
     }
+
     // last segment: lanes holding the same row combine before the atomic
     const unsigned long long key = (unsigned long long)r;
     const unsigned grp = __match_any_sync(kFull, j0 < jend ? key : ~0ull);
@@ -77,14 +115,99 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
       if (lane + o < 32 && ((grp >> (lane + o)) & 1u)) sum += v;
     }
     if (lane == leader && j0 < jend && sum) atomicAdd(flop + r, sum);
+    if (use_bm && useful_row) {  // same segmented sum for the useful-entry counts
+      unsigned long long su = acc_u;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_down_sync(kFull, su, o);
+        if (lane + o < 32 && ((grp >> (lane + o)) & 1u)) su += v;
+      }
+      if (lane == leader && j0 < jend && su) atomicAdd(useful_row + r, su);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long t = __shfl_xor_sync(kFull, maxb, o);
     maxb = t > maxb ? t : maxb;
   }
-  if (lane == 0) atomicMax(&s_maxb, maxb);
+  useful = warp_sum(useful);
+  if (lane == 0) {
+    atomicMax(&s_maxb, maxb);
+    if (useful) atomicAdd(&s_useful, useful);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&info->max_brow, s_maxb);
+  if (threadIdx.x == 0) {
+    atomicMax(&info->max_brow, s_maxb);
+    if (s_useful) atomicAdd(&info->useful, s_useful);
+    if (blockIdx.x == 0) info->a_nnz = (unsigned long long)nz;
+  }
+}
+
+// Nonempty-row bitmap of B (bit k = B row k has entries) and its count of
+// empty rows (info->b_empty): one thread per 32 rows.
+__global__ void __launch_bounds__(256) k_b_rowmask(DevCSR B, uint32_t *__restrict__ bm,
+                                                   PlanInfo *info) {
+  const int64_t nw = (B.nrows + 31) >> 5;
+  unsigned long long empty = 0;
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nw;
+       w += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t word = 0u;
+    const int64_t k0 = w << 5;
+    const int nk = (B.nrows - k0) < 32 ? int(B.nrows - k0) : 32;
+    int64_t prev = B.rp[k0];
+    for (int t = 0; t < nk; ++t) {
+      const int64_t nxt = B.rp[k0 + t + 1];
+      if (nxt > prev) word |= 1u << t;
+      prev = nxt;
+    }
+    bm[w] = word;
+    empty += (unsigned long long)(nk - __popc(word));
+  }
+  empty = warp_sum(empty);
+  if ((threadIdx.x & 31) == 0 && empty) atomicAdd(&info->b_empty, empty);
+}
+
+// Pruning of A for a mostly-empty B: a_ik whose B row is empty contribute no
+// product, so C = A'*B with A' = A restricted to the useful a_ik.  The row
+// counts of A' come from k_flop_nz (useful_row); k_prune_scatter writes, for
+// each useful a_ik, its column and its index in A at a per-row cursor (order
+// inside a row arbitrary); k_prune_values gathers A' values from the index.
+__global__ void __launch_bounds__(kFlopThreads) k_prune_scatter(DevCSR A, const uint32_t *__restrict__ bnz,
+                                                                unsigned long long *__restrict__ cursor,
+                                                                const int64_t *__restrict__ rp2,
+                                                                int32_t *__restrict__ col2,
+                                                                int64_t *__restrict__ idx2) {
+  __shared__ long long s_r[2];
+  const int64_t base = A.rp[0], nz = A.rp[A.nrows] - base;
+  for (int64_t t0 = int64_t(blockIdx.x) * kFlopTile; t0 < nz; t0 += int64_t(gridDim.x) * kFlopTile) {
+    __syncthreads();
+    tile_rows(A, base, t0, nz, s_r);
+    __syncthreads();
+    const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
+    const int64_t jend = base + nz;
+    if (j0 >= jend) continue;
+    int64_t r = row_of(A.rp, s_r[0], s_r[1], j0);
+    int64_t rend = __ldg(A.rp + r + 1);
+    for (int u = 0; u < kFlopRun; ++u) {
+      const int64_t j = j0 + u;
+      if (j >= jend) break;
+      if (j >= rend) {
+        r = advance_row(A.rp, r + 1, s_r[1], j);
+        rend = __ldg(A.rp + r + 1);
+      }
+      const int k = __ldg(A.col + j);
+      if (!((__ldg(bnz + (k >> 5)) >> (k & 31)) & 1u)) continue;
+      const int64_t pos = rp2[r] + (int64_t)atomicAdd(cursor + r, 1ull);
+      col2[pos] = k;
+      idx2[pos] = j;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_prune_values(const double *__restrict__ aval,
+                                                      const int64_t *__restrict__ idx2, int64_t n,
+                                                      double *__restrict__ val2) {
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += int64_t(gridDim.x) * blockDim.x)
+    val2[p] = __ldg(aval + idx2[p]);
 }
 
 // Per-row pass after k_flop_nz: symbolic bin counts, flop total / max, longest a_i.

@@ -49,6 +49,9 @@ struct PlanInfo {
   unsigned long long parts_overflow;
   unsigned long long row_counter;   // dynamic work queue of the numeric G tier
   unsigned long long b_end;         // B.row_ptr[B.nrows] (tile offsets are int32 positions)
+  unsigned long long b_empty;       // empty rows of B (k_b_rowmask)
+  unsigned long long useful;        // a_ik whose B row is nonempty (k_flop_nz)
+  unsigned long long a_nnz;         // nnz of A (k_flop_nz)
   unsigned long long mask_ctr[2];   // row queues of the fused mask-and-sum kernels
   double mask_acc;                  // their fp64 sum
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)

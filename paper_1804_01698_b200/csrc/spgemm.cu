@@ -40,6 +40,10 @@ struct spg_ctx {
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
   Buf parts, part_row, part_n, toff;  // column-tile parts of long rows (BM tier), B tile offsets
+  Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
+  bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
+  int64_t prune_n = 0;
+  spg_csr Ap{};
   bool plan_parts = false;           // parts were produced for the numeric G tier
   PlanInfo *host_info = nullptr;  // pinned
   cudaStream_t sub[kSubStreams] = {};
@@ -178,7 +182,8 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // a1 (+ a2 counts): per-row flop, nonzero-parallel (balanced whatever the row
 // lengths), then a per-row pass for bins / totals.
 spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count_bins,
-                       cudaStream_t s) {
+                       cudaStream_t s, const uint32_t *bnz = nullptr,
+                       unsigned long long *useful_row = nullptr) {
   const int64_t m = A->nrows;
   if (m == 0) return SPG_OK;
   PlanInfo *info = (PlanInfo *)c->info.p;
@@ -188,7 +193,7 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
   {
     ProfScope _ps(c, s, "k_flop_nz");
     k_flop_nz<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
-        a, B->row_ptr, (unsigned long long *)flop, info);
+        a, B->row_ptr, B->nrows, bnz, (unsigned long long *)flop, info, useful_row);
   }
   SPG_LAUNCHED(c, "k_flop_nz");
   {
@@ -400,9 +405,27 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     SPG_CUDA(c, cudaMemcpyAsync(&info->b_end, B->row_ptr + B->nrows, 8, cudaMemcpyDeviceToDevice, s));
   int64_t *row_nnz = C_row_ptr + 1;
   int64_t *flop = (int64_t *)c->flop.p;
+  c->pruned = false;
+  const spg_csr *A0 = A;  // the caller's A (the plan is keyed on it)
   if (m > 0 && B->nrows > 0) {
-    // a1 + a2: flop, symbolic bins
-    if ((st = launch_flop(c, A, B, 1, s)) != SPG_OK) return st;
+    // B nonempty-row bitmap: k_flop_nz skips the B.rp gathers of empty rows
+    // when most rows are empty (decided on the device)
+    const uint32_t *bnz = nullptr;
+    {
+      const int64_t nw = (B->nrows + 31) / 32;
+      if ((st = buf_ensure(c, c->bnz, size_t(nw) * 4, s)) != SPG_OK) return st;
+      ProfScope _ps(c, s, "k_b_rowmask");
+      k_b_rowmask<<<(unsigned)std::min<int64_t>(ceil_div(nw, 256), int64_t(c->num_sms) * 8), 256, 0, s>>>(
+          dev(B), (uint32_t *)c->bnz.p, info);
+      bnz = (const uint32_t *)c->bnz.p;
+    }
+    SPG_LAUNCHED(c, "k_b_rowmask");
+    // a1 + a2: flop, symbolic bins (+ per-row useful a_ik counts when most B
+    // rows are empty, for the pruning below)
+    if ((st = buf_ensure(c, c->prune_cnt, size_t(m) * 8, s)) != SPG_OK) return st;
+    SPG_CUDA(c, cudaMemsetAsync(c->prune_cnt.p, 0, size_t(m) * 8, s));
+    if ((st = launch_flop(c, A, B, 1, s, bnz, (unsigned long long *)c->prune_cnt.p)) != SPG_OK)
+      return st;
     {
       ProfScope _ps(c, s, "k_bin_scatter_sym");
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, A->row_ptr, B->ncols, 0, info,
@@ -411,6 +434,61 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     SPG_LAUNCHED(c, "k_bin_scatter(sym)");
     if ((st = read_info(c, s)) != SPG_OK) return st;
     PlanInfo h = *c->host_info;
+    if (2 * (int64_t)h.b_empty > B->nrows && 4 * (int64_t)h.useful < (int64_t)h.a_nnz &&
+        h.a_nnz >= (1ull << 20)) {
+      // most a_ik hit empty B rows: run the plan on A' = the useful a_ik of A
+      // (same rows, same flop; the walks of the symbolic / numeric tiers no
+      // longer visit the dead entries)
+      const int64_t nu = (int64_t)h.useful;
+      if ((st = buf_ensure(c, c->prune_rp, size_t(m + 1) * 8, s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->prune_col, size_t(std::max<int64_t>(nu, 1)) * 4, s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->prune_val, size_t(std::max<int64_t>(nu, 1)) * 8, s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->prune_idx, size_t(std::max<int64_t>(nu, 1)) * 8, s)) != SPG_OK) return st;
+      int64_t *cnt = (int64_t *)c->prune_cnt.p, *rp2 = (int64_t *)c->prune_rp.p;
+      DevCSR a = dev(A);
+      SPG_CUDA(c, cudaMemsetAsync(rp2, 0, 8, s));
+      SPG_CUDA(c, cudaMemcpyAsync(rp2 + 1, cnt, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
+      if ((st = launch_scan(c, rp2 + 1, m, s)) != SPG_OK) return st;
+      SPG_CUDA(c, cudaMemsetAsync(cnt, 0, size_t(m) * 8, s));
+      {
+        ProfScope _ps(c, s, "k_prune_scatter");
+        k_prune_scatter<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
+            a, bnz, (unsigned long long *)cnt, rp2, (int32_t *)c->prune_col.p,
+            (int64_t *)c->prune_idx.p);
+      }
+      SPG_LAUNCHED(c, "k_prune_scatter");
+      c->prune_n = nu;
+      c->Ap = spg_csr{m, A->ncols, rp2, (const int32_t *)c->prune_col.p,
+                      (const double *)c->prune_val.p};
+      c->pruned = true;
+      A = &c->Ap;
+      // re-bin on A': flop per row is unchanged (no flop pass again), the bins
+      // also depend on |a_i|; keep the first pass's B facts, reset the rest
+      {
+        PlanInfo h2{};
+        h2.max_brow = h.max_brow;
+        h2.b_end = h.b_end;
+        h2.b_empty = h.b_empty;
+        h2.useful = h.useful;
+        h2.a_nnz = (unsigned long long)nu;
+        *c->host_info = h2;  // (pinned; consumed by the copy before the next read_info)
+        SPG_CUDA(c, cudaMemcpyAsync(info, c->host_info, sizeof(PlanInfo), cudaMemcpyHostToDevice, s));
+      }
+      {
+        ProfScope _ps(c, s, "k_flop_stats");
+        const int64_t grid = std::min<int64_t>(ceil_div(m, 256), int64_t(c->num_sms) * 8);
+        k_flop_stats<<<(unsigned)grid, 256, 0, s>>>(dev(A), B->ncols, flop, info, 1);
+      }
+      SPG_LAUNCHED(c, "k_flop_stats");
+      {
+        ProfScope _ps(c, s, "k_bin_scatter_sym");
+        k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, flop, A->row_ptr, B->ncols, 0, info,
+                                                                 (int32_t *)c->rows_sym.p, row_nnz);
+      }
+      SPG_LAUNCHED(c, "k_bin_scatter(sym)");
+      if ((st = read_info(c, s)) != SPG_OK) return st;
+      h = *c->host_info;
+    }
     if ((int64_t)h.max_brow > kMaxBRow)
       return fail(c, SPG_ERR_OVERFLOW, "a row of B has more than 2^26 entries");
     // BM tier: is B row-sorted (column-range parts need it)?  parts buffers
@@ -520,7 +598,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   *nnz_C = (int64_t)c->plan.nnz_total;
   if (flop_total) *flop_total = (int64_t)c->plan.flop_total;
   c->have_plan = true;
-  c->plan_a_rp = A->row_ptr;
+  c->plan_a_rp = A0->row_ptr;
   c->plan_b_rp = B->row_ptr;
   c->plan_c_rp = C_row_ptr;
   c->plan_m = m;
@@ -545,6 +623,18 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   if (!A->val || !B->val) return fail(c, SPG_ERR_INVALID_ARG, "A.val / B.val is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   SPG_CUDA(c, cudaSetDevice(c->device));
+  if (c->pruned) {
+    // the plan runs on the pruned A' (same rows, same products): gather its
+    // values from the caller's A now (the symbolic needs none)
+    if (c->prune_n > 0) {
+      ProfScope _ps(c, s, "k_prune_values");
+      k_prune_values<<<(unsigned)std::min<int64_t>(ceil_div(c->prune_n, 256), int64_t(c->num_sms) * 8),
+                       256, 0, s>>>(A->val, (const int64_t *)c->prune_idx.p, c->prune_n,
+                                    (double *)c->prune_val.p);
+    }
+    SPG_LAUNCHED(c, "k_prune_values");
+    A = &c->Ap;
+  }
   DevCSR a = dev(A), b = dev(B);
   const int32_t *rows = (const int32_t *)c->rows_num.p;
   const int64_t *flop = (const int64_t *)c->flop.p;

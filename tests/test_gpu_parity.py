@@ -198,6 +198,24 @@ def test_c4_tallskinny_small(spg, ctx):
     gpu_vs_oracle(A, B, False, ctx=ctx, what="C4 s14")
 
 
+@pytest.mark.parametrize("sorted_out", [False, True])
+def test_c4_tallskinny_pruned(spg, ctx, sorted_out):
+    """Scale 16 (nnz(A) > 2^20, B 99.9% empty rows): the plan runs on the
+    pruned A' -- structure and values still exact vs the oracle, and a second
+    numeric on the same plan with other A values uses the new values."""
+    A, B, _ = synth.workload("c4_tallskinny", scale=16)
+    assert A.nnz >= (1 << 20)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="C4 s16 pruned")
+    A2 = synth.with_values(A, 77, 0.5, 1.5)
+    dA, dB = spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B)
+    dA2 = spg.DeviceCSR(A.nrows, A.ncols, dA.row_ptr, dA.col,
+                        torch.from_numpy(A2.val).to(dA.row_ptr.device))
+    rp, nnz, _ = spg.spg_symbolic(dA, dB, ctx)           # plan on A (values unused)
+    C = spg.spg_numeric(dA2, dB, rp, nnz, sorted_out, ctx)  # same structure, new values
+    from parity import compare
+    compare(*C.to_host(), *oracle.spgemm(A2, B), sorted_out, "C4 s16 pruned, new values")
+
+
 @pytest.mark.parametrize("scale", [10, 14])
 def test_c5_triangles_small(spg, ctx, scale):
     L, U, ex = synth.workload("c5_triangle", scale=scale)
