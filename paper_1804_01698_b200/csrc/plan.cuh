@@ -44,14 +44,37 @@ __device__ __forceinline__ int64_t advance_row(const int64_t *__restrict__ rp, i
   return lo;
 }
 
-// Rows of the first and last entries of the tile of kFlopTile consecutive
-// a_ik starting at t0 (threads 0 and 1) into s_r[0..1].
+// Row of the first a_ik of every tile of kFlopTile consecutive a_ik (one
+// thread per tile, all searches in parallel), plus the row of the last a_ik:
+// the nonzero-parallel kernels read their tile's row range from it instead
+// of searching row_ptr per tile.
+__global__ void __launch_bounds__(256) k_tile_rows(DevCSR A, int64_t cap, int64_t *__restrict__ trow) {
+  // trow[t] for t < min(ntile, cap) (+ the last row at index ntile if it fits)
+  const int64_t base = A.rp[0], nz = A.rp[A.nrows] - base;
+  const int64_t ntile = (nz + kFlopTile - 1) / kFlopTile;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t <= ntile && t <= cap;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    if (nz == 0) break;
+    const int64_t j = t < ntile ? base + t * kFlopTile : base + nz - 1;
+    trow[t] = row_of(A.rp, 0, A.nrows - 1, j);
+  }
+}
+
+// Rows of the first and last entries of the tile starting at t0 into
+// s_r[0..1]: from the tile-row index (last row of tile t = first row of tile
+// t + 1, or the row of the last a_ik), else by binary search.
 __device__ __forceinline__ void tile_rows(const DevCSR &A, int64_t base, int64_t t0, int64_t nz,
-                                          long long *s_r) {
+                                          long long *s_r, const int64_t *__restrict__ trow,
+                                          int64_t cap) {
   if (threadIdx.x < 2) {
-    const int64_t tl = (nz - t0) < kFlopTile ? (nz - t0) : kFlopTile;
-    const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : tl - 1);
-    s_r[threadIdx.x] = row_of(A.rp, 0, A.nrows - 1, j);
+    const int64_t t = t0 / kFlopTile;
+    if (trow && t + 1 <= cap) {
+      s_r[threadIdx.x] = threadIdx.x == 0 ? trow[t] : trow[t + 1];
+    } else {
+      const int64_t tl = (nz - t0) < kFlopTile ? (nz - t0) : kFlopTile;
+      const int64_t j = base + t0 + (threadIdx.x == 0 ? 0 : tl - 1);
+      s_r[threadIdx.x] = row_of(A.rp, 0, A.nrows - 1, j);
+    }
   }
 }
 
@@ -60,7 +83,8 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
                                                           const uint32_t *__restrict__ b_nonempty,
                                                           unsigned long long *__restrict__ flop,
                                                           PlanInfo *info,
-                                                          unsigned long long *__restrict__ useful_row) {
+                                                          unsigned long long *__restrict__ useful_row,
+                                                          const int64_t *__restrict__ trow, int64_t tcap) {
   __shared__ long long s_r[2];
   __shared__ unsigned long long s_maxb, s_useful;
   const int lane = threadIdx.x & 31;
@@ -72,7 +96,7 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
   if (threadIdx.x == 0) { s_maxb = 0; s_useful = 0; }
   for (int64_t t0 = int64_t(blockIdx.x) * kFlopTile; t0 < nz; t0 += int64_t(gridDim.x) * kFlopTile) {
     __syncthreads();
-    tile_rows(A, base, t0, nz, s_r);
+    tile_rows(A, base, t0, nz, s_r, trow, tcap);
     __syncthreads();
     const int64_t rlo = s_r[0], rhi = s_r[1];
     const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
@@ -174,12 +198,14 @@ __global__ void __launch_bounds__(kFlopThreads) k_prune_scatter(DevCSR A, const 
                                                                 unsigned long long *__restrict__ cursor,
                                                                 const int64_t *__restrict__ rp2,
                                                                 int32_t *__restrict__ col2,
-                                                                int64_t *__restrict__ idx2) {
+                                                                int64_t *__restrict__ idx2,
+                                                                const int64_t *__restrict__ trow,
+                                                                int64_t tcap) {
   __shared__ long long s_r[2];
   const int64_t base = A.rp[0], nz = A.rp[A.nrows] - base;
   for (int64_t t0 = int64_t(blockIdx.x) * kFlopTile; t0 < nz; t0 += int64_t(gridDim.x) * kFlopTile) {
     __syncthreads();
-    tile_rows(A, base, t0, nz, s_r);
+    tile_rows(A, base, t0, nz, s_r, trow, tcap);
     __syncthreads();
     const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
     const int64_t jend = base + nz;

@@ -41,6 +41,7 @@ struct spg_ctx {
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
   Buf parts, part_row, part_n, toff;  // column-tile parts of long rows (BM tier), B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
+  Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
   bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
   int64_t prune_n = 0;
   spg_csr Ap{};
@@ -190,10 +191,21 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
   int64_t *flop = (int64_t *)c->flop.p;
   DevCSR a = dev(A);
   SPG_CUDA(c, cudaMemsetAsync(flop, 0, size_t(m) * 8, s));
+  // tile-row index of A for the nonzero-parallel kernels (capacity m + 1
+  // tiles -- nnz(A) is not known on the host; tiles beyond it search)
+  spg_status st0;
+  if ((st0 = buf_ensure(c, c->trow, size_t(m + 1) * 8, s)) != SPG_OK) return st0;
+  {
+    ProfScope _ps(c, s, "k_tile_rows");
+    k_tile_rows<<<(unsigned)std::min<int64_t>(ceil_div(m + 1, 256), int64_t(c->num_sms) * 8), 256, 0, s>>>(
+        a, m, (int64_t *)c->trow.p);
+  }
+  SPG_LAUNCHED(c, "k_tile_rows");
   {
     ProfScope _ps(c, s, "k_flop_nz");
     k_flop_nz<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
-        a, B->row_ptr, B->nrows, bnz, (unsigned long long *)flop, info, useful_row);
+        a, B->row_ptr, B->nrows, bnz, (unsigned long long *)flop, info, useful_row,
+        (const int64_t *)c->trow.p, m);
   }
   SPG_LAUNCHED(c, "k_flop_nz");
   {
@@ -454,7 +466,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         ProfScope _ps(c, s, "k_prune_scatter");
         k_prune_scatter<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
             a, bnz, (unsigned long long *)cnt, rp2, (int32_t *)c->prune_col.p,
-            (int64_t *)c->prune_idx.p);
+            (int64_t *)c->prune_idx.p, (const int64_t *)c->trow.p, m);
       }
       SPG_LAUNCHED(c, "k_prune_scatter");
       c->prune_n = nu;
