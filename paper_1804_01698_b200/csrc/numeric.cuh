@@ -555,12 +555,14 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // ---------------------------------------------------------------------------
 constexpr int kTEnt = 1024;                 // a_ik staged per chunk
 constexpr int kTPartT = 2 * kTPartKeys;     // hash slots (load <= 1/2)
+constexpr int64_t kTRankCols = int64_t(8) * kTileCols;  // sorted emit by bitmap rank up to this span
 constexpr size_t kTDenseBytes = size_t(kTileCols) * 8 + size_t(kTileCols) / 8;
 constexpr size_t kTHashBytes = size_t(kTPartT) * 12 + size_t(kTPartKeys) * 2;
 constexpr size_t kTUnion = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;
 constexpr size_t kTEntBytes = 24576;        // es i64 + ea f64 + epre i32 [kTEnt(+1)]; sorted gather
 static_assert(size_t(kTEnt) * 20 + 4 <= kTEntBytes, "entry stage");
 static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
+static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
 
 // Number of lanes whose (nondecreasing across lanes) value wv is <= x: 0..32.
@@ -793,11 +795,46 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         gv[p] = hv[s];
       }
       __syncthreads();
-      int NB = 32;
-      while (NB < cnt) NB <<= 1;
-      uint32_t *scr = reinterpret_cast<uint32_t *>(base);
-      block_bucket_sort_to(gk, gv, cnt, NB, scr, scr + NB, scr + NB + kTPartKeys, out, c_col,
-                           c_val, s_red);
+      const int64_t span = (int64_t(t1 - t0)) << kTileLog;
+      if (span <= kTRankCols) {
+        // narrow part: rank by a bitmap over its columns [lo, lo + span)
+        // (table region as scratch): set bits, prefix popcounts per word,
+        // position = prefix + bits below in the word
+        uint32_t *rbm = reinterpret_cast<uint32_t *>(base);
+        int32_t *rpre = reinterpret_cast<int32_t *>(base + size_t(kTRankCols / 32) * 4);
+        const int nw = (int)(span >> 5);
+        for (int q = threadIdx.x; q < nw; q += THREADS) rbm[q] = 0u;
+        __syncthreads();
+        for (int p = threadIdx.x; p < cnt; p += THREADS) {
+          const uint32_t off = gk[p] - (uint32_t)lo;
+          atomicOr(rbm + (off >> 5), 1u << (off & 31u));
+        }
+        __syncthreads();
+        const int per = (nw + THREADS - 1) / THREADS;
+        const int q0 = min(nw, (int)threadIdx.x * per), q1 = min(nw, q0 + per);
+        int mine = 0;
+        for (int q = q0; q < q1; ++q) mine += __popc(rbm[q]);
+        int tot;
+        int ex = block_excl_scan_int(mine, s_warp, &tot);
+        for (int q = q0; q < q1; ++q) {
+          rpre[q] = ex;
+          ex += __popc(rbm[q]);
+        }
+        __syncthreads();
+        for (int p = threadIdx.x; p < cnt; p += THREADS) {
+          const uint32_t off = gk[p] - (uint32_t)lo;
+          const uint32_t wd = off >> 5;
+          const int64_t o = out + rpre[wd] + __popc(rbm[wd] & ((1u << (off & 31u)) - 1u));
+          c_col[o] = (int32_t)gk[p];
+          c_val[o] = gv[p];
+        }
+      } else {
+        int NB = 32;
+        while (NB < cnt) NB <<= 1;
+        uint32_t *scr = reinterpret_cast<uint32_t *>(base);
+        block_bucket_sort_to(gk, gv, cnt, NB, scr, scr + NB, scr + NB + kTPartKeys, out, c_col,
+                             c_val, s_red);
+      }
     }
     __syncthreads();
     if (instr) {
