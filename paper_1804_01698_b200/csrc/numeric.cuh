@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
                                                        double *__restrict__ c_val, int sorted,
                                                        int tmax) {
   extern __shared__ double s_dyn_f64[];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_next;
   __shared__ int s_red[66];
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5;
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
     const int logT = num_log2(nnz);
     const int T = 1 << logT;
     for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
@@ -396,8 +396,8 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
       auto acc_comb = [&](bool act, uint32_t c, double v) {  // keys may repeat in a round
         if (warp_combine(act, c, v)) atomicAdd(vals + num_probe_smem(keys, c, logT), v);
       };
-      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc);
-      else for_row<false, true>(A, B, as, ae, w, NW, acc_comb);
+      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc_comb, &s_next);
     }
     __syncthreads();
     block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
                                                         double *__restrict__ slab_vals,
                                                         int64_t slabT) {
   extern __shared__ uint32_t s_dyn_u32[];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_next;
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5;
   uint32_t *keys = slab_keys + int64_t(blockIdx.x) * slabT;
@@ -515,15 +515,15 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
     const int logT = num_log2(nnz);
     const int64_t T = int64_t(1) << logT;
     for (int64_t s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
       auto acc = [&](bool act, uint32_t c, double v) {
         if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
       };
-      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc);
-      else for_row<false, true>(A, B, as, ae, w, NW, acc);
+      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc, &s_next);
     }
     __syncthreads();
     if (!sorted) {
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_warp[33];
   __shared__ int s_red[66];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_next;
   __shared__ long long s_q;
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     } else {
       for (int s = threadIdx.x; s < T; s += THREADS) { hk[s] = kEmpty; hv[s] = 0.0; }
     }
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     const int64_t as = A.rp[i];
     const int na = (int)(A.rp[i + 1] - as);
     auto acc = [&](bool act, uint32_t c, double v) {

@@ -56,27 +56,47 @@ __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
 // `entry(j) -> Entry{bs, len, a}` describes entry j of the row: the B
 // segment [bs, bs+len) that its a_ik multiplies.  kVal = false skips values.
 // ---------------------------------------------------------------------------
+constexpr int kFlatAvgLen = 12;  // kAutoFlat: chunks averaging shorter B rows run flattened
+
 struct Entry {
   int64_t bs;
   int len;
   double a;
 };
 
-template <bool kSeq, bool kVal, int kDepth, typename EF, typename F>
+template <bool kSeq, bool kVal, int kDepth, bool kAutoFlat = false, typename EF, typename F>
 __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w, int NW,
-                                            EF &&entry, F &&f) {
+                                            EF &&entry, F &&f, int *next = nullptr) {
   const int lane = lane_id();
-  // Many chunks: each warp owns whole chunks (chunk overhead paid once).  Few
-  // chunks: every warp walks every chunk and takes a contiguous slice of its
-  // rounds (keeps all warps busy on rows with few, long B rows).
+  // Many chunks: each warp owns whole chunks (chunk overhead paid once) --
+  // taken from the block's counter `next` when given (chunk costs differ with
+  // the B-row lengths), else strided.  Few chunks: every warp walks every
+  // chunk and takes a contiguous slice of its rounds (keeps all warps busy on
+  // rows with few, long B rows).
   const int64_t nchunks = (nent + 31) >> 5;
   const bool own_chunks = NW == 1 || nchunks >= 2 * int64_t(NW);
-  const int64_t c_first = own_chunks ? int64_t(w) * 32 : 0;
-  const int64_t c_step = own_chunks ? int64_t(NW) * 32 : 32;
-  for (int64_t cb = c_first; cb < nent; cb += c_step) {
+  const bool dyn = own_chunks && next != nullptr && NW > 1;
+  auto next_chunk = [&](int64_t cur) -> int64_t {
+    if (!dyn) return own_chunks ? cur + int64_t(NW) * 32 : cur + 32;
+    int v = 0;
+    if (lane == 0) v = atomicAdd(next, 32);
+    return (int64_t)__shfl_sync(kFull, v, 0);
+  };
+  int64_t cb0 = own_chunks ? int64_t(w) * 32 : 0;
+  if (dyn) cb0 = next_chunk(0);
+  for (int64_t cb = cb0; cb < nent; cb = next_chunk(cb)) {
     Entry en{0, 0, 0.0};
     if (cb + lane < nent) en = entry(cb + lane);
-    if (kSeq && own_chunks && __all_sync(kFull, en.len <= 32)) {
+    // kAutoFlat (f tolerates equal keys inside a round): a chunk of short B
+    // rows (average < kFlatAvgLen) runs flattened (full lanes) even in a
+    // sequential row
+    bool seq = kSeq;
+    if (kSeq && kAutoFlat && own_chunks) {
+      const int sum = (int)__reduce_add_sync(kFull, (unsigned)en.len);
+      const int ne = __popc(__ballot_sync(kFull, en.len > 0));
+      seq = sum >= kFlatAvgLen * ne;
+    }
+    if (seq && own_chunks && __all_sync(kFull, en.len <= 32)) {
       // this warp owns the chunk and every B row fits one round: one round per
       // nonempty entry.  kDepth <= 2 (warp tiers, occupancy-bound): one round
       // ahead.  Deeper (block / bitmap tiers): rolling software pipeline over
@@ -153,7 +173,7 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
       }
       continue;
     }
-    if (kSeq && own_chunks) {
+    if (seq && own_chunks) {
       // this warp owns the chunk: walk its nonempty entries directly
       unsigned pend = __ballot_sync(kFull, en.len > 0);
       while (pend) {
@@ -175,14 +195,14 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
       }
       continue;
     }
-    const int r = kSeq ? ((en.len + 31) >> 5) : en.len;  // rounds (seq) or products
+    const int r = seq ? ((en.len + 31) >> 5) : en.len;  // rounds (seq) or products
     const int incl = warp_incl_scan(r);
     const int total = __shfl_sync(kFull, incl, 31);
-    const int nr = kSeq ? total : ((total + 31) >> 5);
+    const int nr = seq ? total : ((total + 31) >> 5);
     const int g0 = own_chunks ? 0 : (int)((int64_t)nr * w / NW);
     const int g1 = own_chunks ? nr : (int)((int64_t)nr * (w + 1) / NW);
     if (g0 >= g1) continue;
-    if (kSeq) {
+    if (seq) {
       // the owner entry of round g advances monotonically along [g0, g1)
       int own = 0, obeg = 0, oend = 0, olen = 0;
       int64_t obs = 0;
@@ -245,10 +265,10 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
 }
 
 // All products of row [as, ae) of A.
-template <bool kSeq, bool kVal, int kDepth = (kVal ? 4 : 8), typename F>
+template <bool kSeq, bool kVal, int kDepth = (kVal ? 4 : 8), bool kAutoFlat = false, typename F>
 __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_t as,
-                                        int64_t ae, int w, int NW, F &&f) {
-  for_entries<kSeq, kVal, kDepth>(
+                                        int64_t ae, int w, int NW, F &&f, int *next = nullptr) {
+  for_entries<kSeq, kVal, kDepth, kAutoFlat>(
       B, ae - as, w, NW,
       [&](int64_t j) {
         const int k = __ldg(A.col + as + j);
@@ -258,7 +278,7 @@ __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_
         en.a = kVal ? __ldg(A.val + as + j) : 0.0;
         return en;
       },
-      f);
+      f, next);
 }
 
 // Rows whose B rows average >= kSeqMinLen entries use the sequential
@@ -309,7 +329,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
                                                        const int64_t *__restrict__ flop,
                                                        int64_t *__restrict__ row_nnz) {
   extern __shared__ uint32_t s_dyn_u32[];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_next;
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_dyn_u32;
@@ -318,15 +338,15 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
     const int logT = sym_log2_gpu(flop[i], B.ncols);
     const int T = 1 << logT;
     for (int s = threadIdx.x; s < T; s += THREADS) tab[s] = kEmpty;
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
       if (act) cnt += sym_insert_smem(tab, c, logT);
     };
-    if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
-    else for_row<false, false>(A, B, as, ae, w, NW, ins);
+    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
+    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
@@ -393,7 +413,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         int32_t *__restrict__ part_row,
                                                         int32_t *__restrict__ part_n) {
   extern __shared__ uint32_t s_dyn_u32[];
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_next;
   __shared__ int s_warp[THREADS / 32];
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_cut[kMaxTiles];       // first tile of each part
@@ -406,15 +426,15 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int i = rows[r];
     for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
       if (act) cnt += sym_bitmap_insert(bm, c);
     };
-    if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
-    else for_row<false, false>(A, B, as, ae, w, NW, ins);
+    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
+    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
@@ -470,7 +490,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_global(const int32_t *__restric
                                                         int64_t *__restrict__ row_nnz,
                                                         uint32_t *__restrict__ slab,
                                                         int64_t slabT) {
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_next;
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = slab + int64_t(blockIdx.x) * slabT;
@@ -479,7 +499,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_global(const int32_t *__restric
     const int logT = sym_log2_gpu(flop[i], B.ncols);
     const int64_t T = int64_t(1) << logT;
     for (int64_t s = threadIdx.x; s < T; s += THREADS) tab[s] = kEmpty;
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
     int cnt = 0;
     {
@@ -487,8 +507,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_global(const int32_t *__restric
       auto ins = [&](bool act, uint32_t c, double) {
         if (act) cnt += sym_insert(tab, c, logT);
       };
-      if (use_seq(flop[i], ae - as)) for_row<true, false>(A, B, as, ae, w, NW, ins);
-      else for_row<false, false>(A, B, as, ae, w, NW, ins);
+      if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
+      else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
     }
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
