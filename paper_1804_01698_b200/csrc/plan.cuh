@@ -166,27 +166,22 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
 }
 
 // Nonempty-row bitmap of B (bit k = B row k has entries) and its count of
-// empty rows (info->b_empty): one thread per 32 rows.
+// empty rows (info->b_empty): one thread per row, words built by warp ballots.
 __global__ void __launch_bounds__(256) k_b_rowmask(DevCSR B, uint32_t *__restrict__ bm,
                                                    PlanInfo *info) {
-  const int64_t nw = (B.nrows + 31) >> 5;
+  const int lane = threadIdx.x & 31;
   unsigned long long empty = 0;
-  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nw;
-       w += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t word = 0u;
-    const int64_t k0 = w << 5;
-    const int nk = (B.nrows - k0) < 32 ? int(B.nrows - k0) : 32;
-    int64_t prev = B.rp[k0];
-    for (int t = 0; t < nk; ++t) {
-      const int64_t nxt = B.rp[k0 + t + 1];
-      if (nxt > prev) word |= 1u << t;
-      prev = nxt;
-    }
-    bm[w] = word;
-    empty += (unsigned long long)(nk - __popc(word));
+  const int64_t nr32 = ((B.nrows + 31) >> 5) << 5;
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nr32;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const bool valid = k < B.nrows;
+    const bool ne = valid && B.rp[k + 1] > B.rp[k];
+    const unsigned word = __ballot_sync(kFull, ne);
+    if (lane == 0) bm[k >> 5] = word;
+    empty += (valid && !ne) ? 1ull : 0ull;
   }
   empty = warp_sum(empty);
-  if ((threadIdx.x & 31) == 0 && empty) atomicAdd(&info->b_empty, empty);
+  if (lane == 0 && empty) atomicAdd(&info->b_empty, empty);
 }
 
 // Pruning of A for a mostly-empty B: a_ik whose B row is empty contribute no

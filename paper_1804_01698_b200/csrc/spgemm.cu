@@ -427,7 +427,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       const int64_t nw = (B->nrows + 31) / 32;
       if ((st = buf_ensure(c, c->bnz, size_t(nw) * 4, s)) != SPG_OK) return st;
       ProfScope _ps(c, s, "k_b_rowmask");
-      k_b_rowmask<<<(unsigned)std::min<int64_t>(ceil_div(nw, 256), int64_t(c->num_sms) * 8), 256, 0, s>>>(
+      k_b_rowmask<<<(unsigned)std::min<int64_t>(ceil_div(nw * 32, 256), int64_t(c->num_sms) * 8), 256, 0, s>>>(
           dev(B), (uint32_t *)c->bnz.p, info);
       bnz = (const uint32_t *)c->bnz.p;
     }
