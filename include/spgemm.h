@@ -163,10 +163,13 @@ spg_status spg_rows_to_parts(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
                              void *stream);
 
 /* Masked sum for triangle counting (Sec 5.6; BASELINE config 5):
- * sum over stored C(i,j) with (i,j) in pattern(G) of (int64)C(i,j).
- * C rows may be in any order; G rows MUST be sorted ascending; C.nrows ==
- * G.nrows rows are matched by index, C a row block starting at row
- * g_row_begin of G.  Result to HOST *sum (blocks for 8 bytes). */
+ * sum over stored C(i,j) with (i,j) in pattern(G) of C(i,j), accumulated in
+ * fp64 and rounded to the nearest int64 (exact for integer-valued C below
+ * 2^53, e.g. the wedge counts of L*U).  C and G rows may be in any column
+ * order (G rows sorted ascending when G.ncols > 1.6M: binary search); row i
+ * of C is row g_row_begin + i of G.  G's row is an smem hash set (short rows)
+ * or bitmap (long rows) probed by every C entry.  Result to HOST *sum
+ * (blocks for 8 bytes). */
 spg_status spg_mask_sum(spg_ctx *ctx, const spg_csr *C, const spg_csr *G,
                         int64_t g_row_begin, int64_t *sum, void *stream);
 

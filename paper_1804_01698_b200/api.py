@@ -212,7 +212,10 @@ def triangle_count_rows(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, r0: int, r1: i
         return 0
     Lr = L.rows(r0, r1)
     if block_entries is None:
-        free, _ = torch.cuda.mem_get_info(L.row_ptr.device)
+        dev = L.row_ptr.device
+        free, _ = torch.cuda.mem_get_info(dev)
+        # memory cached by torch's allocator is reusable for the C blocks too
+        free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
         block_entries = max(1 << 20, int(free * 0.6) // 12)
     offs = row_blocks_by_bytes(Lr, U, block_entries, ctx)
     total = 0

@@ -148,4 +148,100 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
   if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
 }
 
+// ---------------------------------------------------------------------------
+// a9 (triangle counting with C formed): sum over stored C(i,j) with
+// (i,j) in pattern(G) of C(i,j).  Same mask structures as above: G's row is a
+// warp-private hash set (short rows) or an ncols-bit block bitmap (long rows;
+// binary search of the sorted G row when ncols > kBitmapMaxCols); the C row
+// is read once, coalesced, and every entry probes the set.
+// ---------------------------------------------------------------------------
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevCSR G,
+                                                                  int64_t g_row_begin,
+                                                                  unsigned long long *row_counter,
+                                                                  double *sum) {
+  __shared__ uint32_t s_tab[WARPS][kMaskWarpT];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *tab = s_tab[w];
+  double acc = 0.0;
+  while (true) {
+    long long r = 0;
+    if (lane == 0) r = (long long)atomicAdd(row_counter, 1ull);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= C.nrows) break;
+    const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
+    const int64_t cs = C.rp[r], ce = C.rp[r + 1];
+    const int64_t gn = ge - gs;
+    if (gn == 0 || gn > kMaskWarpKeys || cs == ce) continue;  // (block tier: long G rows)
+    const int lg = log2_ceil64(uint64_t(2 * gn));
+    const int logT = lg < kMinLogT ? kMinLogT : lg;
+    const int T = 1 << logT;
+    for (int s = lane; s < T; s += 32) tab[s] = kEmpty;
+    __syncwarp();
+    for (int64_t q = gs + lane; q < ge; q += 32) sym_insert(tab, (uint32_t)__ldg(G.col + q), logT);
+    __syncwarp();
+    for (int64_t q = cs + lane; q < ce; q += 32)
+      if (set_contains(tab, (uint32_t)__ldg(C.col + q), logT)) acc += __ldg(C.val + q);
+    __syncwarp();
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_csr_mask_sum_block(DevCSR C, DevCSR G,
+                                                                int64_t g_row_begin,
+                                                                unsigned long long *row_counter,
+                                                                double *sum, int use_bitmap) {
+  extern __shared__ uint32_t s_bm[];
+  __shared__ long long s_row;
+  const int lane = threadIdx.x & 31;
+  const int nwords = (int)((G.ncols + 31) >> 5);
+  if (use_bitmap)
+    for (int s = threadIdx.x; s < nwords; s += THREADS) s_bm[s] = 0u;
+  double acc = 0.0;
+  while (true) {
+    if (threadIdx.x == 0) s_row = (long long)atomicAdd(row_counter, 1ull);
+    __syncthreads();
+    const long long r = s_row;
+    if (r >= C.nrows) break;
+    const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
+    const int64_t cs = C.rp[r], ce = C.rp[r + 1];
+    if (ge - gs <= kMaskWarpKeys || cs == ce) {
+      __syncthreads();
+      continue;
+    }
+    if (use_bitmap)
+      for (int64_t q = gs + threadIdx.x; q < ge; q += THREADS) {
+        const uint32_t c = (uint32_t)__ldg(G.col + q);
+        atomicOr(s_bm + (c >> 5), 1u << (c & 31u));
+      }
+    __syncthreads();
+    for (int64_t q = cs + threadIdx.x; q < ce; q += THREADS) {
+      const uint32_t c = (uint32_t)__ldg(C.col + q);
+      bool hit;
+      if (use_bitmap) {
+        hit = (s_bm[c >> 5] >> (c & 31u)) & 1u;
+      } else {
+        int64_t lo = gs, hi = ge;
+        while (lo < hi) {
+          const int64_t m = (lo + hi) >> 1;
+          if ((uint32_t)__ldg(G.col + m) < c) lo = m + 1; else hi = m;
+        }
+        hit = lo < ge && (uint32_t)__ldg(G.col + lo) == c;
+      }
+      if (hit) acc += __ldg(C.val + q);
+    }
+    __syncthreads();
+    if (use_bitmap)
+      for (int64_t q = gs + threadIdx.x; q < ge; q += THREADS) {
+        const uint32_t c = (uint32_t)__ldg(G.col + q);
+        s_bm[c >> 5] = 0u;
+      }
+    __syncthreads();
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
+}
+
 }  // namespace spg

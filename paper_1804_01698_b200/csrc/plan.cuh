@@ -488,34 +488,6 @@ __global__ void k_lowbnd(const int64_t *__restrict__ ps, int64_t m, int64_t npar
 }
 
 // ---------------------------------------------------------------------------
-// a9: sum over stored C(i,j) with (i,j) in pattern(G) of (int64)C(i,j)
-// (triangle counting, Sec 5.6; BASELINE config 5).  Warp per C row,
-// binary search of each C column in the sorted G row.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_mask_sum(DevCSR C, DevCSR G, int64_t g_row_begin,
-                                                  PlanInfo *info) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  long long acc = 0;
-  for (int64_t i = warp; i < C.nrows; i += nwarps) {
-    const int64_t gs = G.rp[g_row_begin + i], ge = G.rp[g_row_begin + i + 1];
-    if (gs == ge) continue;
-    for (int64_t q = C.rp[i] + lane; q < C.rp[i + 1]; q += 32) {
-      const int j = C.col[q];
-      int64_t lo = gs, hi = ge;
-      while (lo < hi) {
-        const int64_t mid = lo + (hi - lo) / 2;
-        if (__ldg(G.col + mid) < j) lo = mid + 1; else hi = mid;
-      }
-      if (lo < ge && __ldg(G.col + lo) == j) acc += (long long)C.val[q];
-    }
-  }
-  acc = warp_sum(acc);
-  if (lane == 0 && acc) atomicAdd(&info->mask_sum, (unsigned long long)acc);
-}
-
-// ---------------------------------------------------------------------------
 // Validation (untimed): flags bit0 = row_ptr decreasing, bit1 = column out of
 // range, bit2 = row not strictly increasing (only when check_sorted).
 // ---------------------------------------------------------------------------

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -307,6 +308,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_tpart<512>, kTPartSmem) == SPG_OK &&
          set_smem(c, k_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
+         set_smem(c, k_csr_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
   }
   if (!ok) {
@@ -825,20 +827,26 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
   SPG_CUDA(c, cudaSetDevice(c->device));
   if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
-  SPG_CUDA(c, cudaMemsetAsync(&info->mask_sum, 0, 8, s));
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 3 * 8, s));  // both queues and the fp64 sum
   if (C->nrows > 0) {
-    const int64_t grid = std::min<int64_t>(ceil_div(C->nrows, 8), int64_t(c->num_sms) * 16);
     {
-      ProfScope _ps(c, s, "k_mask_sum");
-      k_mask_sum<<<(unsigned)grid, 256, 0, s>>>(dev(C), dev(G), g_row_begin, info);
+      ProfScope _ps(c, s, "k_csr_mask_sum_warp<8>");
+      k_csr_mask_sum_warp<kWarps><<<(unsigned)(c->num_sms * 8), kWarps * 32, 0, s>>>(
+          dev(C), dev(G), g_row_begin, &info->mask_ctr[0], &info->mask_acc);
     }
-    SPG_LAUNCHED(c, "k_mask_sum");
+    SPG_LAUNCHED(c, "k_csr_mask_sum_warp");
+    const int use_bitmap = G->ncols <= kBitmapMaxCols ? 1 : 0;
+    const size_t smem = use_bitmap ? size_t((G->ncols + 31) / 32) * 4 : 0;
+    {
+      ProfScope _ps(c, s, "k_csr_mask_sum_block<1024>");
+      k_csr_mask_sum_block<1024><<<(unsigned)c->num_sms, 1024, smem, s>>>(
+          dev(C), dev(G), g_row_begin, &info->mask_ctr[1], &info->mask_acc, use_bitmap);
+    }
+    SPG_LAUNCHED(c, "k_csr_mask_sum_block");
   }
-  unsigned long long h = 0;
-  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_sum, &info->mask_sum, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
-  h = c->host_info->mask_sum;
-  *sum = (int64_t)h;
+  *sum = (int64_t)llround(c->host_info->mask_acc);
   return SPG_OK;
 }
 
