@@ -745,8 +745,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       __syncthreads();
       const long long cbk = instr ? clock64() : 0;
       const int R = (Pn + 31) >> 5;
-      for_tpart_rounds(B, es, ea, epre, n, Pn, (int)((int64_t)R * w / NW),
-                       (int)((int64_t)R * (w + 1) / NW), acc);
+      for_tpart_rounds<2>(B, es, ea, epre, n, Pn, (int)((int64_t)R * w / NW),
+                          (int)((int64_t)R * (w + 1) / NW), acc);
       if (instr) {
         c_stage += cbk - ca;
         c_rounds += clock64() - cbk;  // (thread 0's own rounds; the barrier wait lands in the next stage)

@@ -187,6 +187,8 @@ __device__ __forceinline__ uint32_t probe_chunk(uint32_t *keys, uint32_t c, int 
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
+
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
