@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // ---------------------------------------------------------------------------
 constexpr int kTEnt = 1024;                 // a_ik staged per chunk
 constexpr int kTPartT = 2 * kTPartKeys;     // hash slots (load <= 1/2)
-constexpr int64_t kTRankCols = int64_t(8) * kTileCols;  // sorted emit by bitmap rank up to this span
+constexpr int64_t kTRankCols = int64_t(32) * kTileCols;  // sorted emit by bitmap rank up to this span
 constexpr size_t kTDenseBytes = size_t(kTileCols) * 8 + size_t(kTileCols) / 8;
 constexpr size_t kTHashBytes = size_t(kTPartT) * 12 + size_t(kTPartKeys) * 2;
 constexpr size_t kTUnion = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;

@@ -655,12 +655,13 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   // G tier: column-tile parts (B sorted, parts cut by the symbolic) or the
   // global-hash fallback (slab: keys + vals of lowest 2^n >= 2 max nnz(c_i) per block)
   int64_t g_grid = 0, slabT = 0, ntiles = 0;
-  const bool use_parts = c->plan_parts && h.b_unsorted == 0 && h.parts_overflow == 0;
+  // (tile offsets are int32 positions: a B with >= 2^31 entries takes the
+  // global-hash tier instead)
+  const bool use_parts = c->plan_parts && h.b_unsorted == 0 && h.parts_overflow == 0 &&
+                         h.b_end < (unsigned long long)INT32_MAX;
   if (h.num_count[NB_G]) {
     if (use_parts) {
       ntiles = (B->ncols + kTileCols - 1) / kTileCols;
-      if (h.b_end >= (unsigned long long)INT32_MAX)
-        return fail(c, SPG_ERR_OVERFLOW, "tile offsets need B.row_ptr[nrows] < 2^31");
       if ((st = buf_ensure(c, c->toff, size_t(B->nrows) * size_t(ntiles + 1) * 4, s)) != SPG_OK)
         return st;
       SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));

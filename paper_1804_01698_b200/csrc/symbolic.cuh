@@ -428,13 +428,17 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;
     if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
-    int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    // set the bit of every product's column (the old value is not used: no
+    // dependency on the atomic's return), then count the set bits once
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) cnt += sym_bitmap_insert(bm, c);
+      if (act) atomicOr(bm + (c >> 5), 1u << (c & 31u));
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
     else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
+    __syncthreads();
+    int cnt = 0;
+    for (int q = threadIdx.x; q < nwords; q += THREADS) cnt += __popc(bm[q]);
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
