@@ -78,6 +78,69 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
       base += __popc(bal);
     }
   } else {
+    if (nnz <= 128 && T <= 256) {
+      // <= 128 keys: bitonic sort in registers of packed
+      // (column - min) << 8 | slot, 4 per lane (element e = 4 lane + r); the
+      // values stay in their slots until the store.  Needs a span < 2^24.
+      unsigned mn = 0xFFFFFFFFu, mx = 0u;
+      for (int s0 = 0; s0 < T; s0 += 32) {
+        const unsigned k = keys[s0 + lane];
+        if (k != kEmpty) {
+          mn = k < mn ? k : mn;
+          mx = k > mx ? k : mx;
+        }
+      }
+      mn = __reduce_min_sync(kFull, mn);
+      mx = __reduce_max_sync(kFull, mx);
+      if (mx - mn < (1u << 24)) {
+        uint32_t *pk_s = cnt;  // scratch: packed keys compacted to the front
+        int base = 0;
+        for (int s0 = 0; s0 < T; s0 += 32) {
+          const uint32_t k = keys[s0 + lane];
+          const bool occ = k != kEmpty;
+          const unsigned bal = __ballot_sync(kFull, occ);
+          if (occ) pk_s[base + __popc(bal & lt_mask)] = ((k - mn) << 8) | (uint32_t)(s0 + lane);
+          base += __popc(bal);
+        }
+        for (int e = base + lane; e < 128; e += 32) pk_s[e] = 0xFFFFFFFFu;
+        __syncwarp();
+        const uint4 kk = reinterpret_cast<const uint4 *>(pk_s)[lane];
+        uint32_t pk[4] = {kk.x, kk.y, kk.z, kk.w};
+#pragma unroll
+        for (int k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 4) {  // partner: same r in lane ^ (j / 4)
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                const uint32_t o = __shfl_xor_sync(kFull, pk[r], j >> 2);
+                const int e = 4 * lane + r;
+                const bool keepmin = ((e & j) == 0) == ((e & k) == 0);
+                pk[r] = keepmin ? min(pk[r], o) : max(pk[r], o);
+              }
+            } else {  // partner: register r ^ j of this lane
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                if (r & j) continue;
+                const int e = 4 * lane + r;
+                const uint32_t a = pk[r], b = pk[r | j];
+                const bool up = (e & k) == 0;
+                if ((a > b) == up) { pk[r] = b; pk[r | j] = a; }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int e = 4 * lane + r;
+          if (e < nnz) {
+            c_col[rp0 + e] = (int32_t)(mn + (pk[r] >> 8));
+            c_val[rp0 + e] = vals[pk[r] & 255u];
+          }
+        }
+        return;
+      }
+    }
     // a7: ascending columns by a bucket (counting) sort.  Buckets
     // are monotone in the column: b(c) = (c - min) >> sh, T buckets for
     // nnz <= T/2 keys; each key's position = bucket offset + its rank
@@ -107,51 +170,7 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
     }
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
-    if (nnz <= 128 && mx - mn < (1u << 25)) {
-      // <= 128 keys within 2^25 columns: bitonic sort in registers of packed
-      // (column - min) << 7 | index, 4 per lane (element e = 4 lane + r)
-      uint32_t pk[4];
-      const uint4 kk = reinterpret_cast<const uint4 *>(keys)[lane];  // keys[4 lane .. 4 lane + 3]
-      const uint32_t kr[4] = {kk.x, kk.y, kk.z, kk.w};
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int e = 4 * lane + r;
-        pk[r] = e < nnz ? ((kr[r] - mn) << 7) | (uint32_t)e : 0xFFFFFFFFu;
-      }
-#pragma unroll
-      for (int k = 2; k <= 128; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          if (j >= 4) {  // partner: same r in lane ^ (j / 4)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const uint32_t o = __shfl_xor_sync(kFull, pk[r], j >> 2);
-              const int e = 4 * lane + r;
-              const bool keepmin = ((e & j) == 0) == ((e & k) == 0);
-              pk[r] = keepmin ? min(pk[r], o) : max(pk[r], o);
-            }
-          } else {  // partner: register r ^ j of this lane
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              if (r & j) continue;
-              const int e = 4 * lane + r;
-              const uint32_t a = pk[r], b = pk[r | j];
-              const bool up = (e & k) == 0;
-              if ((a > b) == up) { pk[r] = b; pk[r | j] = a; }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int e = 4 * lane + r;
-        if (e < nnz) {
-          c_col[rp0 + e] = (int32_t)(mn + (pk[r] >> 7));
-          c_val[rp0 + e] = vals[pk[r] & 127u];
-        }
-      }
-      return;
-    }
+
     int sh = log2_ceil64(uint64_t(mx - mn) + 1) - logT;
     sh = sh < 0 ? 0 : sh;
     for (int b = lane; b < T; b += 32) cnt[b] = 0u;
