@@ -403,10 +403,7 @@ def run_ours(args):
 
     # ---- e2e: through the public API with HOST buffers (H2D of A,B from pinned
     # memory, the multiply, D2H of C) inside the timed region
-    e2e = None
-    if rank == 0 or world > 1:
-        e2e = e2e_measure(args, spg, ctx, A if rank == 0 else None, B if rank == 0 else None,
-                          same, dev, world, rank, r0, r1, tri, extra if rank == 0 else None)
+    e2e = e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total)
 
     # ---- roofline of the dominant kernel (live per-launch events, sorted run)
     roof = None
@@ -441,11 +438,17 @@ def run_ours(args):
                                "(share = kernel time / sum of the step's kernel times)",
                 "kernels_ms_per_step": {n: v[0] / prof_steps for n, v in sorted(agg.items(), key=lambda x: -x[1][0])}}
 
+    # nnz(C) of the whole job (each rank holds its row block's row_ptr)
+    nnzC = None
+    if Cs is not None and not tri:
+        t = torch.tensor([int(Cs[-1].item()) - int(Cs[0].item())], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(t)
+        nnzC = int(t.item())
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = oracle_sample(A, B, target_s=args.cpu_seconds)
-        nnzC = int(Cs[-1].item()) if (Cs is not None and not tri) else None
         mb = None
         if nnzC is not None:
             mb = (8 * (A.nrows + 1) + 12 * A.nnz + 8 * (B.nrows + 1) + 12 * flop_total
@@ -466,7 +469,8 @@ def run_ours(args):
                                                     "product (SURVEY 8(f) row 1); C not formed"}}
                             if ms_fused is not None else {})},
             "minimal_bytes_model": mb,
-            "hbm_roofline_frac_step": (mb / (ms_sorted * 1e-3) / 1e9 / measured_peak()[0]) if mb else None,
+            "hbm_roofline_frac_step": (mb / (ms_sorted * 1e-3) / 1e9 / (world * measured_peak()[0]))
+                                      if mb else None,
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -480,71 +484,82 @@ def run_ours(args):
     return 0
 
 
-def e2e_measure(args, spg, ctx, A, B, same, dev, world, rank, r0, r1, tri, extra):
-    """Same metric through the public API with host (pinned) buffers: H2D of
-    the inputs, C = A*B, D2H of C (chunked through a bounded pinned buffer)."""
+def e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total):
+    """Same metric through the public API with host (pinned) buffers: every
+    rank uploads ITS inputs (rows [r0, r1) of A, all of B, and for C5 the same
+    rows of G) from pinned host memory, multiplies (C5: counts), and reads its
+    result back (rows [r0, r1) of C, chunked through a bounded pinned buffer;
+    C5: the count).  Time = max over ranks of the per-step device events; the
+    byte counts are summed over ranks (whole job)."""
     import torch
     import torch.distributed as dist
-    if world > 1 and rank != 0:
-        return None
-    if world > 1:
-        return None  # multi-rank e2e: reported by rank 0 only at N=1 (see DESIGN.md)
 
-    def pin(M):
-        return (torch.from_numpy(M.row_ptr).pin_memory(), torch.from_numpy(M.col).pin_memory(),
-                torch.from_numpy(M.val).pin_memory())
-    hA = pin(A)
-    hB = hA if same else pin(B)
-    hG = pin(extra["G"]) if tri else None
+    def host_rows(M, a, b):  # pinned host copy of rows [a, b) of a device CSR, row_ptr rebased
+        rp = M.row_ptr[a:b + 1]
+        s, e = int(rp[0].item()), int(rp[-1].item())
+        return ((rp - s).cpu().pin_memory(), M.col[s:e].cpu().pin_memory(),
+                M.val[s:e].cpu().pin_memory(), M.ncols)
+
+    hA = host_rows(dA, r0, r1)
+    hB = host_rows(dB, 0, dB.nrows) if not (same and world == 1) else hA
+    hG = host_rows(dG, r0, r1) if tri else None
+    m = r1 - r0
     chunk = 1 << 28
     outbuf_c = torch.empty(chunk // 4, dtype=torch.int32).pin_memory()
     outbuf_v = torch.empty(chunk // 8, dtype=torch.float64).pin_memory()
-    outbuf_r = torch.empty(A.nrows + 1, dtype=torch.int64).pin_memory()
+    outbuf_r = torch.empty(m + 1, dtype=torch.int64).pin_memory()
     k = max(1, min(args.steps, args.e2e_steps))
     s = torch.cuda.current_stream()
-    flop = None
+    nbytes = lambda h: sum(t.numel() * t.element_size() for t in h[:3])  # noqa: E731
     h2d = d2h = 0
     times = []
     for it in range(k + 1):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
 
-        def up(h, M):
-            return spg.DeviceCSR(M.nrows, M.ncols, h[0].to(dev, non_blocking=True),
+        def up(h):
+            n = h[0].numel() - 1
+            return spg.DeviceCSR(n, h[3], h[0].to(dev, non_blocking=True),
                                  h[1].to(dev, non_blocking=True), h[2].to(dev, non_blocking=True))
-        dA = up(hA, A)
-        dB = dA if same else up(hB, B)
-        hb = sum(t.numel() * t.element_size() for t in hA) + (0 if same else sum(
-            t.numel() * t.element_size() for t in hB))
+        dAl = up(hA)
+        dBl = dAl if hB is hA else up(hB)
+        hb = nbytes(hA) + (0 if hB is hA else nbytes(hB))
         if tri:
-            dG = up(hG, extra["G"])
-            hb += sum(t.numel() * t.element_size() for t in hG)
-            cnt = spg.triangle_count(dA, dB, dG, ctx=ctx)
+            dGl = up(hG)
+            hb += nbytes(hG)
+            cnt = spg.triangle_count_rows(dAl, dBl, dGl, 0, m, sorted=True, ctx=ctx) if m else 0
             outbuf_r[:1].copy_(torch.tensor([cnt]))
             db = 8
         else:
-            C = spg.spgemm(dA, dB, sorted=True, ctx=ctx)
+            C = spg.spgemm(dAl, dBl, sorted=True, ctx=ctx)
             nnz = C.col.numel()
             outbuf_r.copy_(C.row_ptr, non_blocking=True)
             for o in range(0, nnz, chunk // 8):
                 n = min(chunk // 8, nnz - o)
                 outbuf_c[:n].copy_(C.col[o:o + n], non_blocking=True)
                 outbuf_v[:n].copy_(C.val[o:o + n], non_blocking=True)
-            db = (A.nrows + 1) * 8 + nnz * 12
+            db = (m + 1) * 8 + nnz * 12
             del C
         e1.record(s)
         torch.cuda.synchronize()
         if it > 0:  # first iteration is a warm-up
             times.append(e0.elapsed_time(e1))
         h2d, d2h = hb, db
-        del dA, dB
-    flop = ctx.info()["flop_total"] if not tri else None
-    if tri:
-        _, flop = spg.rows_to_parts(spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B), 1, ctx)
-    ms = float(np.mean(times))
-    return {"value": 2.0 * flop / (ms * 1e-3) / 1e9, "unit": "GFLOPS", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": len(times)}
+        del dAl, dBl
+    red = torch.tensor([float(np.mean(times)), float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = red[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = red[1:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        red = torch.cat([mx, sm])
+    ms, h2d, d2h = (float(x) for x in red.tolist())
+    return {"value": 2.0 * flop_total / (ms * 1e-3) / 1e9, "unit": "GFLOPS", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": len(times),
+            "timing": "max over ranks of per-rank device events; bytes summed over ranks"}
 
 
 def main():
