@@ -78,10 +78,11 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
       base += __popc(bal);
     }
   } else {
-    if (nnz <= 128 && T <= 256) {
+    if (nnz <= 128) {
       // <= 128 keys: bitonic sort in registers of packed
-      // (column - min) << 8 | slot, 4 per lane (element e = 4 lane + r); the
-      // values stay in their slots until the store.  Needs a span < 2^24.
+      // (column - min) << logT | slot, 4 per lane (element e = 4 lane + r);
+      // the values stay in their slots until the store.  Needs a span
+      // < 2^(32 - logT).
       unsigned mn = 0xFFFFFFFFu, mx = 0u;
       for (int s0 = 0; s0 < T; s0 += 32) {
         const unsigned k = keys[s0 + lane];
@@ -92,14 +93,14 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
       }
       mn = __reduce_min_sync(kFull, mn);
       mx = __reduce_max_sync(kFull, mx);
-      if (mx - mn < (1u << 24)) {
+      if (mx - mn < (1u << (32 - logT))) {
         uint32_t *pk_s = cnt;  // scratch: packed keys compacted to the front
         int base = 0;
         for (int s0 = 0; s0 < T; s0 += 32) {
           const uint32_t k = keys[s0 + lane];
           const bool occ = k != kEmpty;
           const unsigned bal = __ballot_sync(kFull, occ);
-          if (occ) pk_s[base + __popc(bal & lt_mask)] = ((k - mn) << 8) | (uint32_t)(s0 + lane);
+          if (occ) pk_s[base + __popc(bal & lt_mask)] = ((k - mn) << logT) | (uint32_t)(s0 + lane);
           base += __popc(bal);
         }
         for (int e = base + lane; e < 128; e += 32) pk_s[e] = 0xFFFFFFFFu;
@@ -134,8 +135,8 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
         for (int r = 0; r < 4; ++r) {
           const int e = 4 * lane + r;
           if (e < nnz) {
-            c_col[rp0 + e] = (int32_t)(mn + (pk[r] >> 8));
-            c_val[rp0 + e] = vals[pk[r] & 255u];
+            c_col[rp0 + e] = (int32_t)(mn + (pk[r] >> logT));
+            c_val[rp0 + e] = vals[pk[r] & uint32_t(T - 1)];
           }
         }
         return;
@@ -216,7 +217,7 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
 // __match_any_sync) use the atomic add.  Rounds are separated by __syncwarp.
 // ---------------------------------------------------------------------------
 template <int TMAX, int WARPS, int SORTED>
-__global__ void __launch_bounds__(WARPS * 32, 40 / WARPS) k_num_warp(const int32_t *__restrict__ rows,
+__global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_warp(const int32_t *__restrict__ rows,
                                                          int64_t nrows, DevCSR A, DevCSR B,
                                                          const int64_t *__restrict__ flop,
                                                          const int64_t *__restrict__ c_rp,
