@@ -187,6 +187,30 @@ spg_status spg_mask_sum(spg_ctx *ctx, const spg_csr *C, const spg_csr *G,
 spg_status spg_masked_sum(spg_ctx *ctx, const spg_csr *A, const spg_csr *B, const spg_csr *G,
                           int64_t g_row_begin, double *sum, void *stream);
 
+/* Degree-ascending relabelling for triangle counting (Sec 5.6,
+ * "we reorder rows with increasing number of nonzeros.  The algorithm
+ * then splits the reordered matrix A as A = L + U").
+ * Untimed preprocessing in the paper.
+ *   G     : device CSR, n x n pattern of a symmetric adjacency matrix WITHOUT
+ *           diagonal (values unused, any column order), n and nnz(G) < 2^31.
+ *   perm  : device out int32[n]: perm[r] = old id of new vertex r, the order
+ *           of the keys (deg(v), v) ascending (ties by old id: unique).
+ *   L_rp, L_col, L_val : device out, int64[n+1], int32[nnz(G)/2], f64[nnz(G)/2]
+ *           (L_val may be NULL): L' = strict lower triangle of P G P^T.
+ *   U_rp, U_col, U_val : the same for U' = strict upper triangle.
+ *   G_rp, G_col, G_val : device out, int64[n+1], int32[nnz(G)], f64[nnz(G)]
+ *           (G_val may be NULL): G' = P G P^T (the mask).
+ * All rows of L', U', G' have strictly increasing columns; values are 1.0.
+ * Buffers are caller-allocated; workspace from the ctx allocator.  Errors:
+ * SPG_ERR_INVALID_ARG when nnz(G) is odd, a diagonal entry is present, or the
+ * lower and upper counts differ (necessary conditions of symmetry; a
+ * non-symmetric G with equal counts is not detected); SPG_ERR_OVERFLOW for
+ * n or nnz >= 2^31.  Synchronizes `stream` twice (nnz(G), count check). */
+spg_status spg_degree_relabel(spg_ctx *ctx, const spg_csr *G, int32_t *perm, int64_t *L_rp,
+                              int32_t *L_col, double *L_val, int64_t *U_rp, int32_t *U_col,
+                              double *U_val, int64_t *G_rp, int32_t *G_col, double *G_val,
+                              void *stream);
+
 /* Validation of the CSR invariants (untimed): row_ptr nondecreasing, columns
  * in [0, ncols); with check_sorted != 0 also strictly increasing columns per
  * row (which implies uniqueness).  Returns SPG_OK or SPG_ERR_INDEX_RANGE /

@@ -15,6 +15,8 @@ numpy arrays.  Functions and the PAPER.md passages they follow:
 * ``spgemm``          Fig:code_spgemm with a SPA; sorted
                       output (P:286)
 * ``mask_sum`` / ``triangle_count``  Sec 5.6 + BASELINE config 5
+* ``degree_relabel``  Sec 5.6 P:604 ("we reorder rows with increasing number
+                      of nonzeros ... splits the reordered matrix A as A = L + U")
 
 Pins (tests/test_oracle.py): dense brute force, identity, stencil and K_n
 closed forms, tall-skinny column identity, row-sum identity, L*U symmetry,
@@ -183,3 +185,37 @@ def triangle_count(L, U, G, block_rows: int | None = None, nthreads: int = 0) ->
         total += mask_sum(rp, col, val, G, r0)
     assert total % 2 == 0, "sum(C o G) must be even for symmetric G"
     return total // 2
+
+
+class OCSR:
+    """Minimal CSR record returned by the oracle (row_ptr int64, col int32, val f64)."""
+
+    def __init__(self, nrows, ncols, row_ptr, col, val):
+        self.nrows, self.ncols = int(nrows), int(ncols)
+        self.row_ptr, self.col, self.val = row_ptr, col, val
+
+
+def degree_relabel(G):
+    """Degree-ascending relabelling: new id of vertex v = rank of
+    (deg(v), v) ascending; G' = P G P^T; L' / U' = strict lower / upper
+    triangle of G' (the split "A = L + U" of the reordered matrix).  Rows with
+    ascending columns, values 1.0.  Returns (perm, L', U', G') with perm[r] =
+    old id of new vertex r."""
+    n = G.nrows
+    rp = np.asarray(G.row_ptr, dtype=np.int64)
+    deg = np.diff(rp)
+    perm = np.lexsort((np.arange(n), deg))          # by degree, then by id
+    rank = np.empty(n, dtype=np.int64)
+    rank[perm] = np.arange(n)
+    old_rows = np.repeat(np.arange(n), deg)
+    r2 = rank[old_rows]
+    c2 = rank[np.asarray(G.col[rp[0]:rp[-1]], dtype=np.int64)]
+    order = np.lexsort((c2, r2))                    # row-major, ascending columns
+    r2, c2 = r2[order], c2[order]
+
+    def csr(keep):
+        rr, cc = r2[keep], c2[keep]
+        ptr = np.zeros(n + 1, dtype=np.int64)
+        ptr[1:] = np.cumsum(np.bincount(rr, minlength=n))
+        return OCSR(n, n, ptr, cc.astype(np.int32), np.ones(len(cc)))
+    return (perm.astype(np.int32), csr(c2 < r2), csr(c2 > r2), csr(np.ones(len(r2), bool)))

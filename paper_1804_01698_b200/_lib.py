@@ -22,7 +22,7 @@ EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_co
            "spg_symbolic", "spg_numeric", "spg_get_info", "spg_plan_export",
            "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
-           "spg_debug_counters", "spg_masked_sum")
+           "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel")
 
 
 class spg_csr(ct.Structure):
@@ -77,6 +77,7 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_profile_record.argtypes = [vp, i64, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_float)]
     lib.spg_debug_counters.argtypes = [vp, i64p, vp]
     lib.spg_masked_sum.argtypes = [vp, csrp, csrp, csrp, i64, ct.POINTER(ct.c_double), vp]
+    lib.spg_degree_relabel.argtypes = [vp, csrp] + [vp] * 11
     for name in EXPORTS:
         if name not in ("spg_last_error", "spg_launch_count", "spg_profile_count"):
             getattr(lib, name).restype = ct.c_int
@@ -186,3 +187,10 @@ def spg_masked_sum(ctx: int, A: spg_csr, B: spg_csr, G: spg_csr, g_row_begin: in
            load().spg_masked_sum(ctx, ct.byref(A), ct.byref(B), ct.byref(G), g_row_begin,
                                  ct.byref(out), stream))
     return out.value
+
+
+def spg_degree_relabel(ctx: int, G: spg_csr, perm: int, L: tuple, U: tuple, Gn: tuple,
+                       stream: int) -> None:
+    """L, U, Gn: (row_ptr, col, val) device pointers of the outputs."""
+    _check(ctx, "spg_degree_relabel",
+           load().spg_degree_relabel(ctx, ct.byref(G), perm, *L, *U, *Gn, stream))

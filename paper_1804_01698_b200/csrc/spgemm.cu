@@ -14,6 +14,7 @@
 #include "masked.cuh"
 #include "numeric.cuh"
 #include "plan.cuh"
+#include "relabel.cuh"
 #include "spg_internal.cuh"
 #include "symbolic.cuh"
 
@@ -43,6 +44,7 @@ struct spg_ctx {
   Buf parts, part_row, part_n, toff;  // column-tile parts of long rows (BM tier), B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
+  Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (keys, ranks, unsorted rows, CUB temp)
   bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
   int64_t prune_n = 0;
   spg_csr Ap{};
@@ -323,8 +325,11 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
 spg_status spg_ctx_destroy(spg_ctx *c) {
   if (!c) return SPG_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
-  Buf *bufs[] = {&c->flop,  &c->rows_sym, &c->rows_num, &c->partial, &c->slab,
-                 &c->info,  &c->scratch,  &c->parts,    &c->part_row, &c->part_n, &c->toff};
+  Buf *bufs[] = {&c->flop,      &c->rows_sym,  &c->rows_num,  &c->partial,   &c->slab,
+                 &c->info,      &c->scratch,   &c->parts,     &c->part_row,  &c->part_n,
+                 &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
+                 &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
+                 &c->rl_tmp,    &c->rl_cub};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {
@@ -887,6 +892,99 @@ spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const 
   SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
   *sum = c->host_info->mask_acc;
+  return SPG_OK;
+}
+
+spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64_t *L_rp,
+                              int32_t *L_col, double *L_val, int64_t *U_rp, int32_t *U_col,
+                              double *U_val, int64_t *G_rp, int32_t *G_col, double *G_val,
+                              void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, G, "G", false)) != SPG_OK) return st;
+  if (G->nrows != G->ncols) return fail(c, SPG_ERR_DIM_MISMATCH, "G must be square");
+  if (!perm || !L_rp || !U_rp || !G_rp) return fail(c, SPG_ERR_INVALID_ARG, "NULL output");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  const int64_t n = G->nrows;
+  int64_t nnz = 0;
+  if (n > 0) {
+    int64_t ends[2];
+    SPG_CUDA(c, cudaMemcpyAsync(&ends[0], G->row_ptr, 8, cudaMemcpyDeviceToHost, s));
+    SPG_CUDA(c, cudaMemcpyAsync(&ends[1], G->row_ptr + n, 8, cudaMemcpyDeviceToHost, s));
+    SPG_CUDA(c, cudaStreamSynchronize(s));
+    nnz = ends[1] - ends[0];
+  }
+  if (nnz % 2 != 0) return fail(c, SPG_ERR_INVALID_ARG, "nnz(G) is odd: G is not a symmetric pattern");
+  if (n >= INT32_MAX || nnz >= INT32_MAX)
+    return fail(c, SPG_ERR_OVERFLOW, "degree relabel supports n, nnz(G) < 2^31");
+  if (nnz > 0 && (!L_col || !U_col || !G_col)) return fail(c, SPG_ERR_INVALID_ARG, "NULL output");
+  SPG_CUDA(c, cudaMemsetAsync(L_rp, 0, 8, s));
+  SPG_CUDA(c, cudaMemsetAsync(U_rp, 0, 8, s));
+  SPG_CUDA(c, cudaMemsetAsync(G_rp, 0, 8, s));
+  if (n == 0) return SPG_OK;
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rl_key, size_t(n) * 16, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rl_rank, size_t(n) * 4, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rl_tmp, size_t(std::max<int64_t>(nnz, 1)) * 8, s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  unsigned long long *bad = &info->mask_ctr[0];
+  SPG_CUDA(c, cudaMemsetAsync(bad, 0, 8, s));
+  unsigned long long *key = (unsigned long long *)c->rl_key.p, *skey = key + n;
+  int32_t *rank = (int32_t *)c->rl_rank.p;
+  int32_t *Lt = (int32_t *)c->rl_tmp.p, *Ut = Lt + nnz / 2, *Gt = Lt + nnz;
+  // CUB temporary storage: the max over the calls below
+  int end_bit = 32;
+  while (end_bit < 64 && (1ull << (end_bit - 32)) <= (unsigned long long)n) ++end_bit;  // deg <= n - 1
+  size_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  SPG_CUDA(c, cub::DeviceRadixSort::SortKeys(nullptr, t0, key, skey, (int)n, 0, end_bit, s));
+  SPG_CUDA(c, cub::DeviceScan::InclusiveSum(nullptr, t1, L_rp + 1, L_rp + 1, (int)n, s));
+  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(nullptr, t2, Gt, G_col, (int)nnz, (int)n, G_rp,
+                                                 G_rp + 1, s));
+  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(nullptr, t3, Lt, L_col, (int)(nnz / 2), (int)n,
+                                                 L_rp, L_rp + 1, s));
+  const size_t tb = std::max(std::max(t0, t1), std::max(t2, t3));
+  if ((st = buf_ensure(c, c->rl_cub, tb, s)) != SPG_OK) return st;
+  size_t tbytes = c->rl_cub.bytes;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), int64_t(c->num_sms) * 8);
+  const unsigned wgrid = (unsigned)std::min<int64_t>(ceil_div(n, 8), int64_t(c->num_sms) * 16);
+  DevCSR g = dev(G);
+  k_rl_keys<<<grid, 256, 0, s>>>(g, key);
+  SPG_LAUNCHED(c, "k_rl_keys");
+  SPG_CUDA(c, cub::DeviceRadixSort::SortKeys(c->rl_cub.p, tbytes, key, skey, (int)n, 0, end_bit, s));
+  k_rl_rank<<<grid, 256, 0, s>>>(skey, n, perm, rank);
+  SPG_LAUNCHED(c, "k_rl_rank");
+  k_rl_count<<<wgrid, 256, 0, s>>>(g, perm, rank, L_rp + 1, U_rp + 1, G_rp + 1, bad);
+  SPG_LAUNCHED(c, "k_rl_count");
+  for (int64_t *rp : {L_rp, U_rp, G_rp}) {
+    tbytes = c->rl_cub.bytes;
+    SPG_CUDA(c, cub::DeviceScan::InclusiveSum(c->rl_cub.p, tbytes, rp + 1, rp + 1, (int)n, s));
+  }
+  int64_t tail[3];
+  SPG_CUDA(c, cudaMemcpyAsync(&tail[0], L_rp + n, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaMemcpyAsync(&tail[1], U_rp + n, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaMemcpyAsync(&tail[2], bad, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  if (tail[2] != 0 || tail[0] != nnz / 2 || tail[1] != nnz / 2)
+    return fail(c, SPG_ERR_INVALID_ARG,
+                "G is not a symmetric pattern without diagonal (lower/upper counts differ or a "
+                "diagonal entry is present)");
+  if (nnz == 0) return SPG_OK;
+  k_rl_fill<<<wgrid, 256, 0, s>>>(g, perm, rank, L_rp, U_rp, G_rp, Lt, Ut, Gt);
+  SPG_LAUNCHED(c, "k_rl_fill");
+  tbytes = c->rl_cub.bytes;
+  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->rl_cub.p, tbytes, Gt, G_col, (int)nnz, (int)n,
+                                                 G_rp, G_rp + 1, s));
+  tbytes = c->rl_cub.bytes;
+  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->rl_cub.p, tbytes, Lt, L_col, (int)(nnz / 2),
+                                                 (int)n, L_rp, L_rp + 1, s));
+  tbytes = c->rl_cub.bytes;
+  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->rl_cub.p, tbytes, Ut, U_col, (int)(nnz / 2),
+                                                 (int)n, U_rp, U_rp + 1, s));
+  const unsigned vgrid = (unsigned)std::min<int64_t>(ceil_div(nnz, 256), int64_t(c->num_sms) * 8);
+  if (L_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(L_val, nnz / 2, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
+  if (U_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(U_val, nnz / 2, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
+  if (G_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(G_val, nnz, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
   return SPG_OK;
 }
 

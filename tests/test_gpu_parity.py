@@ -251,6 +251,55 @@ def test_c5_triangles_fused(spg, ctx, scale):
         assert int(np.diff(G.row_ptr).max()) > 256  # both tiers ran
 
 
+def _relabel_vs_oracle(spg, ctx, G):
+    perm, L2, U2, G2 = spg.degree_relabel(spg.DeviceCSR.from_host(G), ctx=ctx)
+    o_perm, oL, oU, oG = oracle.degree_relabel(G)
+    assert np.array_equal(perm.cpu().numpy(), o_perm)  # unique order: (degree, id)
+    for d, o in ((L2, oL), (U2, oU), (G2, oG)):
+        assert np.array_equal(d.row_ptr.cpu().numpy(), o.row_ptr)
+        assert np.array_equal(d.col.cpu().numpy(), o.col)  # sorted rows, bit-exact
+        assert (d.val.cpu().numpy() == 1.0).all()
+    return L2, U2, G2
+
+
+@pytest.mark.parametrize("scale", [10, 14])
+def test_degree_relabel_parity(spg, ctx, scale):
+    """P:604 reordering on the GPU vs the oracle (perm, L', U', G' exact), and
+    the triangle count of the reordered split equals the natural-order count
+    (oracle), fused and with C formed."""
+    L, U, ex = synth.workload("c5_triangle", scale=scale)
+    G = ex["G"]
+    want = oracle.triangle_count(L, U, G)
+    L2, U2, G2 = _relabel_vs_oracle(spg, ctx, G)
+    assert spg.triangle_count_fused(L2, U2, G2, ctx=ctx) == want
+    assert spg.triangle_count(L2, U2, G2, sorted=True, ctx=ctx) == want
+    # the point of the reordering: far fewer products than the natural order
+    _, f_nat = oracle.flop(L, U)
+    _, f_deg = spg.rows_to_parts(L2, U2, 1, ctx)
+    assert f_deg < f_nat
+
+
+def test_degree_relabel_edge_cases(spg, ctx):
+    # star (hub moves last), K_n (identity), a graph with isolated vertices,
+    # an edgeless graph, a single vertex
+    n = 40
+    r = np.r_[np.zeros(n - 1, int), np.arange(1, n)]
+    c = np.r_[np.arange(1, n), np.zeros(n - 1, int)]
+    _relabel_vs_oracle(spg, ctx, synth.from_coo(n, n, r, c))
+    _relabel_vs_oracle(spg, ctx, synth.complete_graph(50))
+    iso = synth.from_coo(10, 10, np.array([2, 7, 7, 9]), np.array([7, 2, 9, 7]))
+    _relabel_vs_oracle(spg, ctx, iso)
+    _relabel_vs_oracle(spg, ctx, synth.from_coo(6, 6, np.array([], int), np.array([], int)))
+    _relabel_vs_oracle(spg, ctx, synth.from_coo(1, 1, np.array([], int), np.array([], int)))
+    # errors: a diagonal entry; a non-symmetric pattern
+    with pytest.raises(Exception):
+        spg.degree_relabel(spg.DeviceCSR.from_host(
+            synth.from_coo(3, 3, np.array([0, 1, 2, 1]), np.array([1, 0, 2, 2]))), ctx=ctx)
+    with pytest.raises(Exception):
+        spg.degree_relabel(spg.DeviceCSR.from_host(
+            synth.from_coo(3, 3, np.array([0, 0]), np.array([1, 2]))), ctx=ctx)
+
+
 def test_triangles_fused_complete_graph(spg, ctx):
     for n in (3, 60, 700):  # 700: G rows of 699 > the warp tier
         G = synth.complete_graph(n)

@@ -250,6 +250,71 @@ def test_triangles_bruteforce(seed):
     assert (np.diag(D) == np.diff(L.row_ptr)).all()
 
 
+def _dense_pattern(M):
+    D = np.zeros((M.nrows, M.ncols), dtype=bool)
+    rows = np.repeat(np.arange(M.nrows), np.diff(M.row_ptr))
+    D[rows, M.col[M.row_ptr[0]:M.row_ptr[-1]]] = True
+    return D
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_degree_relabel_definition(seed):
+    """P:604 reordering: G' = P G P^T (dense indexing), degrees nondecreasing
+    along the new ids with ties by old id, L'/U' the strict triangles, sorted
+    rows; the triangle count is invariant (brute force)."""
+    rng = np.random.default_rng(100 + seed)
+    n = 45
+    adj = np.triu(rng.random((n, n)) < 0.15, 1)
+    adj[0, 1:] |= rng.random(n - 1) < 0.6  # one hub
+    adj = np.triu(adj, 1)
+    adj = adj | adj.T
+    r, c = np.nonzero(adj)
+    G = synth.from_coo(n, n, r, c)
+    perm, L2, U2, G2 = oracle.degree_relabel(G)
+    assert sorted(perm.tolist()) == list(range(n))
+    deg = adj.sum(1)
+    key = [(deg[v], v) for v in perm]
+    assert key == sorted(key)
+    D2 = _dense_pattern(G2)
+    assert (D2 == adj[np.ix_(perm, perm)]).all()
+    assert (_dense_pattern(L2) == np.tril(D2, -1)).all()
+    assert (_dense_pattern(U2) == np.triu(D2, 1)).all()
+    for M in (L2, U2, G2):
+        for i in range(n):
+            row = M.col[M.row_ptr[i]:M.row_ptr[i + 1]]
+            assert (np.diff(row) > 0).all()
+    brute = sum(1 for a in range(n) for b in range(a + 1, n) for c_ in range(b + 1, n)
+                if adj[a, b] and adj[b, c_] and adj[a, c_])
+    assert oracle.triangle_count(L2, U2, G2) == brute
+    # the hub goes last
+    assert perm[-1] == int(np.argmax(deg)) or deg[perm[-1]] == deg.max()
+
+
+@pytest.mark.parametrize("n", [5, 33])
+def test_degree_relabel_star_closed_form(n):
+    """Star K_{1,n-1} with the centre at id 0: natural-order L*U has (n-1)^2
+    products (every leaf row meets the centre's U row); degree order puts the
+    centre last and leaves n-1 products; no triangles either way."""
+    r = np.r_[np.zeros(n - 1, int), np.arange(1, n)]
+    c = np.r_[np.arange(1, n), np.zeros(n - 1, int)]
+    G = synth.from_coo(n, n, r, c)
+    L, U = synth.tril_strict(G), synth.triu_strict(G)
+    assert oracle.flop(L, U)[1] == (n - 1) ** 2
+    perm, L2, U2, G2 = oracle.degree_relabel(G)
+    assert perm[-1] == 0 and list(perm[:-1]) == list(range(1, n))
+    assert oracle.flop(L2, U2)[1] == n - 1
+    assert oracle.triangle_count(L, U, G) == 0 == oracle.triangle_count(L2, U2, G2)
+
+
+def test_degree_relabel_complete_graph_identity():
+    """K_n: all degrees equal, so the order is the identity (ties by id)."""
+    G = synth.complete_graph(9)
+    perm, L2, U2, G2 = oracle.degree_relabel(G)
+    assert list(perm) == list(range(9))
+    L = synth.tril_strict(G)
+    assert (L2.row_ptr == L.row_ptr).all() and (L2.col == L.col).all()
+
+
 def test_tallskinny_columns():
     """C(:, j) = A(:, r_j) exactly when B has one 1.0 per column (config 4)."""
     A = synth.symmetrise_pattern(synth.rmat(8, 8, 5))
