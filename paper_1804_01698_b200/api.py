@@ -209,6 +209,20 @@ def degree_relabel(G: DeviceCSR, ctx: Context | None = None):
     return perm, L, U, Gn
 
 
+def triangle_count_graph(G: DeviceCSR, degree_order: bool = True, fused: bool = True,
+                         ctx: Context | None = None) -> int:
+    """Triangles of the undirected graph with symmetric pattern G (no
+    diagonal): split G = L + U (after the degree-ascending reordering of
+    P:604 when degree_order), then sum(L*U o G)/2 (fused mask, or with C
+    formed in row blocks)."""
+    ctx = ctx or default_context()
+    if degree_order:
+        _, L, U, G = degree_relabel(G, ctx)
+    else:
+        raise ValueError("natural order needs L and U: use triangle_count(L, U, G)")
+    return triangle_count_fused(L, U, G, ctx) if fused else triangle_count(L, U, G, ctx=ctx)
+
+
 def validate(M: DeviceCSR, check_sorted: bool = False, ctx: Context | None = None) -> None:
     ctx = ctx or default_context()
     _lib.spg_validate(ctx.handle, M.c(), check_sorted, _stream())

@@ -37,24 +37,57 @@ __device__ __forceinline__ bool set_contains(const uint32_t *tab, uint32_t c, in
   }
 }
 
+// Row lists of the two tiers: rows i with a nonempty row of the product's
+// left operand (A, or C when formed) and a nonempty G row, split by |G_i|.
+// Only these rows are visited by the sum kernels (most rows of a reordered
+// or sparse graph have no work; a per-row queue pop for every row cost more
+// than the sums).  Warp-aggregated appends; order within a list arbitrary.
+__global__ void k_mask_rows(const int64_t *__restrict__ a_rp, int64_t nrows, DevCSR G,
+                            int64_t g_row_begin, int32_t *__restrict__ list_w,
+                            int32_t *__restrict__ list_b, unsigned long long *n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t b = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; b < nrows;
+       b += nw * 32) {
+    const int64_t r = b + lane;
+    bool ok = r < nrows && a_rp[r + 1] > a_rp[r];
+    const int64_t gn = ok ? G.rp[g_row_begin + r + 1] - G.rp[g_row_begin + r] : 0;
+    const bool isw = ok && gn > 0 && gn <= kMaskWarpKeys, isb = ok && gn > kMaskWarpKeys;
+    const unsigned bw = __ballot_sync(kFull, isw), bb = __ballot_sync(kFull, isb);
+    unsigned long long ow = 0, ob = 0;
+    if (lane == 0) {
+      if (bw) ow = atomicAdd(n + 0, (unsigned long long)__popc(bw));
+      if (bb) ob = atomicAdd(n + 1, (unsigned long long)__popc(bb));
+    }
+    ow = __shfl_sync(kFull, ow, 0);
+    ob = __shfl_sync(kFull, ob, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (isw) list_w[ow + __popc(bw & lt)] = (int32_t)r;
+    if (isb) list_b[ob + __popc(bb & lt)] = (int32_t)r;
+  }
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_mask_sum_warp(DevCSR A, DevCSR B, DevCSR G,
                                                               int64_t g_row_begin,
+                                                              const int32_t *__restrict__ list,
+                                                              const unsigned long long *nlist,
                                                               unsigned long long *row_counter,
                                                               double *sum) {
   __shared__ uint32_t s_tab[WARPS][kMaskWarpT];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_tab[w];
+  const long long nl = (long long)*nlist;
   double acc = 0.0;
   while (true) {
-    long long r = 0;
-    if (lane == 0) r = (long long)atomicAdd(row_counter, 1ull);
-    r = __shfl_sync(kFull, r, 0);
-    if (r >= A.nrows) break;
+    long long q = 0;
+    if (lane == 0) q = (long long)atomicAdd(row_counter, 1ull);
+    q = __shfl_sync(kFull, q, 0);
+    if (q >= nl) break;
+    const int64_t r = list[q];  // (warp-tier row: 0 < |G_i| <= kMaskWarpKeys, A row nonempty)
     const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
     const int64_t as = A.rp[r], ae = A.rp[r + 1];
     const int64_t gn = ge - gs;
-    if (gn == 0 || gn > kMaskWarpKeys || as == ae) continue;  // (block tier takes the long G rows)
     const int logT = log2_ceil64(uint64_t(2 * gn)) < kMinLogT ? kMinLogT : log2_ceil64(uint64_t(2 * gn));
     const int T = 1 << logT;
     for (int s = lane; s < T; s += 32) tab[s] = kEmpty;
@@ -81,6 +114,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_mask_sum_warp(DevCSR A, DevCSR B
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, DevCSR G,
                                                             int64_t g_row_begin,
+                                                            const int32_t *__restrict__ list,
+                                                            const unsigned long long *nlist,
                                                             unsigned long long *row_counter,
                                                             double *sum, int use_bitmap) {
   extern __shared__ uint32_t s_bm[];
@@ -91,18 +126,20 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
   const int nwords = (int)((B.ncols + 31) >> 5);
   if (use_bitmap)
     for (int s = threadIdx.x; s < nwords; s += THREADS) s_bm[s] = 0u;
+  const long long nl = (long long)*nlist;
   double acc = 0.0;
   while (true) {
-    if (threadIdx.x == 0) s_row = (long long)atomicAdd(row_counter, 1ull);
+    // the list is walked from its end: for a degree-ordered graph the
+    // heaviest rows have the largest ids and go first
+    if (threadIdx.x == 0) {
+      const long long q = (long long)atomicAdd(row_counter, 1ull);
+      s_row = q < nl ? (long long)list[nl - 1 - q] : -1;
+    }
     __syncthreads();
     const long long r = s_row;
-    if (r >= A.nrows) break;
+    if (r < 0) break;
     const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
     const int64_t as = A.rp[r], ae = A.rp[r + 1];
-    if (ge - gs <= kMaskWarpKeys || as == ae) {
-      __syncthreads();  // s_row is rewritten next iteration
-      continue;
-    }
     if (use_bitmap)
       for (int64_t q = gs + threadIdx.x; q < ge; q += THREADS) {
         const uint32_t c = (uint32_t)__ldg(G.col + q);
@@ -158,21 +195,24 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevCSR G,
                                                                   int64_t g_row_begin,
+                                                                  const int32_t *__restrict__ list,
+                                                                  const unsigned long long *nlist,
                                                                   unsigned long long *row_counter,
                                                                   double *sum) {
   __shared__ uint32_t s_tab[WARPS][kMaskWarpT];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_tab[w];
+  const long long nl = (long long)*nlist;
   double acc = 0.0;
   while (true) {
-    long long r = 0;
-    if (lane == 0) r = (long long)atomicAdd(row_counter, 1ull);
-    r = __shfl_sync(kFull, r, 0);
-    if (r >= C.nrows) break;
+    long long q = 0;
+    if (lane == 0) q = (long long)atomicAdd(row_counter, 1ull);
+    q = __shfl_sync(kFull, q, 0);
+    if (q >= nl) break;
+    const int64_t r = list[q];  // (warp-tier row: 0 < |G_i| <= kMaskWarpKeys, C row nonempty)
     const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
     const int64_t cs = C.rp[r], ce = C.rp[r + 1];
     const int64_t gn = ge - gs;
-    if (gn == 0 || gn > kMaskWarpKeys || cs == ce) continue;  // (block tier: long G rows)
     const int lg = log2_ceil64(uint64_t(2 * gn));
     const int logT = lg < kMinLogT ? kMinLogT : lg;
     const int T = 1 << logT;
@@ -180,8 +220,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevC
     __syncwarp();
     for (int64_t q = gs + lane; q < ge; q += 32) sym_insert(tab, (uint32_t)__ldg(G.col + q), logT);
     __syncwarp();
-    for (int64_t q = cs + lane; q < ce; q += 32)
-      if (set_contains(tab, (uint32_t)__ldg(C.col + q), logT)) acc += __ldg(C.val + q);
+    // C rows are long (C5: ~18 K entries per row): kU coalesced column loads
+    // in flight before the probes
+    constexpr int kU = 8;
+    for (int64_t q0 = cs + lane; q0 < ce; q0 += 32 * kU) {
+      uint32_t cc[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t q = q0 + 32 * u;
+        cc[u] = q < ce ? (uint32_t)__ldg(C.col + q) : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (cc[u] != kEmpty && set_contains(tab, cc[u], logT)) acc += __ldg(C.val + q0 + 32 * u);
+    }
     __syncwarp();
   }
   acc = warp_sum(acc);
@@ -191,6 +243,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevC
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_csr_mask_sum_block(DevCSR C, DevCSR G,
                                                                 int64_t g_row_begin,
+                                                                const int32_t *__restrict__ list,
+                                                                const unsigned long long *nlist,
                                                                 unsigned long long *row_counter,
                                                                 double *sum, int use_bitmap) {
   extern __shared__ uint32_t s_bm[];
@@ -199,26 +253,37 @@ __global__ void __launch_bounds__(THREADS) k_csr_mask_sum_block(DevCSR C, DevCSR
   const int nwords = (int)((G.ncols + 31) >> 5);
   if (use_bitmap)
     for (int s = threadIdx.x; s < nwords; s += THREADS) s_bm[s] = 0u;
+  const long long nl = (long long)*nlist;
   double acc = 0.0;
   while (true) {
-    if (threadIdx.x == 0) s_row = (long long)atomicAdd(row_counter, 1ull);
+    if (threadIdx.x == 0) {
+      const long long q = (long long)atomicAdd(row_counter, 1ull);
+      s_row = q < nl ? (long long)list[nl - 1 - q] : -1;
+    }
     __syncthreads();
     const long long r = s_row;
-    if (r >= C.nrows) break;
+    if (r < 0) break;
     const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
     const int64_t cs = C.rp[r], ce = C.rp[r + 1];
-    if (ge - gs <= kMaskWarpKeys || cs == ce) {
-      __syncthreads();
-      continue;
-    }
     if (use_bitmap)
       for (int64_t q = gs + threadIdx.x; q < ge; q += THREADS) {
         const uint32_t c = (uint32_t)__ldg(G.col + q);
         atomicOr(s_bm + (c >> 5), 1u << (c & 31u));
       }
     __syncthreads();
-    for (int64_t q = cs + threadIdx.x; q < ce; q += THREADS) {
-      const uint32_t c = (uint32_t)__ldg(C.col + q);
+    constexpr int kU = 4;
+    for (int64_t q0 = cs + threadIdx.x; q0 < ce; q0 += THREADS * kU) {
+      uint32_t cc[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t q = q0 + int64_t(THREADS) * u;
+        cc[u] = q < ce ? (uint32_t)__ldg(C.col + q) : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+      const uint32_t c = cc[u];
+      const int64_t q = q0 + int64_t(THREADS) * u;
+      if (c == kEmpty) continue;
       bool hit;
       if (use_bitmap) {
         hit = (s_bm[c >> 5] >> (c & 31u)) & 1u;
@@ -231,6 +296,7 @@ __global__ void __launch_bounds__(THREADS) k_csr_mask_sum_block(DevCSR C, DevCSR
         hit = lo < ge && (uint32_t)__ldg(G.col + lo) == c;
       }
       if (hit) acc += __ldg(C.val + q);
+      }
     }
     __syncthreads();
     if (use_bitmap)

@@ -54,6 +54,7 @@ struct PlanInfo {
   unsigned long long a_nnz;         // nnz of A (k_flop_nz)
   unsigned long long mask_ctr[2];   // row queues of the fused mask-and-sum kernels
   double mask_acc;                  // their fp64 sum
+  unsigned long long mask_n[2];     // lengths of their row lists (warp tier, block tier)
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)
 };
 

@@ -45,6 +45,7 @@ struct spg_ctx {
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
   Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (keys, ranks, unsorted rows, CUB temp)
+  Buf mask_rows;                     // row lists of the mask-and-sum tiers
   bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
   int64_t prune_n = 0;
   spg_csr Ap{};
@@ -329,7 +330,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
                  &c->info,      &c->scratch,   &c->parts,     &c->part_row,  &c->part_n,
                  &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
                  &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
-                 &c->rl_tmp,    &c->rl_cub};
+                 &c->rl_tmp,    &c->rl_cub,    &c->mask_rows};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {
@@ -833,12 +834,22 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
   SPG_CUDA(c, cudaSetDevice(c->device));
   if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
-  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 3 * 8, s));  // both queues and the fp64 sum
+  // both queues, the fp64 sum and the list lengths
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 5 * 8, s));
   if (C->nrows > 0) {
+    if ((st = buf_ensure(c, c->mask_rows, size_t(C->nrows) * 8, s)) != SPG_OK) return st;
+    int32_t *list_w = (int32_t *)c->mask_rows.p, *list_b = list_w + C->nrows;
+    {
+      ProfScope _ps(c, s, "k_mask_rows");
+      k_mask_rows<<<(unsigned)std::min<int64_t>(ceil_div(C->nrows, 256), c->num_sms * 8), 256, 0,
+                    s>>>(C->row_ptr, C->nrows, dev(G), g_row_begin, list_w, list_b, info->mask_n);
+    }
+    SPG_LAUNCHED(c, "k_mask_rows");
     {
       ProfScope _ps(c, s, "k_csr_mask_sum_warp<8>");
       k_csr_mask_sum_warp<kWarps><<<(unsigned)(c->num_sms * 8), kWarps * 32, 0, s>>>(
-          dev(C), dev(G), g_row_begin, &info->mask_ctr[0], &info->mask_acc);
+          dev(C), dev(G), g_row_begin, list_w, &info->mask_n[0], &info->mask_ctr[0],
+          &info->mask_acc);
     }
     SPG_LAUNCHED(c, "k_csr_mask_sum_warp");
     const int use_bitmap = G->ncols <= kBitmapMaxCols ? 1 : 0;
@@ -846,7 +857,8 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
     {
       ProfScope _ps(c, s, "k_csr_mask_sum_block<1024>");
       k_csr_mask_sum_block<1024><<<(unsigned)c->num_sms, 1024, smem, s>>>(
-          dev(C), dev(G), g_row_begin, &info->mask_ctr[1], &info->mask_acc, use_bitmap);
+          dev(C), dev(G), g_row_begin, list_b, &info->mask_n[1], &info->mask_ctr[1],
+          &info->mask_acc, use_bitmap);
     }
     SPG_LAUNCHED(c, "k_csr_mask_sum_block");
   }
@@ -871,13 +883,21 @@ spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const 
   SPG_CUDA(c, cudaSetDevice(c->device));
   if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
-  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 3 * 8, s));  // both queues and the sum
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 5 * 8, s));  // queues, sum, list lengths
   if (A->nrows > 0 && B->nrows > 0) {
     DevCSR a = dev(A), b = dev(B), g = dev(G);
+    if ((st = buf_ensure(c, c->mask_rows, size_t(A->nrows) * 8, s)) != SPG_OK) return st;
+    int32_t *list_w = (int32_t *)c->mask_rows.p, *list_b = list_w + A->nrows;
+    {
+      ProfScope _ps(c, s, "k_mask_rows");
+      k_mask_rows<<<(unsigned)std::min<int64_t>(ceil_div(A->nrows, 256), c->num_sms * 8), 256, 0,
+                    s>>>(A->row_ptr, A->nrows, g, g_row_begin, list_w, list_b, info->mask_n);
+    }
+    SPG_LAUNCHED(c, "k_mask_rows");
     {
       ProfScope _ps(c, s, "k_mask_sum_warp<8>");
       k_mask_sum_warp<kWarps><<<(unsigned)(c->num_sms * 8), kWarps * 32, 0, s>>>(
-          a, b, g, g_row_begin, &info->mask_ctr[0], &info->mask_acc);
+          a, b, g, g_row_begin, list_w, &info->mask_n[0], &info->mask_ctr[0], &info->mask_acc);
     }
     SPG_LAUNCHED(c, "k_mask_sum_warp");
     const int use_bitmap = B->ncols <= kBitmapMaxCols ? 1 : 0;
@@ -885,7 +905,8 @@ spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const 
     {
       ProfScope _ps(c, s, "k_mask_sum_block<1024>");
       k_mask_sum_block<1024><<<(unsigned)c->num_sms, 1024, smem, s>>>(
-          a, b, g, g_row_begin, &info->mask_ctr[1], &info->mask_acc, use_bitmap);
+          a, b, g, g_row_begin, list_b, &info->mask_n[1], &info->mask_ctr[1], &info->mask_acc,
+          use_bitmap);
     }
     SPG_LAUNCHED(c, "k_mask_sum_block");
   }

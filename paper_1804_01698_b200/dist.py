@@ -113,3 +113,12 @@ def triangle_count_dist(L, U, G, group=None, ctx: Context | None = None,
     if total % 2:
         raise RuntimeError("sum(C o G) is odd: G is not symmetric")
     return total // 2
+
+
+def triangle_count_graph_dist(G, group=None, ctx: Context | None = None, fused: bool = True) -> int:
+    """Triangles of the graph G (replicated on every rank): every rank computes
+    the same degree-ascending relabelling (deterministic), then
+    triangle_count_dist on the reordered split L' + U'."""
+    from .api import degree_relabel
+    _, L, U, G2 = degree_relabel(G, ctx)
+    return triangle_count_dist(L, U, G2, group, ctx, fused=fused)

@@ -53,3 +53,6 @@ def test_triangles_dist_nccl_world1(pg):
     want = oracle.triangle_count(L, U, ex["G"])
     assert sdist.triangle_count_dist(dL, dU, dG) == want
     assert sdist.triangle_count_dist(dL, dU, dG, fused=True) == want
+    assert sdist.triangle_count_graph_dist(dG) == want            # degree order
+    assert sdist.triangle_count_graph_dist(dG, fused=False) == want
+    assert spg.triangle_count_graph(dG) == want
