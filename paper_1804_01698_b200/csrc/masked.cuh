@@ -23,7 +23,8 @@
 namespace spg {
 
 constexpr int kMaskWarpKeys = 256;             // G rows up to this size: warp tier
-constexpr int kMaskWarpT = 2 * kMaskWarpKeys;  // warp hash-set slots (load <= 1/2)
+constexpr int kMaskWarpT = 4 * kMaskWarpKeys;  // warp hash-set slots (load <= 1/4: most
+                                               // probes miss, and a miss walks to an empty slot)
 
 // probe-only lookup in a warp-private smem hash set (no insertion)
 __device__ __forceinline__ bool set_contains(const uint32_t *tab, uint32_t c, int logT) {
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_mask_sum_warp(DevCSR A, DevCSR B
     const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
     const int64_t as = A.rp[r], ae = A.rp[r + 1];
     const int64_t gn = ge - gs;
-    const int logT = log2_ceil64(uint64_t(2 * gn)) < kMinLogT ? kMinLogT : log2_ceil64(uint64_t(2 * gn));
+    const int logT = log2_ceil64(uint64_t(4 * gn)) < kMinLogT ? kMinLogT : log2_ceil64(uint64_t(4 * gn));
     const int T = 1 << logT;
     for (int s = lane; s < T; s += 32) tab[s] = kEmpty;
     __syncwarp();
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevC
     const int64_t gs = G.rp[g_row_begin + r], ge = G.rp[g_row_begin + r + 1];
     const int64_t cs = C.rp[r], ce = C.rp[r + 1];
     const int64_t gn = ge - gs;
-    const int lg = log2_ceil64(uint64_t(2 * gn));
+    const int lg = log2_ceil64(uint64_t(4 * gn));
     const int logT = lg < kMinLogT ? kMinLogT : lg;
     const int T = 1 << logT;
     for (int s = lane; s < T; s += 32) tab[s] = kEmpty;

@@ -173,8 +173,10 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
       }
       continue;
     }
-    if (seq && own_chunks) {
-      // this warp owns the chunk: walk its nonempty entries directly
+    if ((kDepth <= 2 || !kVal) && seq && own_chunks) {
+      // warp tiers and the symbolic walks: the nonempty entries directly
+      // (measured: the pipelined walker below costs the occupancy-bound warp
+      // kernels registers, and the symbolic bitmap tier time)
       unsigned pend = __ballot_sync(kFull, en.len > 0);
       while (pend) {
         const int j = __ffs(pend) - 1;
@@ -192,6 +194,53 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
           }
           f(act, c, v);
         }
+      }
+      continue;
+    }
+    if (seq && own_chunks) {
+      // this warp owns the chunk (some B rows longer than 32): walk its
+      // nonempty entries, a round = 32 consecutive b_kj of one B row, with
+      // the gathers of the next round issued before this one is applied
+      unsigned pend = __ballot_sync(kFull, en.len > 0);
+      if (!pend) continue;
+      int L = 0, t = -32;
+      int64_t jbs = 0;
+      double aj = 0.0;
+      auto next_round = [&]() -> bool {  // warp-uniform
+        t += 32;
+        if (t < L) return true;
+        if (!pend) return false;
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        jbs = shfl_i64(en.bs, j);
+        L = __shfl_sync(kFull, en.len, j);
+        if (kVal) aj = shfl_f64(en.a, j);
+        t = 0;
+        return true;
+      };
+      next_round();
+      bool act = t + lane < L;
+      uint32_t c = act ? (uint32_t)__ldg(B.col + jbs + t + lane) : 0u;
+      double bv = (kVal && act) ? __ldg(B.val + jbs + t + lane) : 0.0;
+      double a = aj;
+      while (true) {
+        const bool more = next_round();
+        bool nact = false;
+        uint32_t nc = 0u;
+        double nbv = 0.0;
+        if (more) {
+          nact = t + lane < L;
+          if (nact) {
+            nc = (uint32_t)__ldg(B.col + jbs + t + lane);
+            if (kVal) nbv = __ldg(B.val + jbs + t + lane);
+          }
+        }
+        f(act, c, a * bv);  // value <- a_ik * b_kj (Fig:code_spgemm l.5)
+        if (!more) break;
+        act = nact;
+        c = nc;
+        bv = nbv;
+        a = aj;
       }
       continue;
     }
