@@ -585,48 +585,23 @@ static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
 
-// Number of lanes whose (nondecreasing across lanes) value wv is <= x: 0..32.
-__device__ __forceinline__ int count_le(int wv, int x) {
-  int pos = 0;
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1) {
-    const int v = __shfl_sync(kFull, wv, pos + s - 1);
-    if (v <= x) pos += s;
-  }
-  const int last = __shfl_sync(kFull, wv, 31);  // (all lanes shuffle)
-  if (pos == 31 && last <= x) pos = 32;
-  return pos;
-}
-
-// Owner entry of product x (x < pre[n]): the last j with pre[j] <= x, searched
-// from entry jb (pre[jb] <= every product of the round) in windows of 32
-// boundaries pre[jb+1 .. jb+32] loaded by the warp at once.  All lanes call.
-__device__ __forceinline__ int part_owner(const int32_t *__restrict__ pre, int n, int jb, int x,
-                                          bool act) {
-  const int lane = lane_id();
-  int own = act ? -1 : 0;
-  while (true) {
-    const int e = jb + 1 + lane;
-    const int wv = e <= n ? pre[e] : INT32_MAX;
-    const int c = count_le(wv, x);
-    if (own < 0 && c < 32) own = jb + c;
-    if (__all_sync(kFull, own >= 0)) break;
-    jb += 32;
-  }
-  return own;
-}
-
-// Rounds [g0, g1) of 32 consecutive products of the staged entries (segment
-// of entry j = [es[j], es[j] + pre[j+1] - pre[j]) of B, multiplier ea[j]);
-// owners and gather addresses of kD rounds first, then the kD gathers, then
-// the kD updates f(active, column, a_ik * b_kj).
+// Rounds [g0, g1) of 32 consecutive products of the staged entries (all
+// NONEMPTY: segment of entry j = [es[j], es[j] + pre[j+1] - pre[j]) of B,
+// multiplier ea[j], pre strictly increasing, pre[n] = P).  The owner entry of
+// product x is tracked per warp: `cur` owns the round's first product; the
+// <= 32 entries that start inside the round are found from a window of the
+// next 32 entry starts (one smem load per lane), their start positions
+// OR-ed into a 32-bit mask, and lane t's owner = cur + (starts at or before
+// t).  Owners and gather addresses of kD rounds first, then the kD gathers,
+// then the kD updates f(active, column, a_ik * b_kj).
 template <int kD = 4, typename F>
 __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t *es,
                                                  const double *ea, const int32_t *pre, int n,
                                                  int P, int g0, int g1, F &&f) {
   if (g0 >= g1) return;
   const int lane = lane_id();
-  int jb;
+  const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // lanes <= this one
+  int cur;
   {
     const int x = g0 * 32;
     int lo = 0, hi = n;  // last j with pre[j] <= x
@@ -634,7 +609,7 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t 
       const int m = (lo + hi) >> 1;
       if (pre[m] <= x) lo = m; else hi = m;
     }
-    jb = lo;
+    cur = lo;
   }
   for (int g = g0; g < g1; g += kD) {
     uint32_t c[kD];
@@ -643,10 +618,13 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t 
     int64_t q[kD];
 #pragma unroll
     for (int d = 0; d < kD; ++d) {
-      const int x = (g + d) * 32 + lane;
+      const int x0 = (g + d) * 32, x = x0 + lane;
       act[d] = (g + d < g1) && x < P;
-      const int j = part_owner(pre, n, jb, x, act[d]);
-      jb = __shfl_sync(kFull, act[d] ? j : jb, 31);
+      const int e = cur + 1 + lane;
+      const int st = e < n ? pre[e] : INT32_MAX;  // start of entry cur + 1 + lane (> x0)
+      const unsigned pos = __reduce_or_sync(kFull, st < x0 + 32 ? (1u << (st - x0)) : 0u);
+      const int j = cur + __popc(pos & le);
+      cur += __popc(__ballot_sync(kFull, st <= x0 + 32));  // owner of the next round's first product
       q[d] = act[d] ? es[j] + (x - pre[j]) : 0;
       a[d] = act[d] ? ea[j] : 0.0;
     }
@@ -741,31 +719,49 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       const int n = min(kTEnt, na - cb);
       __syncthreads();  // table init / the previous chunk's rounds are done
       const long long ca = instr ? clock64() : 0;
-      // stage: thread owns entries [t*per, t*per + per), per <= 2
+      // stage: thread owns entries [t*per, t*per + per), per <= 2; the
+      // entries with a nonempty segment in the part's tiles are compacted
+      // (the round owner search needs strictly increasing starts)
+      constexpr int kPer = (kTEnt + THREADS - 1) / THREADS;
       const int per = (n + THREADS - 1) / THREADS;
       const int jlo = min(n, (int)threadIdx.x * per), jhi = min(n, jlo + per);
-      int mine = 0;
-      for (int j = jlo; j < jhi; ++j) {
-        const int k = __ldg(A.col + as + cb + j);
-        const int32_t *tk = toff + int64_t(k) * (ntiles + 1);
-        const int s0 = __ldg(tk + t0), e0 = __ldg(tk + t1);
-        es[j] = s0;
-        ea[j] = __ldg(A.val + as + cb + j);
-        epre[j] = e0 - s0;
-        mine += e0 - s0;
+      int mine = 0, mine_n = 0;
+      int Ls[kPer];
+      int s0s[kPer];
+      double avs[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int j = jlo + u;
+        Ls[u] = 0;
+        if (j < jhi) {
+          const int k = __ldg(A.col + as + cb + j);
+          const int32_t *tk = toff + int64_t(k) * (ntiles + 1);
+          const int s0 = __ldg(tk + t0), e0 = __ldg(tk + t1);
+          s0s[u] = s0;
+          Ls[u] = e0 - s0;
+          avs[u] = __ldg(A.val + as + cb + j);
+          mine += e0 - s0;
+          mine_n += e0 > s0;
+        }
       }
-      int Pn;
-      int ex = block_excl_scan_int(mine, s_warp, &Pn);  // (contains barriers)
-      for (int j = jlo; j < jhi; ++j) {
-        const int L = epre[j];
-        epre[j] = ex;
-        ex += L;
+      int Pn, nn;
+      int ex = block_excl_scan_int(mine, s_warp, &Pn);     // (contains barriers)
+      int exn = block_excl_scan_int(mine_n, s_warp, &nn);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        if (Ls[u] > 0) {
+          es[exn] = s0s[u];
+          ea[exn] = avs[u];
+          epre[exn] = ex;
+          ++exn;
+          ex += Ls[u];
+        }
       }
-      if (threadIdx.x == 0) epre[n] = Pn;
+      if (threadIdx.x == 0) epre[nn] = Pn;
       __syncthreads();
       const long long cbk = instr ? clock64() : 0;
       const int R = (Pn + 31) >> 5;
-      for_tpart_rounds<2>(B, es, ea, epre, n, Pn, (int)((int64_t)R * w / NW),
+      for_tpart_rounds<2>(B, es, ea, epre, nn, Pn, (int)((int64_t)R * w / NW),
                           (int)((int64_t)R * (w + 1) / NW), acc);
       if (instr) {
         c_stage += cbk - ca;
