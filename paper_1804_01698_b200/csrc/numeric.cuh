@@ -584,6 +584,7 @@ static_assert(size_t(kTEnt) * 20 + 4 <= kTEntBytes, "entry stage");
 static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
+static_assert(kTEnt <= 32 * 32, "for_tpart_rounds: 32-ary owner search");
 
 // Rounds [g0, g1) of 32 consecutive products of the staged entries (all
 // NONEMPTY: segment of entry j = [es[j], es[j] + pre[j+1] - pre[j]) of B,
@@ -603,13 +604,15 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t 
   const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // lanes <= this one
   int cur;
   {
+    // last j < n with pre[j] <= x (pre[0] = 0): a 32-ary search, two
+    // ballots over strided then consecutive starts (n <= kTEnt = 32 * 32)
     const int x = g0 * 32;
-    int lo = 0, hi = n;  // last j with pre[j] <= x
-    while (hi - lo > 1) {
-      const int m = (lo + hi) >> 1;
-      if (pre[m] <= x) lo = m; else hi = m;
-    }
-    cur = lo;
+    const int c1 = lane * 32;
+    const unsigned b1 = __ballot_sync(kFull, c1 < n && pre[c1] <= x);
+    const int blk = 31 - __clz(b1);
+    const int c2 = blk * 32 + lane;
+    const unsigned b2 = __ballot_sync(kFull, c2 < n && pre[c2] <= x);
+    cur = blk * 32 + 31 - __clz(b2);
   }
   for (int g = g0; g < g1; g += kD) {
     uint32_t c[kD];
