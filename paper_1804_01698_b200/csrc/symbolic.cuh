@@ -403,47 +403,6 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
   }
 }
 
-// Block-wide walk of bitmap words bm[0, nwords) in order with the exclusive
-// prefix popcount of each word: f(q, word, cum) for every word q.  Warp w owns
-// a contiguous range of 32-word chunks; lane l reads word chunk + l, so every
-// shared load is conflict-free.  Two passes: warp totals, then the walk.
-// Contains barriers (all threads must call it).
-template <typename F>
-__device__ __forceinline__ void bitmap_prefix_walk(const uint32_t *bm, int nwords, int *s_warp,
-                                                   F &&f) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
-  const int nchunks = (nwords + 31) >> 5;
-  const int cper = (nchunks + NW - 1) / NW;
-  const int q0 = w * cper * 32, q1 = min(nwords, (w + 1) * cper * 32);
-  int mine = 0;
-  for (int q = q0 + lane; q < q1; q += 32) mine += __popc(bm[q]);
-  mine = warp_sum(mine);
-  if (lane == 0) s_warp[w] = mine;
-  __syncthreads();
-  if (w == 0) {
-    const int v = lane < NW ? s_warp[lane] : 0;
-    const int vi = warp_incl_scan(v);
-    if (lane < NW) s_warp[lane] = vi - v;
-  }
-  __syncthreads();
-  int carry = s_warp[w];
-  for (int c0 = q0; c0 < q1; c0 += 32) {
-    const int q = c0 + lane;
-    const uint32_t word = q < q1 ? bm[q] : 0u;
-    const int pc = __popc(word);
-    const int incl = warp_incl_scan(pc);
-    if (q < q1) f(q, word, carry + incl - pc);
-    carry += __shfl_sync(kFull, incl, 31);
-  }
-  __syncthreads();
-}
-
-// column of the n-th (0-based) set bit of word q
-__device__ __forceinline__ int nth_bit_col(int q, uint32_t word, int n) {
-  for (int t = 0; t < n; ++t) word &= word - 1;  // drop the n lower set bits
-  return q * 32 + __ffs(word) - 1;
-}
-
 // ---------------------------------------------------------------------------
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
@@ -463,8 +422,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         int32_t *__restrict__ part_n) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
-  __shared__ int s_warp[THREADS / 32];
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
+  __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
   __shared__ int s_cut[kMaxTiles];       // first tile of each part
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -472,10 +431,10 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   const int ntiles = (int)((B.ncols + kTileCols - 1) >> kTileLog);
   uint32_t *bm = s_dyn_u32;
   const bool want_parts = parts != nullptr && info->b_unsorted == 0;
+  for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;  // (the count pass re-clears)
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int i = rows[r];
-    for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;
-    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
+    if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     // set the bit of every product's column (the old value is not used: no
@@ -486,20 +445,38 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
     else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
     __syncthreads();
-    int cnt = 0;
-    for (int q = threadIdx.x; q < nwords; q += THREADS) cnt += __popc(bm[q]);
-    cnt = warp_sum(cnt);
-    if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
+    // keys per column tile (a warp per tile), clearing the words for the next
+    // row on the way; then the exclusive scan over the tiles = keys before
+    // each tile, and the row's count
+    for (int t = w; t < ntiles; t += NW) {
+      const int q0 = t << (kTileLog - 5), q1 = min(nwords, q0 + kTileCols / 32);
+      int c = 0;
+      for (int q = q0 + lane; q < q1; q += 32) {
+        c += __popc(bm[q]);
+        bm[q] = 0u;
+      }
+      c = (int)__reduce_add_sync(kFull, (unsigned)c);
+      if (lane == 0) s_tcnt[t] = c;
+    }
+    __syncthreads();
+    if (w == 0) {
+      int carry = 0;
+      for (int t0 = 0; t0 < ntiles; t0 += 32) {
+        const int v = t0 + lane < ntiles ? s_tcnt[t0 + lane] : 0;
+        const int incl = warp_incl_scan(v);
+        if (t0 + lane < ntiles) s_tile[t0 + lane] = carry + incl - v;
+        carry += __shfl_sync(kFull, incl, 31);
+      }
+      if (lane == 0) {
+        s_tile[ntiles] = carry;
+        s_cnt = carry;
+      }
+    }
     __syncthreads();
     const int nnz = s_cnt;
     if (threadIdx.x == 0) row_nnz[i] = nnz;
     if (want_parts && nnz > kPartMinKeys) {
-      // keys before each column tile (from the prefix popcounts of the bitmap)
-      bitmap_prefix_walk(bm, nwords, s_warp, [&](int q, uint32_t, int cum) {
-        if ((q & (kTileCols / 32 - 1)) == 0) s_tile[q >> (kTileLog - 5)] = cum;
-      });
       if (threadIdx.x == 0) {
-        s_tile[ntiles] = nnz;
         // parts: greedy runs of consecutive tiles holding <= kTPartKeys keys;
         // a tile holding more stands alone (dense window in the numeric phase)
         int np = 0, start = 0, acc = 0;
