@@ -84,7 +84,9 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
                                                           unsigned long long *__restrict__ flop,
                                                           PlanInfo *info,
                                                           unsigned long long *__restrict__ useful_row,
-                                                          const int64_t *__restrict__ trow, int64_t tcap) {
+                                                          const int64_t *__restrict__ trow, int64_t tcap,
+                                                          uint32_t *__restrict__ useful_bits,
+                                                          int64_t bits_cap) {
   __shared__ long long s_r[2];
   __shared__ unsigned long long s_maxb, s_useful;
   const int lane = threadIdx.x & 31;
@@ -104,26 +106,36 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
     int64_t r = j0 < jend ? row_of(A.rp, rlo, rhi, j0) : rhi;
     int64_t rend = __ldg(A.rp + r + 1);
     unsigned long long acc = 0, acc_u = 0;
+    // useful-entry bitmask for the pruning pass: word (tile, warp, u), bit =
+    // lane <-> entry tile + (warp * 32 + lane) * kFlopRun + u
+    const int64_t wbase = (t0 / kFlopTile) * (kFlopThreads / 32) * kFlopRun +
+                          int64_t(threadIdx.x >> 5) * kFlopRun;
+    const bool want_bits = use_bm && useful_bits != nullptr && wbase + kFlopRun <= bits_cap;
     // walk the run; flush acc at each row boundary (all but the last segment)
     for (int u = 0; u < kFlopRun; ++u) {
       const int64_t j = j0 + u;
-      if (j >= jend) break;
-      if (j >= rend) {
-        if (acc) atomicAdd(flop + r, acc);
-        if (use_bm && useful_row && acc_u) atomicAdd(useful_row + r, acc_u);
-        acc = 0;
-        acc_u = 0;
-        r = advance_row(A.rp, r + 1, rhi, j);
-        rend = __ldg(A.rp + r + 1);
-      }
-      const int k = __ldg(A.col + j);
       unsigned long long len = 0;
-      if (!use_bm || ((__ldg(b_nonempty + (k >> 5)) >> (k & 31)) & 1u))
-        len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
-      acc += len;
-      acc_u += len > 0;
-      useful += len > 0;
-      maxb = len > maxb ? len : maxb;
+      if (j < jend) {
+        if (j >= rend) {
+          if (acc) atomicAdd(flop + r, acc);
+          if (use_bm && useful_row && acc_u) atomicAdd(useful_row + r, acc_u);
+          acc = 0;
+          acc_u = 0;
+          r = advance_row(A.rp, r + 1, rhi, j);
+          rend = __ldg(A.rp + r + 1);
+        }
+        const int k = __ldg(A.col + j);
+        if (!use_bm || ((__ldg(b_nonempty + (k >> 5)) >> (k & 31)) & 1u))
+          len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
+        acc += len;
+        acc_u += len > 0;
+        useful += len > 0;
+        maxb = len > maxb ? len : maxb;
+      }
+      if (want_bits) {  // (warp-uniform)
+        const unsigned bal = __ballot_sync(kFull, len > 0);
+        if (lane == 0) useful_bits[wbase + u] = bal;
+      }
     }
 
     // last segment: lanes holding the same row combine before the atomic
@@ -216,6 +228,42 @@ __global__ void __launch_bounds__(kFlopThreads) k_prune_scatter(DevCSR A, const 
       }
       const int k = __ldg(A.col + j);
       if (!((__ldg(bnz + (k >> 5)) >> (k & 31)) & 1u)) continue;
+      const int64_t pos = rp2[r] + (int64_t)atomicAdd(cursor + r, 1ull);
+      col2[pos] = k;
+      idx2[pos] = j;
+    }
+  }
+}
+
+// The same scatter from the useful-entry bitmask of k_flop_nz: only the
+// useful a_ik are visited (their row by a search over the tile's row range).
+__global__ void __launch_bounds__(256) k_prune_scatter_bits(DevCSR A, const uint32_t *__restrict__ bits,
+                                                            int64_t nwords,
+                                                            unsigned long long *__restrict__ cursor,
+                                                            const int64_t *__restrict__ rp2,
+                                                            int32_t *__restrict__ col2,
+                                                            int64_t *__restrict__ idx2,
+                                                            const int64_t *__restrict__ trow,
+                                                            int64_t tcap) {
+  const int64_t base = A.rp[0];
+  constexpr int kWordsPerTile = (kFlopThreads / 32) * kFlopRun;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t word = bits[q];
+    if (!word) continue;
+    const int64_t t = q / kWordsPerTile;
+    const int wi = (int)((q % kWordsPerTile) / kFlopRun), u = (int)(q % kFlopRun);
+    int64_t rlo = 0, rhi = A.nrows - 1;
+    if (trow && t + 1 <= tcap) {
+      rlo = trow[t];
+      rhi = trow[t + 1];
+    }
+    while (word) {
+      const int lane = __ffs(word) - 1;
+      word &= word - 1;
+      const int64_t j = base + t * kFlopTile + int64_t(wi * 32 + lane) * kFlopRun + u;
+      const int64_t r = row_of(A.rp, rlo, rhi, j);
+      const int k = __ldg(A.col + j);
       const int64_t pos = rp2[r] + (int64_t)atomicAdd(cursor + r, 1ull);
       col2[pos] = k;
       idx2[pos] = j;

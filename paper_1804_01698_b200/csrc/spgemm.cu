@@ -46,6 +46,7 @@ struct spg_ctx {
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
   Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (keys, ranks, unsorted rows, CUB temp)
   Buf mask_rows;                     // row lists of the mask-and-sum tiers
+  Buf useful_bits;                   // useful-entry bitmask of k_flop_nz (pruning), grow-only
   bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
   int64_t prune_n = 0;
   spg_csr Ap{};
@@ -207,9 +208,12 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
   SPG_LAUNCHED(c, "k_tile_rows");
   {
     ProfScope _ps(c, s, "k_flop_nz");
+    // the useful-entry bitmask is written when a previous call sized it (its
+    // capacity covers this A: checked again before the pruning scatter uses it)
+    uint32_t *bits = useful_row && c->useful_bits.p ? (uint32_t *)c->useful_bits.p : nullptr;
     k_flop_nz<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
         a, B->row_ptr, B->nrows, bnz, (unsigned long long *)flop, info, useful_row,
-        (const int64_t *)c->trow.p, m);
+        (const int64_t *)c->trow.p, m, bits, bits ? int64_t(c->useful_bits.bytes / 4) : 0);
   }
   SPG_LAUNCHED(c, "k_flop_nz");
   {
@@ -330,7 +334,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
                  &c->info,      &c->scratch,   &c->parts,     &c->part_row,  &c->part_n,
                  &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
                  &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
-                 &c->rl_tmp,    &c->rl_cub,    &c->mask_rows};
+                 &c->rl_tmp,    &c->rl_cub,    &c->mask_rows, &c->useful_bits};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {
@@ -470,13 +474,27 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       SPG_CUDA(c, cudaMemcpyAsync(rp2 + 1, cnt, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
       if ((st = launch_scan(c, rp2 + 1, m, s)) != SPG_OK) return st;
       SPG_CUDA(c, cudaMemsetAsync(cnt, 0, size_t(m) * 8, s));
-      {
-        ProfScope _ps(c, s, "k_prune_scatter");
-        k_prune_scatter<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
-            a, bnz, (unsigned long long *)cnt, rp2, (int32_t *)c->prune_col.p,
-            (int64_t *)c->prune_idx.p, (const int64_t *)c->trow.p, m);
+      const int64_t nwords = ceil_div((int64_t)h.a_nnz, kFlopTile) * (kFlopThreads / 32) * kFlopRun;
+      if (c->useful_bits.p && int64_t(c->useful_bits.bytes / 4) >= nwords) {
+        // k_flop_nz wrote the useful-entry bitmask of this A: visit only those
+        ProfScope _ps(c, s, "k_prune_scatter_bits");
+        k_prune_scatter_bits<<<(unsigned)std::min<int64_t>(ceil_div(nwords, 256), c->num_sms * 8),
+                               256, 0, s>>>(a, (const uint32_t *)c->useful_bits.p, nwords,
+                                            (unsigned long long *)cnt, rp2,
+                                            (int32_t *)c->prune_col.p, (int64_t *)c->prune_idx.p,
+                                            (const int64_t *)c->trow.p, m);
+        SPG_LAUNCHED(c, "k_prune_scatter_bits");
+      } else {
+        {
+          ProfScope _ps(c, s, "k_prune_scatter");
+          k_prune_scatter<<<(unsigned)(c->num_sms * 8), kFlopThreads, 0, s>>>(
+              a, bnz, (unsigned long long *)cnt, rp2, (int32_t *)c->prune_col.p,
+              (int64_t *)c->prune_idx.p, (const int64_t *)c->trow.p, m);
+        }
+        SPG_LAUNCHED(c, "k_prune_scatter");
+        // size the bitmask for the next multiply (grow-only workspace)
+        if ((st = buf_ensure(c, c->useful_bits, size_t(nwords) * 4, s)) != SPG_OK) return st;
       }
-      SPG_LAUNCHED(c, "k_prune_scatter");
       c->prune_n = nu;
       c->Ap = spg_csr{m, A->ncols, rp2, (const int32_t *)c->prune_col.p,
                       (const double *)c->prune_val.p};
