@@ -33,7 +33,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "spgemm.cu")]
+    extra = os.environ.get("SPG_NVCC_EXTRA", "").split()  # (A/B builds only)
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", os.path.join(CSRC, "spgemm.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
