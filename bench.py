@@ -34,6 +34,9 @@ L2_FLUSH_BYTES = 256 << 20
 FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback
 
 
+METRIC = "SpGEMM GFLOPS (2*flop/s), sorted C (unsorted in variants)"
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -244,7 +247,7 @@ def run_reference(args):
     ms = 1e3 * float(np.mean(times))
     val = 2 * f / (ms * 1e-3) / 1e9
     sample = f"rows [0, {r_end}) of {A.nrows}: {f} of {tot} flop per step"
-    out = {"impl": "reference", "metric": "SpGEMM GFLOPS (2*flop/s), sorted C", "value": val,
+    out = {"impl": "reference", "metric": METRIC, "value": val,
            "unit": "GFLOPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -470,7 +473,7 @@ def run_ours(args):
             mb = (8 * (A.nrows + 1) + 12 * A.nnz + 8 * (B.nrows + 1) + 12 * flop_total
                   + 8 * (A.nrows + 1) + 12 * nnzC)
         out = {
-            "metric": "SpGEMM GFLOPS (2*flop/s), sorted C (unsorted in variants)",
+            "metric": METRIC,
             "value": gflops(ms_sorted), "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_sorted, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
