@@ -942,7 +942,8 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
   spg_status st;
   if ((st = check_csr(c, G, "G", false)) != SPG_OK) return st;
   if (G->nrows != G->ncols) return fail(c, SPG_ERR_DIM_MISMATCH, "G must be square");
-  if (!perm || !L_rp || !U_rp || !G_rp) return fail(c, SPG_ERR_INVALID_ARG, "NULL output");
+  if ((G->nrows > 0 && !perm) || !L_rp || !U_rp || !G_rp)
+    return fail(c, SPG_ERR_INVALID_ARG, "NULL output");
   cudaStream_t s = (cudaStream_t)stream;
   SPG_CUDA(c, cudaSetDevice(c->device));
   const int64_t n = G->nrows;

@@ -291,6 +291,7 @@ def test_degree_relabel_edge_cases(spg, ctx):
     _relabel_vs_oracle(spg, ctx, iso)
     _relabel_vs_oracle(spg, ctx, synth.from_coo(6, 6, np.array([], int), np.array([], int)))
     _relabel_vs_oracle(spg, ctx, synth.from_coo(1, 1, np.array([], int), np.array([], int)))
+    _relabel_vs_oracle(spg, ctx, synth.from_coo(0, 0, np.array([], int), np.array([], int)))
     # errors: a diagonal entry; a non-symmetric pattern
     with pytest.raises(Exception):
         spg.degree_relabel(spg.DeviceCSR.from_host(
