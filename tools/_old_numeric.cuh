@@ -696,10 +696,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   int64_t *es = reinterpret_cast<int64_t *>(eb);
   double *ea = reinterpret_cast<double *>(eb + size_t(kTEnt) * 8);
   int32_t *epre = reinterpret_cast<int32_t *>(eb + size_t(kTEnt) * 16);
-  if (threadIdx.x == 0) s_q = (long long)atomicAdd(counter, 1ull);
-  __syncthreads();
   while (true) {
-    const int64_t q = s_q;  // (the next part is fetched before the part's last barrier)
+    if (threadIdx.x == 0) s_q = (long long)atomicAdd(counter, 1ull);
+    __syncthreads();
+    const int64_t q = s_q;
     if (q >= nparts) break;
     const int i = part_row[q];
     const int2 P = parts[q];
@@ -886,7 +886,6 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
                              c_val, s_red);
       }
     }
-    if (threadIdx.x == 0) s_q = (long long)atomicAdd(counter, 1ull);  // every thread has read q
     __syncthreads();
     if (instr) {
       const long long cz = clock64();
