@@ -211,6 +211,22 @@ spg_status spg_degree_relabel(spg_ctx *ctx, const spg_csr *G, int32_t *perm, int
                               double *U_val, int64_t *G_rp, int32_t *G_col, double *G_val,
                               void *stream);
 
+/* Collision factor c of Eq:hash_est ("the average number
+ * of probes") of the warp-tier numeric tables, for
+ * MEASUREMENT (not on the product path).  For every row i of A with
+ * 0 < 2 nnz(c_i) <= 1024, the row's products are inserted (keys only, in the
+ * numeric phase's order) into a table of T = lowest 2^n >= 2 nnz(c_i) slots
+ * three times: mode 0 linear probing on the high bits of col * H (the build,
+ * reading R5), mode 1 linear probing on the low bits (the literal remainder),
+ * mode 2 4-slot chunks (HashVector-style; a probe = one chunk).
+ *   A, B      : device CSR (values unused); C_row_ptr: device int64[A.nrows+1]
+ *               from spg_symbolic on the same A, B.
+ *   out       : HOST int64[9]: out[3m] = probes, out[3m+1] = products,
+ *               out[3m+2] = keys inserted (= sum of nnz(c_i) over those rows).
+ * Synchronizes `stream`. */
+spg_status spg_probe_stats(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
+                           const int64_t *C_row_ptr, int64_t *out, void *stream);
+
 /* Validation of the CSR invariants (untimed): row_ptr nondecreasing, columns
  * in [0, ncols); with check_sorted != 0 also strictly increasing columns per
  * row (which implies uniqueness).  Returns SPG_OK or SPG_ERR_INDEX_RANGE /

@@ -22,7 +22,8 @@ EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_co
            "spg_symbolic", "spg_numeric", "spg_get_info", "spg_plan_export",
            "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
-           "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel")
+           "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel",
+           "spg_probe_stats")
 
 
 class spg_csr(ct.Structure):
@@ -78,6 +79,7 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_debug_counters.argtypes = [vp, i64p, vp]
     lib.spg_masked_sum.argtypes = [vp, csrp, csrp, csrp, i64, ct.POINTER(ct.c_double), vp]
     lib.spg_degree_relabel.argtypes = [vp, csrp] + [vp] * 11
+    lib.spg_probe_stats.argtypes = [vp, csrp, csrp, vp, i64p, vp]
     for name in EXPORTS:
         if name not in ("spg_last_error", "spg_launch_count", "spg_profile_count"):
             getattr(lib, name).restype = ct.c_int
@@ -194,3 +196,10 @@ def spg_degree_relabel(ctx: int, G: spg_csr, perm: int, L: tuple, U: tuple, Gn: 
     """L, U, Gn: (row_ptr, col, val) device pointers of the outputs."""
     _check(ctx, "spg_degree_relabel",
            load().spg_degree_relabel(ctx, ct.byref(G), perm, *L, *U, *Gn, stream))
+
+
+def spg_probe_stats(ctx: int, A: spg_csr, B: spg_csr, c_row_ptr: int, stream: int) -> list[int]:
+    out = (ct.c_int64 * 9)()
+    _check(ctx, "spg_probe_stats",
+           load().spg_probe_stats(ctx, ct.byref(A), ct.byref(B), c_row_ptr, out, stream))
+    return list(out)

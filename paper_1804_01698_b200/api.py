@@ -223,6 +223,19 @@ def triangle_count_graph(G: DeviceCSR, degree_order: bool = True, fused: bool = 
     return triangle_count_fused(L, U, G, ctx) if fused else triangle_count(L, U, G, ctx=ctx)
 
 
+def probe_stats(A: DeviceCSR, B: DeviceCSR, ctx: Context | None = None) -> dict:
+    """Measured collision factor c (Eq:hash_est P:362) of the warp-tier numeric
+    tables: {mode: (probes, products, keys, c = probes / products)} for
+    linear probing on high / low hash bits and 4-slot chunks (SURVEY §8(f)
+    row 2).  Runs the symbolic phase first (for nnz(c_i))."""
+    ctx = ctx or default_context()
+    rp, _, _ = spg_symbolic(A, B, ctx)
+    o = _lib.spg_probe_stats(ctx.handle, A.c(), B.c(), rp.data_ptr(), _stream())
+    names = ("linear_high_bits", "linear_low_bits", "chunk4_high_bits")
+    return {n: (o[3 * m], o[3 * m + 1], o[3 * m + 2], o[3 * m] / max(o[3 * m + 1], 1))
+            for m, n in enumerate(names)}
+
+
 def validate(M: DeviceCSR, check_sorted: bool = False, ctx: Context | None = None) -> None:
     ctx = ctx or default_context()
     _lib.spg_validate(ctx.handle, M.c(), check_sorted, _stream())

@@ -14,6 +14,7 @@
 #include "masked.cuh"
 #include "numeric.cuh"
 #include "plan.cuh"
+#include "probestats.cuh"
 #include "relabel.cuh"
 #include "spg_internal.cuh"
 #include "symbolic.cuh"
@@ -1025,6 +1026,29 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
   if (L_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(L_val, nnz / 2, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
   if (U_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(U_val, nnz / 2, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
   if (G_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(G_val, nnz, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
+  return SPG_OK;
+}
+
+spg_status spg_probe_stats(spg_ctx *c, const spg_csr *A, const spg_csr *B,
+                           const int64_t *C_row_ptr, int64_t *out, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", false)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", false)) != SPG_OK) return st;
+  if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
+  if (!out || (A->nrows > 0 && !C_row_ptr)) return fail(c, SPG_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  if ((st = buf_ensure(c, c->scratch, 9 * 8, s)) != SPG_OK) return st;
+  unsigned long long *d = (unsigned long long *)c->scratch.p;
+  SPG_CUDA(c, cudaMemsetAsync(d, 0, 9 * 8, s));
+  if (A->nrows > 0) {
+    k_probe_stats<kWarps><<<(unsigned)std::min<int64_t>(ceil_div(A->nrows, kWarps), c->num_sms * 16),
+                            kWarps * 32, 0, s>>>(dev(A), dev(B), C_row_ptr, d);
+    SPG_LAUNCHED(c, "k_probe_stats");
+  }
+  SPG_CUDA(c, cudaMemcpyAsync(out, d, 9 * 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
   return SPG_OK;
 }
 

@@ -412,3 +412,27 @@ def test_c3_full_size_sampled(spg, ctx):
         np.testing.assert_allclose(rs.cpu().numpy(), ref, rtol=1e-11, atol=1e-300)
         del C, rs
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("which", ["c2", "c3"])
+def test_probe_stats(spg, ctx, which):
+    """Collision-factor measurement (Eq:hash_est P:362):
+    every mode inserts exactly the distinct keys of the measured rows (oracle
+    row nnz), each insert costs >= 1 probe, and on the stencil the high-bit
+    hash collides less than the literal low-bit remainder (reading R5)."""
+    if which == "c2":  # g = 16: neighbour strides 16 and 256 are powers of two (R5)
+        A, B, _ = synth.workload("c2_stencil64", scale=16)
+    else:
+        A, B, _ = synth.workload("c3_rmat20", scale=11)
+    dA = spg.DeviceCSR.from_host(A)
+    dB = dA if B is A else spg.DeviceCSR.from_host(B)
+    st = spg.probe_stats(dA, dB, ctx=ctx)
+    nnz = oracle.row_nnz(A, B)
+    want_keys = int(nnz[(nnz > 0) & (2 * nnz <= 1024)].sum())
+    _, f = oracle.flop(A, B)
+    for mode, (probes, products, keys, c) in st.items():
+        assert keys == want_keys, mode
+        assert probes >= products > 0, mode
+        assert products <= f
+    if which == "c2":
+        assert st["linear_high_bits"][3] < st["linear_low_bits"][3]
