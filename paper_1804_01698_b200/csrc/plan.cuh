@@ -101,41 +101,53 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
     tile_rows(A, base, t0, nz, s_r, trow, tcap);
     __syncthreads();
     const int64_t rlo = s_r[0], rhi = s_r[1];
-    const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
     const int64_t jend = base + nz;
+    if (use_bm) {
+      // mostly-empty B: most a_ik gather nothing, so a warp takes 32
+      // consecutive a_ik at a time (coalesced column loads) and finds rows
+      // only for the useful ones (one atomic each); the ballot of useful
+      // entries is the pruning bitmask: word (tile, chunk), bit = lane
+      for (int ch = threadIdx.x >> 5; ch < kFlopTile / 32; ch += kFlopThreads / 32) {
+        const int64_t j = base + t0 + int64_t(ch) * 32 + lane;
+        unsigned long long len = 0;
+        if (j < jend) {
+          const int k = __ldg(A.col + j);
+          if ((__ldg(b_nonempty + (k >> 5)) >> (k & 31)) & 1u)
+            len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
+        }
+        const unsigned bal = __ballot_sync(kFull, len > 0);
+        const int64_t word = (t0 / kFlopTile) * (kFlopTile / 32) + ch;
+        if (useful_bits != nullptr && word < bits_cap && lane == 0) useful_bits[word] = bal;
+        if (!bal) continue;
+        if (len > 0) {
+          const int64_t r = row_of(A.rp, rlo, rhi, j);
+          atomicAdd(flop + r, len);
+          if (useful_row) atomicAdd(useful_row + r, 1ull);
+          useful += 1;
+          maxb = len > maxb ? len : maxb;
+        }
+      }
+      continue;
+    }
+    const int64_t j0 = base + t0 + int64_t(threadIdx.x) * kFlopRun;
     int64_t r = j0 < jend ? row_of(A.rp, rlo, rhi, j0) : rhi;
     int64_t rend = __ldg(A.rp + r + 1);
-    unsigned long long acc = 0, acc_u = 0;
-    // useful-entry bitmask for the pruning pass: word (tile, warp, u), bit =
-    // lane <-> entry tile + (warp * 32 + lane) * kFlopRun + u
-    const int64_t wbase = (t0 / kFlopTile) * (kFlopThreads / 32) * kFlopRun +
-                          int64_t(threadIdx.x >> 5) * kFlopRun;
-    const bool want_bits = use_bm && useful_bits != nullptr && wbase + kFlopRun <= bits_cap;
+    unsigned long long acc = 0;
     // walk the run; flush acc at each row boundary (all but the last segment)
     for (int u = 0; u < kFlopRun; ++u) {
       const int64_t j = j0 + u;
-      unsigned long long len = 0;
-      if (j < jend) {
-        if (j >= rend) {
-          if (acc) atomicAdd(flop + r, acc);
-          if (use_bm && useful_row && acc_u) atomicAdd(useful_row + r, acc_u);
-          acc = 0;
-          acc_u = 0;
-          r = advance_row(A.rp, r + 1, rhi, j);
-          rend = __ldg(A.rp + r + 1);
-        }
-        const int k = __ldg(A.col + j);
-        if (!use_bm || ((__ldg(b_nonempty + (k >> 5)) >> (k & 31)) & 1u))
-          len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
-        acc += len;
-        acc_u += len > 0;
-        useful += len > 0;
-        maxb = len > maxb ? len : maxb;
+      if (j >= jend) break;
+      if (j >= rend) {
+        if (acc) atomicAdd(flop + r, acc);
+        acc = 0;
+        r = advance_row(A.rp, r + 1, rhi, j);
+        rend = __ldg(A.rp + r + 1);
       }
-      if (want_bits) {  // (warp-uniform)
-        const unsigned bal = __ballot_sync(kFull, len > 0);
-        if (lane == 0) useful_bits[wbase + u] = bal;
-      }
+      const int k = __ldg(A.col + j);
+      const unsigned long long len = (unsigned long long)(__ldg(b_rp + k + 1) - __ldg(b_rp + k));
+      acc += len;
+      useful += len > 0;
+      maxb = len > maxb ? len : maxb;
     }
 
     // last segment: lanes holding the same row combine before the atomic
@@ -151,14 +163,6 @@ __global__ void __launch_bounds__(kFlopThreads) k_flop_nz(DevCSR A, const int64_
       if (lane + o < 32 && ((grp >> (lane + o)) & 1u)) sum += v;
     }
     if (lane == leader && j0 < jend && sum) atomicAdd(flop + r, sum);
-    if (use_bm && useful_row) {  // same segmented sum for the useful-entry counts
-      unsigned long long su = acc_u;
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_down_sync(kFull, su, o);
-        if (lane + o < 32 && ((grp >> (lane + o)) & 1u)) su += v;
-      }
-      if (lane == leader && j0 < jend && su) atomicAdd(useful_row + r, su);
-    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long t = __shfl_xor_sync(kFull, maxb, o);
@@ -246,13 +250,13 @@ __global__ void __launch_bounds__(256) k_prune_scatter_bits(DevCSR A, const uint
                                                             const int64_t *__restrict__ trow,
                                                             int64_t tcap) {
   const int64_t base = A.rp[0];
-  constexpr int kWordsPerTile = (kFlopThreads / 32) * kFlopRun;
+  constexpr int kWordsPerTile = kFlopTile / 32;
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords;
        q += int64_t(gridDim.x) * blockDim.x) {
     uint32_t word = bits[q];
     if (!word) continue;
     const int64_t t = q / kWordsPerTile;
-    const int wi = (int)((q % kWordsPerTile) / kFlopRun), u = (int)(q % kFlopRun);
+    const int ch = (int)(q % kWordsPerTile);
     int64_t rlo = 0, rhi = A.nrows - 1;
     if (trow && t + 1 <= tcap) {
       rlo = trow[t];
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(256) k_prune_scatter_bits(DevCSR A, const uint
     while (word) {
       const int lane = __ffs(word) - 1;
       word &= word - 1;
-      const int64_t j = base + t * kFlopTile + int64_t(wi * 32 + lane) * kFlopRun + u;
+      const int64_t j = base + t * kFlopTile + int64_t(ch) * 32 + lane;
       const int64_t r = row_of(A.rp, rlo, rhi, j);
       const int k = __ldg(A.col + j);
       const int64_t pos = rp2[r] + (int64_t)atomicAdd(cursor + r, 1ull);

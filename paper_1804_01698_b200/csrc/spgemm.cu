@@ -475,7 +475,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       SPG_CUDA(c, cudaMemcpyAsync(rp2 + 1, cnt, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
       if ((st = launch_scan(c, rp2 + 1, m, s)) != SPG_OK) return st;
       SPG_CUDA(c, cudaMemsetAsync(cnt, 0, size_t(m) * 8, s));
-      const int64_t nwords = ceil_div((int64_t)h.a_nnz, kFlopTile) * (kFlopThreads / 32) * kFlopRun;
+      const int64_t nwords = ceil_div((int64_t)h.a_nnz, kFlopTile) * (kFlopTile / 32);
       if (c->useful_bits.p && int64_t(c->useful_bits.bytes / 4) >= nwords) {
         // k_flop_nz wrote the useful-entry bitmask of this A: visit only those
         ProfScope _ps(c, s, "k_prune_scatter_bits");
