@@ -606,12 +606,15 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // keys of the row before the part.  No global atomics.
 // ---------------------------------------------------------------------------
 constexpr int kTEnt = 1024;                 // a_ik staged per chunk
-constexpr int kTPartT = 2 * kTPartKeys;     // hash slots (load <= 1/2)
+constexpr int kTPartLogT = 12;
+constexpr int kTPartT = 1 << kTPartLogT;      // hash slots of a multi-tile part
+static_assert(4 * kTPartKeys <= 3 * kTPartT, "multi-tile part: load <= 3/4");
 constexpr int64_t kTRankCols = int64_t(32) * kTileCols;  // sorted emit by bitmap rank up to this span
 constexpr size_t kTDenseBytes = size_t(kTileCols) * 8 + size_t(kTileCols) / 8;
 constexpr size_t kTHashBytes = size_t(kTPartT) * 12 + size_t(kTPartKeys) * 2;
 constexpr size_t kTUnion = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;
-constexpr size_t kTEntBytes = 24576;        // es i64 + ea f64 + epre i32 [kTEnt(+1)]; sorted gather
+constexpr size_t kTEntBytes = size_t(kTPartKeys) * 12 > 24576 ? size_t(kTPartKeys) * 12 : 24576;
+                                            // es i64 + ea f64 + epre i32 [kTEnt(+1)]; sorted gather
 static_assert(size_t(kTEnt) * 20 + 4 <= kTEntBytes, "entry stage");
 static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
@@ -715,7 +718,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     const long long c0 = instr ? clock64() : 0;
     long long c_stage = 0, c_rounds = 0;
     unsigned long long prods = 0;
-    const int logT = dense ? 0 : num_log2(cnt);
+    const int logT = dense ? 0 : min(num_log2(cnt), kTPartLogT);
     const int T = 1 << logT;
     if (dense) {
       for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;

@@ -115,7 +115,10 @@ __device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols, int64_t na) 
 // parts (the numeric G bin).
 constexpr int kTileLog = 13;
 constexpr int kTileCols = 1 << kTileLog;
-constexpr int kTPartKeys = 2048;
+#ifndef SPG_TPART_KEYS
+#define SPG_TPART_KEYS 2048
+#endif
+constexpr int kTPartKeys = SPG_TPART_KEYS;
 constexpr int kPartMinKeys = 8192;
 constexpr int kMaxTiles = 256;  // >= kBitmapMaxCols / kTileCols + 1
 
