@@ -498,24 +498,24 @@ __global__ void __launch_bounds__(256) k_check_sorted(DevCSR B, PlanInfo *info) 
 // at or before its own.  Positions fit int32 (checked by the host).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_tile_offsets(DevCSR B, int ntiles, int32_t *__restrict__ toff) {
+  // toff[k][t] = first position of B row k (sorted) with column >= t * kTileCols:
+  // a warp per row, lane l searches tiles l, l + 32, ... (lower bound in the
+  // row; coalesced stores, no serial walk over the tiles an entry skips)
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t k = warp; k < B.nrows; k += nwarps) {
     const int64_t s = B.rp[k], e = B.rp[k + 1];
     int32_t *o = toff + k * (ntiles + 1);
-    int prev_tile = -1;  // tile of the entry before this chunk's first (-1: none)
-    for (int64_t q0 = s; q0 < e; q0 += 32) {
-      const int64_t q = q0 + lane;
-      const int tc = q < e ? (__ldg(B.col + q) >> kTileLog) : ntiles;
-      int tp = __shfl_up_sync(kFull, tc, 1);
-      if (lane == 0) tp = prev_tile;
-      if (q < e)
-        for (int t = tp + 1; t <= tc; ++t) o[t] = (int32_t)q;
-      const int lastlane = (e - q0) < 32 ? int(e - q0) - 1 : 31;
-      prev_tile = __shfl_sync(kFull, tc, lastlane);
+    for (int t = lane; t <= ntiles; t += 32) {
+      const int64_t key = int64_t(t) << kTileLog;
+      int64_t lo = s, hi = e;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)__ldg(B.col + mid) < key) lo = mid + 1; else hi = mid;
+      }
+      o[t] = (int32_t)lo;
     }
-    for (int t = prev_tile + 1 + lane; t <= ntiles; t += 32) o[t] = (int32_t)e;  // after the last entry
   }
 }
 
