@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         int32_t *__restrict__ part_n) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
+  __shared__ long long s_pbase;
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
   __shared__ int s_cut[kMaxTiles];       // first tile of each part
@@ -476,31 +477,45 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     const int nnz = s_cnt;
     if (threadIdx.x == 0) row_nnz[i] = nnz;
     if (want_parts && nnz > kPartMinKeys) {
-      if (threadIdx.x == 0) {
-        // parts: greedy runs of consecutive tiles holding <= kTPartKeys keys;
-        // a tile holding more stands alone (dense window in the numeric phase)
-        int np = 0, start = 0, acc = 0;
-        for (int t = 0; t < ntiles; ++t) {
-          const int c = s_tile[t + 1] - s_tile[t];
-          if (acc > 0 && acc + c > kTPartKeys) {
-            s_cut[np++] = start;
-            start = t;
-            acc = 0;
-          }
-          acc += c;
+      // parts: greedy runs of consecutive tiles holding <= kTPartKeys keys; a
+      // tile holding more stands alone (dense window in the numeric phase).
+      // The greedy run starting at tile t ends before u(t), found by a search
+      // of the tile prefix P = s_tile: x = first x >= t + 2 with P(x) > P(t) +
+      // kTPartKeys; u = x - 1, or x when tiles t .. x - 2 are empty (the
+      // greedy run never cuts before its first key).  One thread per tile,
+      // then the chain 0 -> u(0) -> ... (one step per part).
+      int *s_nxt = s_tcnt;  // (tile counts are consumed)
+      for (int t = threadIdx.x; t < ntiles; t += THREADS) {
+        const int lim = s_tile[t] + kTPartKeys;
+        int lo = t + 2, hi = ntiles + 1;  // first x in [t + 2, ntiles] with P(x) > lim, else ntiles + 1
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (s_tile[m] > lim) hi = m; else lo = m + 1;
         }
-        s_cut[np++] = start;
+        int u = lo - 1;
+        if (lo <= ntiles && s_tile[lo - 1] == s_tile[t]) u = lo;
+        s_nxt[t] = u > ntiles ? ntiles : u;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int np = 0;
+        for (int t = 0; t < ntiles; t = s_nxt[t]) s_cut[np++] = t;
         const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
         if (base + np > parts_cap) {
           atomicAdd(&info->parts_overflow, 1ull);
           part_n[i] = 0;
+          s_cnt = -1;
         } else {
-          for (int p = 0; p < np; ++p) {
-            parts[base + p] = make_int2(s_cut[p] << kTileLog, s_tile[s_cut[p]]);
-            part_row[base + p] = i;
-          }
           part_n[i] = np;
+          s_cnt = np;
+          s_pbase = base;
         }
+      }
+      __syncthreads();
+      const int np = s_cnt;
+      for (int p = threadIdx.x; p < np; p += THREADS) {
+        parts[s_pbase + p] = make_int2(s_cut[p] << kTileLog, s_tile[s_cut[p]]);
+        part_row[s_pbase + p] = i;
       }
     } else if (threadIdx.x == 0 && part_n != nullptr) {
       part_n[i] = 0;  // no parts: a B-tier row
