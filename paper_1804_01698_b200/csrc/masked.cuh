@@ -223,17 +223,28 @@ __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevC
     __syncwarp();
     // C rows are long (C5: ~18 K entries per row): kU coalesced column loads
     // in flight before the probes
+    // (the next batch's loads are issued before this batch is probed)
     constexpr int kU = 8;
-    for (int64_t q0 = cs + lane; q0 < ce; q0 += 32 * kU) {
-      uint32_t cc[kU];
+    uint32_t cc[kU], nc[kU];
+    int64_t q0 = cs + lane;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t q = q0 + 32 * u;
+      cc[u] = q < ce ? (uint32_t)__ldg(C.col + q) : kEmpty;
+    }
+    while (q0 < ce) {
+      const int64_t q1 = q0 + 32 * kU;
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int64_t q = q0 + 32 * u;
-        cc[u] = q < ce ? (uint32_t)__ldg(C.col + q) : kEmpty;
+        const int64_t q = q1 + 32 * u;
+        nc[u] = q < ce ? (uint32_t)__ldg(C.col + q) : kEmpty;
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (cc[u] != kEmpty && set_contains(tab, cc[u], logT)) acc += __ldg(C.val + q0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) cc[u] = nc[u];
+      q0 = q1;
     }
     __syncwarp();
   }
