@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
                                                        int tmax) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_cnt, s_next;
+  __shared__ DeferList s_dl;  // long B rows walked by the whole block
   __shared__ int s_red[66];
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5;
@@ -448,8 +449,8 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
       auto acc_comb = [&](bool act, uint32_t c, double v) {  // keys may repeat in a round
         if (warp_combine(act, c, v)) atomicAdd(vals + num_probe_smem(keys, c, logT), v);
       };
-      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next);
-      else for_row<false, true>(A, B, as, ae, w, NW, acc_comb, &s_next);
+      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next, &s_dl);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc_comb, &s_next, &s_dl);
     }
     __syncthreads();
     block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
@@ -553,6 +554,7 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
                                                         int64_t slabT) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
+  __shared__ DeferList s_dl;  // long B rows walked by the whole block
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5;
   uint32_t *keys = slab_keys + int64_t(blockIdx.x) * slabT;
@@ -574,8 +576,8 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
       auto acc = [&](bool act, uint32_t c, double v) {
         if (act) atomicAdd(vals + num_probe(keys, c, logT), v);
       };
-      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next);
-      else for_row<false, true>(A, B, as, ae, w, NW, acc, &s_next);
+      if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next, &s_dl);
+      else for_row<false, true>(A, B, as, ae, w, NW, acc, &s_next, &s_dl);
     }
     __syncthreads();
     if (!sorted) {

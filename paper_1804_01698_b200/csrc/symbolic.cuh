@@ -64,9 +64,20 @@ struct Entry {
   double a;
 };
 
+// Long B rows deferred to a block-wide walk (for_entries, dynamic chunks).
+constexpr int kLongLen = 64;
+constexpr int kLongCap = 256;
+struct DeferList {
+  long long bs[kLongCap];
+  double a[kLongCap];
+  int len[kLongCap];
+  int n;
+};
+
 template <bool kSeq, bool kVal, int kDepth, bool kAutoFlat = false, typename EF, typename F>
 __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w, int NW,
-                                            EF &&entry, F &&f, int *next = nullptr) {
+                                            EF &&entry, F &&f, int *next = nullptr,
+                                            DeferList *dl = nullptr) {
   const int lane = lane_id();
   // Many chunks: each warp owns whole chunks (chunk overhead paid once) --
   // taken from the block's counter `next` when given (chunk costs differ with
@@ -84,19 +95,19 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
   };
   int64_t cb0 = own_chunks ? int64_t(w) * 32 : 0;
   if (dyn) cb0 = next_chunk(0);
-  for (int64_t cb = cb0; cb < nent; cb = next_chunk(cb)) {
-    Entry en{0, 0, 0.0};
-    if (cb + lane < nent) en = entry(cb + lane);
+  // the per-chunk walk (own = this warp owns the chunk; else every warp
+  // takes a contiguous slice of the chunk's rounds)
+  auto body = [&](Entry en, bool own) {
     // kAutoFlat (f tolerates equal keys inside a round): a chunk of short B
     // rows (average < kFlatAvgLen) runs flattened (full lanes) even in a
     // sequential row
     bool seq = kSeq;
-    if (kSeq && kAutoFlat && own_chunks) {
+    if (kSeq && kAutoFlat && own) {
       const int sum = (int)__reduce_add_sync(kFull, (unsigned)en.len);
       const int ne = __popc(__ballot_sync(kFull, en.len > 0));
       seq = sum >= kFlatAvgLen * ne;
     }
-    if (seq && own_chunks && __all_sync(kFull, en.len <= 32)) {
+    if (seq && own && __all_sync(kFull, en.len <= 32)) {
       // this warp owns the chunk and every B row fits one round: one round per
       // nonempty entry.  kDepth <= 2 (warp tiers, occupancy-bound): one round
       // ahead.  Deeper (block / bitmap tiers): rolling software pipeline over
@@ -107,7 +118,7 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
       if constexpr (kDepth <= 2) {
         // one round ahead: the gathers of the next round are issued before
         // this one is hashed
-        if (!pend) continue;
+        if (!pend) return;
         int j = __ffs(pend) - 1;
         pend &= pend - 1;
         int L = __shfl_sync(kFull, en.len, j);
@@ -140,7 +151,7 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
           bv = nbv;
           aj = na;
         }
-        continue;
+        return;
       }
       int sl[kDepth];
       uint32_t sc[kDepth];
@@ -171,9 +182,9 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
           fill(d);
         }
       }
-      continue;
+      return;
     }
-    if ((kDepth <= 2 || !kVal) && seq && own_chunks) {
+    if ((kDepth <= 2 || !kVal) && seq && own) {
       // warp tiers and the symbolic walks: the nonempty entries directly
       // (measured: the pipelined walker below costs the occupancy-bound warp
       // kernels registers, and the symbolic bitmap tier time)
@@ -195,14 +206,14 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
           f(act, c, v);
         }
       }
-      continue;
+      return;
     }
-    if (seq && own_chunks) {
+    if (seq && own) {
       // this warp owns the chunk (some B rows longer than 32): walk its
       // nonempty entries, a round = 32 consecutive b_kj of one B row, with
       // the gathers of the next round issued before this one is applied
       unsigned pend = __ballot_sync(kFull, en.len > 0);
-      if (!pend) continue;
+      if (!pend) return;
       int L = 0, t = -32;
       int64_t jbs = 0;
       double aj = 0.0;
@@ -242,15 +253,15 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
         bv = nbv;
         a = aj;
       }
-      continue;
+      return;
     }
     const int r = seq ? ((en.len + 31) >> 5) : en.len;  // rounds (seq) or products
     const int incl = warp_incl_scan(r);
     const int total = __shfl_sync(kFull, incl, 31);
     const int nr = seq ? total : ((total + 31) >> 5);
-    const int g0 = own_chunks ? 0 : (int)((int64_t)nr * w / NW);
-    const int g1 = own_chunks ? nr : (int)((int64_t)nr * (w + 1) / NW);
-    if (g0 >= g1) continue;
+    const int g0 = own ? 0 : (int)((int64_t)nr * w / NW);
+    const int g1 = own ? nr : (int)((int64_t)nr * (w + 1) / NW);
+    if (g0 >= g1) return;
     if (seq) {
       // the owner entry of round g advances monotonically along [g0, g1)
       int own = 0, obeg = 0, oend = 0, olen = 0;
@@ -310,13 +321,57 @@ __device__ __forceinline__ void for_entries(const DevCSR &B, int64_t nent, int w
         f(act, c, v);
       }
     }
+  };
+  // Deferral of long B rows (block tiers, dynamic chunks): an entry with more
+  // than kLongLen products would leave its warp walking it alone while the
+  // block waits at the row's barrier (R-MAT hub rows); such entries go to a
+  // block-shared list that all warps split by rounds after the chunks.
+  const bool defer = dyn && dl != nullptr;
+  if (defer) {
+    if (threadIdx.x == 0) dl->n = 0;
+    __syncthreads();
+  }
+  for (int64_t cb = cb0; cb < nent; cb = next_chunk(cb)) {
+    Entry en{0, 0, 0.0};
+    if (cb + lane < nent) en = entry(cb + lane);
+    if (defer) {
+      const bool lg = en.len > kLongLen;
+      const unsigned m = __ballot_sync(kFull, lg);
+      if (m) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&dl->n, __popc(m));
+        base = __shfl_sync(kFull, base, 0);
+        const int idx = base + __popc(m & ((1u << lane) - 1u));
+        if (lg && idx < kLongCap) {
+          dl->bs[idx] = en.bs;
+          dl->len[idx] = en.len;
+          if (kVal) dl->a[idx] = en.a;
+          en.len = 0;  // walked below by the whole block
+        }
+      }
+    }
+    body(en, own_chunks);
+  }
+  if (defer) {
+    __syncthreads();
+    const int nl = min(dl->n, kLongCap);
+    for (int c0 = 0; c0 < nl; c0 += 32) {
+      Entry en{0, 0, 0.0};
+      if (c0 + lane < nl) {
+        en.bs = dl->bs[c0 + lane];
+        en.len = dl->len[c0 + lane];
+        en.a = kVal ? dl->a[c0 + lane] : 0.0;
+      }
+      body(en, false);
+    }
   }
 }
 
 // All products of row [as, ae) of A.
 template <bool kSeq, bool kVal, int kDepth = (kVal ? 4 : 8), bool kAutoFlat = false, typename F>
 __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_t as,
-                                        int64_t ae, int w, int NW, F &&f, int *next = nullptr) {
+                                        int64_t ae, int w, int NW, F &&f, int *next = nullptr,
+                                        DeferList *dl = nullptr) {
   for_entries<kSeq, kVal, kDepth, kAutoFlat>(
       B, ae - as, w, NW,
       [&](int64_t j) {
@@ -327,7 +382,7 @@ __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_
         en.a = kVal ? __ldg(A.val + as + j) : 0.0;
         return en;
       },
-      f, next);
+      f, next, dl);
 }
 
 // Rows whose B rows average >= kSeqMinLen entries use the sequential
@@ -379,6 +434,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
                                                        int64_t *__restrict__ row_nnz) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
+  __shared__ DeferList s_dl;  // long B rows walked by the whole block
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_dyn_u32;
@@ -394,8 +450,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
     auto ins = [&](bool act, uint32_t c, double) {
       if (act) cnt += sym_insert_smem(tab, c, logT);
     };
-    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
-    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
+    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
+    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
@@ -422,6 +478,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         int32_t *__restrict__ part_n) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
+  __shared__ DeferList s_dl;  // long B rows walked by the whole block
   __shared__ long long s_pbase;
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
@@ -443,8 +500,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     auto ins = [&](bool act, uint32_t c, double) {
       if (act) atomicOr(bm + (c >> 5), 1u << (c & 31u));
     };
-    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
-    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
+    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
+    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     __syncthreads();
     // keys per column tile (a warp per tile), clearing the words for the next
     // row on the way; then the exclusive scan over the tiles = keys before
@@ -536,6 +593,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_global(const int32_t *__restric
                                                         uint32_t *__restrict__ slab,
                                                         int64_t slabT) {
   __shared__ int s_cnt, s_next;
+  __shared__ DeferList s_dl;  // long B rows walked by the whole block
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = slab + int64_t(blockIdx.x) * slabT;
@@ -552,8 +610,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_global(const int32_t *__restric
       auto ins = [&](bool act, uint32_t c, double) {
         if (act) cnt += sym_insert(tab, c, logT);
       };
-      if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next);
-      else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next);
+      if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
+      else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     }
     cnt = warp_sum(cnt);
     if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
