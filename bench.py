@@ -148,7 +148,7 @@ NUM_KERNEL_BIN = {"k_num_warp<256>": [1], "k_num_warp<1024>": [2],
                   "k_num_block<512>": [3, 4], "k_num_block<1024>": [5, 6],
                   "k_num_global<1024>": [7], "k_num_tpart<512>": [7]}
 SYM_KERNEL_BIN = {"k_sym_warp<128>": [1], "k_sym_warp<1024>": [2],
-                  "k_sym_block<512>": [3, 4, 5], "k_sym_block<1024>": [6, 7],
+                  "k_sym_block<128>": [3, 4], "k_sym_block<256>": [5], "k_sym_block<1024>": [6, 7],
                   "k_sym_bitmap<1024>": [9], "k_sym_global<1024>": [8]}
 
 
