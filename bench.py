@@ -145,7 +145,7 @@ def bin_of_rows_sym(flop: np.ndarray, ncols: int) -> np.ndarray:
 
 
 NUM_KERNEL_BIN = {"k_num_warp<256>": [1], "k_num_warp<1024>": [2],
-                  "k_num_block<512>": [3, 4], "k_num_block<1024>": [5, 6],
+                  "k_num_block<128>": [3], "k_num_block<512>": [4, 5], "k_num_block<1024>": [6],
                   "k_num_global<1024>": [7], "k_num_tpart<512>": [7]}
 SYM_KERNEL_BIN = {"k_sym_warp<128>": [1], "k_sym_warp<1024>": [2],
                   "k_sym_block<128>": [3, 4], "k_sym_block<256>": [5], "k_sym_block<1024>": [6, 7],

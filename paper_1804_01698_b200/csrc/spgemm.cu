@@ -309,6 +309,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
     const size_t s_num_b = size_t(16384) * 12;
     ok = set_smem(c, k_num_warp<1024, 4, 0>, s_num_w1024) == SPG_OK &&
          set_smem(c, k_num_warp<1024, 4, 1>, s_num_w1024) == SPG_OK &&
+         set_smem(c, k_num_block<128>, size_t(2048) * 12) == SPG_OK &&
          set_smem(c, k_num_block<512>, s_num_b) == SPG_OK &&
          set_smem(c, k_num_block<1024>, s_num_b) == SPG_OK &&
          set_smem(c, k_sym_block<512>, size_t(32768) * 4) == SPG_OK &&
@@ -753,16 +754,22 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       const int tmax = 1 << logT;
       const size_t smem = size_t(tmax) * 12;
       const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 8);
-      if (logT <= 12)
-        {
-          ProfScope _ps(c, ss, "k_num_block<512>");
-          k_num_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
-        }
-      else
-        {
-          ProfScope _ps(c, ss, "k_num_block<1024>");
-          k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
-        }
+      // block size per table size (measured on C3: 2K slots 128 threads,
+      // 4K / 8K 512, 16K 1024 -- smaller blocks idle less at the row
+      // barrier, larger ones keep the occupancy of the big tables)
+      if (logT <= 11) {
+        ProfScope _ps(c, ss, "k_num_block<128>");
+        k_num_block<128><<<(unsigned)std::min<int64_t>(n, int64_t(c->num_sms) * 32), 128, smem, ss>>>(
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
+      } else if (logT <= 13) {
+        ProfScope _ps(c, ss, "k_num_block<512>");
+        k_num_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx,
+                                                           C_val, sorted, tmax);
+      } else {
+        ProfScope _ps(c, ss, "k_num_block<1024>");
+        k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx,
+                                                             C_val, sorted, tmax);
+      }
       SPG_LAUNCHED(c, "k_num_block");
     } else if (use_parts) {  // NB_G: column-tile parts, independent work items
       {
