@@ -122,6 +122,8 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
   extern __shared__ uint32_t s_bm[];
   __shared__ long long s_row;
   __shared__ double s_acc[THREADS / 32];
+  __shared__ int s_next;
+  __shared__ DeferList s_dl;  // long B rows walked by the whole block
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwords = (int)((B.ncols + 31) >> 5);
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
     if (threadIdx.x == 0) {
       const long long q = (long long)atomicAdd(row_counter, 1ull);
       s_row = q < nl ? (long long)list[nl - 1 - q] : -1;
+      s_next = 0;
     }
     __syncthreads();
     const long long r = s_row;
@@ -172,8 +175,8 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
     __syncthreads();
     double flt = 0.0;
     for (int u = 0; u < NW; ++u) flt += s_acc[u];
-    if (use_seq((int64_t)flt, ae - as)) for_row<true, true>(A, B, as, ae, w, NW, f);
-    else for_row<false, true>(A, B, as, ae, w, NW, f);
+    if (use_seq((int64_t)flt, ae - as)) for_row<true, true>(A, B, as, ae, w, NW, f, &s_next, &s_dl);
+    else for_row<false, true>(A, B, as, ae, w, NW, f, &s_next, &s_dl);
     __syncthreads();
     if (use_bitmap)  // clear exactly the bits of G_i for the next row
       for (int64_t q = gs + threadIdx.x; q < ge; q += THREADS) {
