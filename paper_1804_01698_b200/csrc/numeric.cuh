@@ -704,8 +704,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   if (threadIdx.x == 0) s_q = (long long)atomicAdd(counter, 1ull);
   __syncthreads();
   while (true) {
-    const int64_t q = s_q;  // (the next part is fetched before the part's last barrier)
+    const int64_t q = s_q;
     if (q >= nparts) break;
+    // the next part is reserved now; its index is published at the part's
+    // last barrier (the atomic's latency hides behind this part's work)
+    long long q_next = 0;
+    if (threadIdx.x == 0) q_next = (long long)atomicAdd(counter, 1ull);
     const int i = part_row[q];
     const int2 P = parts[q];
     const int64_t rp0 = c_rp[i];
@@ -891,7 +895,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
                              c_val, s_red);
       }
     }
-    if (threadIdx.x == 0) s_q = (long long)atomicAdd(counter, 1ull);  // every thread has read q
+    if (threadIdx.x == 0) s_q = q_next;  // every thread has read q
     __syncthreads();
     if (instr) {
       const long long cz = clock64();
