@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     const int i = rows[r];
     const int logT = sym_log2_gpu(flop[i], B.ncols);
     const int T = 1 << logT;
-    for (int s = lane; s < T; s += 32) tab[s] = kEmpty;
+    for (int s = lane * 4; s < T; s += 128)  // T >= 32: 16-byte stores (T % 4 == 0)
+      *reinterpret_cast<uint4 *>(tab + s) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncwarp();
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
