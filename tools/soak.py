@@ -39,5 +39,23 @@ for seed in range(n):
             print("FAIL", seed, kind, so, str(e)[:200], flush=True)
     if seed % 10 == 9:
         print("done", seed + 1, "fails", bad, flush=True)
-print("soak", n, "cases x2 orders, failures:", bad)
+# triangle counting on random graphs: natural order (C formed and fused) and
+# the degree relabelling, against the oracle's count
+import oracle  # noqa: E402
+tbad = 0
+for seed in range(max(1, n // 4)):
+    rng = np.random.default_rng(5000 + seed)
+    G = synth.symmetrise_pattern(synth.rmat(int(rng.integers(8, 12)), int(rng.integers(4, 16)), seed),
+                                 drop_diagonal=True)
+    L, U = synth.tril_strict(G), synth.triu_strict(G)
+    want = oracle.triangle_count(L, U, G)
+    dL, dU, dG = (spg.DeviceCSR.from_host(x) for x in (L, U, G))
+    got = (spg.triangle_count(dL, dU, dG, sorted=bool(seed % 2), ctx=ctx),
+           spg.triangle_count_fused(dL, dU, dG, ctx=ctx), spg.triangle_count_graph(dG, ctx=ctx))
+    if any(g != want for g in got):
+        tbad += 1
+        print("TRI FAIL", seed, want, got, flush=True)
+print("soak", n, "cases x2 orders, failures:", bad, "; triangle graphs", max(1, n // 4),
+      "failures:", tbad)
+bad += tbad
 sys.exit(1 if bad else 0)
