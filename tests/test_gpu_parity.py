@@ -436,3 +436,14 @@ def test_probe_stats(spg, ctx, which):
         assert products <= f
     if which == "c2":
         assert st["linear_high_bits"][3] < st["linear_low_bits"][3]
+
+
+def test_c4_pruned_bitmask_growth(spg):
+    """The pruning scatter's useful-entry bitmask is a grow-only workspace:
+    a smaller A sizes it, a larger A must fall back to the full scan (and
+    regrow), a repeat of the larger A uses the bitmask -- all exact."""
+    ctx = spg.Context()
+    for scale in (16, 17, 17, 16):  # nnz(A) 1.8 M / 3.6 M: both pruned
+        A, B, _ = synth.workload("c4_tallskinny", scale=scale)
+        assert A.nnz >= (1 << 20)
+        gpu_vs_oracle(A, B, True, ctx=ctx, what=f"C4 s{scale} bitmask growth")
