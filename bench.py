@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 # C of the large configs is >100 GB: avoid caching-allocator fragmentation
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
-DEFAULT_CONFIG = "c2_stencil64"   # BASELINE.json configs[1]
+DEFAULT_CONFIG = "c3_rmat20"      # the largest single-GPU config (configs[2]); C2 etc. via --config
 L2_FLUSH_BYTES = 256 << 20
 FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback
 
@@ -189,66 +189,85 @@ def ncu_traffic(config: str, kernel: str):
 
 
 # ----------------------------------------------------------------------------- oracle
-def oracle_sample(A, B, target_s: float = 12.0, nthreads: int = 0):
-    """Time the oracle (as it stands) on a bounded row sample of the workload:
-    a contiguous block of rows grown until ~target_s of CPU work."""
+def row_sample(A, of, frac: float, seed: int = 2024):
+    """Sub-matrix of A made of a seeded uniform random sample of its rows
+    (every row equally likely, so hub and empty rows appear in proportion):
+    returns (sub-A, sampled flop).  Host-side input preparation only."""
+    import synth
+    rng = np.random.default_rng(seed)
+    m = A.nrows
+    k = max(1, min(m, int(round(m * frac))))
+    rows = np.sort(rng.choice(m, size=k, replace=False))
+    lens = np.diff(A.row_ptr)[rows]
+    rp = np.zeros(k + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    idx = np.repeat(A.row_ptr[rows] - rp[:-1], lens) + np.arange(int(rp[-1]), dtype=np.int64)
+    sub = synth.CSR(k, A.ncols, rp, A.col[idx].astype(np.int32), A.val[idx].astype(np.float64))
+    return sub, int(of[rows].sum()), k
+
+
+def oracle_sample(A, B, target_s: float = 12.0, nthreads: int = 0, reps_min_s: float = 3.0):
+    """Time the oracle (as it stands) on a bounded, representative sample of
+    the workload: a seeded uniform random sample of A's rows (times B), sized
+    to ~target_s of CPU work from a calibration run."""
     import oracle
     of, tot = oracle.flop(A, B)
-    ps = np.r_[0, np.cumsum(of)]
     nthreads = nthreads or (os.cpu_count() or 1)
-    # calibrate on ~0.5% of the flop (at least one row)
-    r1 = int(np.searchsorted(ps, max(1, tot // 200))) + 1
-    r1 = min(max(r1, 1), A.nrows)
+    frac = 0.002
+    sub, f, k = row_sample(A, of, frac)
     t0 = time.perf_counter()
-    oracle.spgemm(A, B, 0, r1, nthreads=nthreads)
+    oracle.spgemm(sub, B, nthreads=nthreads)
     dt = max(time.perf_counter() - t0, 1e-6)
-    rate = max(int(ps[r1]), 1) / dt
-    want = min(tot, int(rate * target_s))
-    r_end = min(A.nrows, int(np.searchsorted(ps, want)) + 1)
+    rate = max(f, 1) / dt
+    frac = min(1.0, frac * max(1.0, target_s * rate / max(f, 1)) if f else 1.0)
+    sub, f, k = row_sample(A, of, frac)
     reps, dt = 0, 0.0
-    while reps == 0 or (dt < 3.0 and reps < 50):  # tiny workloads: repeat, average
+    while reps == 0 or (dt < reps_min_s and reps < 50):  # tiny workloads: repeat, average
         t0 = time.perf_counter()
-        oracle.spgemm(A, B, 0, r_end, nthreads=nthreads)
+        oracle.spgemm(sub, B, nthreads=nthreads)
         dt += time.perf_counter() - t0
         reps += 1
     dt /= reps
-    f = int(ps[r_end])
     return {"value": 2 * f / dt / 1e9, "unit": "GFLOPS", "cores": nthreads, "kind": "oracle",
-            "sample": f"rows [0, {r_end}) of {A.nrows}: {f} of {tot} flop ({100.0 * f / max(tot, 1):.1f}%), "
-                      f"{dt:.3f} s per run (mean of {reps}), OpenMP over rows"}
+            "sample": f"{k} of {A.nrows} rows drawn uniformly at random (seed 2024): {f} of {tot} flop "
+                      f"({100.0 * f / max(tot, 1):.2f}%), {dt:.3f} s per run (mean of {reps}), "
+                      f"OpenMP over rows"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        log(f"[rank {rank}] reference arm: rank 0 alone runs the oracle")
         return 0
     import oracle
     A, B, extra = make_workload(args.config)
     of, tot = oracle.flop(A, B)
-    ps = np.r_[0, np.cumsum(of)]
     nthreads = os.cpu_count() or 1
-    # size each step to ~2 s of CPU so the whole run stays within minutes
-    r1 = min(A.nrows, int(np.searchsorted(ps, max(1, tot // 100))) + 1)
+    # each step = the oracle on a seeded random row sample sized to ~2 s of
+    # CPU, so the whole run stays within minutes (calibrated: best of 3)
+    frac = 0.002
+    sub, f, k = row_sample(A, of, frac)
     cal = []
-    for _ in range(3):  # calibration: best of 3 (first calls pay library / thread start-up)
+    for _ in range(3):
         t0 = time.perf_counter()
-        oracle.spgemm(A, B, 0, r1, nthreads=nthreads)
+        oracle.spgemm(sub, B, nthreads=nthreads)
         cal.append(time.perf_counter() - t0)
-    rate = max(int(ps[r1]), 1) / max(min(cal), 1e-6)
-    r_end = min(A.nrows, int(np.searchsorted(ps, min(tot, int(rate * 2.0)))) + 1)
-    f = int(ps[r_end])
+    rate = max(f, 1) / max(min(cal), 1e-6)
+    frac = min(1.0, frac * max(1.0, 2.0 * rate / max(f, 1)) if f else 1.0)
+    sub, f, k = row_sample(A, of, frac)
     for _ in range(args.warmup):
-        oracle.spgemm(A, B, 0, r_end, nthreads=nthreads)
+        oracle.spgemm(sub, B, nthreads=nthreads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.spgemm(A, B, 0, r_end, nthreads=nthreads)
+        oracle.spgemm(sub, B, nthreads=nthreads)
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
     val = 2 * f / (ms * 1e-3) / 1e9
-    sample = f"rows [0, {r_end}) of {A.nrows}: {f} of {tot} flop per step"
+    sample = (f"{k} of {A.nrows} rows drawn uniformly at random (seed 2024): {f} of {tot} flop "
+              f"per step, OpenMP over rows")
     out = {"impl": "reference", "metric": METRIC, "value": val,
-           "unit": "GFLOPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "unit": "GFLOPS", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": args.config, "sorted": True, "flop_total": tot},
@@ -282,6 +301,7 @@ def run_ours(args):
 
     # ---- inputs (host, seeded) -> HBM; B broadcast from rank 0 over NCCL
     t0 = time.perf_counter()
+    A = B = extra = None
     if rank == 0 or world == 1:
         A, B, extra = make_workload(args.config)
     log(f"[rank {rank}] workload {args.config} generated in {time.perf_counter() - t0:.1f}s")
@@ -340,7 +360,7 @@ def run_ours(args):
         C = spg.spgemm(Aloc, dB, sorted=sorted_out, ctx=ctx)
         return C
 
-    def timed(sorted_out, k, profile=False):
+    def timed(sorted_out, k, profile=False, keep=False):
         s = torch.cuda.current_stream()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(k)]
@@ -360,8 +380,11 @@ def run_ours(args):
             ev[i][0].record(s)
             out = step(sorted_out)
             ev[i][1].record(s)
-            if i == k - 1 and out is not None and not isinstance(out, (int, float)):
-                last = out.row_ptr               # keep only the final row_ptr (C can be >100 GB)
+            if i == k - 1:
+                if keep or out is None or isinstance(out, (int, float)):
+                    last = out                   # the final C (parity check) or count
+                else:
+                    last = out.row_ptr           # keep only the final row_ptr (C can be >100 GB)
             del out
         torch.cuda.synchronize()
         if world > 1:
@@ -385,33 +408,53 @@ def run_ours(args):
     for _ in range(args.warmup):
         step(True)
         step(False)
-    ms_sorted, launches, _, Cs = timed(True, args.steps)
-    ms_unsorted, _, _, _ = timed(False, args.steps)
+    ms_sorted, launches, _, last_sorted = timed(True, args.steps, keep=True)
+    # parity of the timed run's own output vs the oracle (outside the timed region)
+    parity = (bench_parity(args, A, B, last_sorted, tri, world, rank, dev, r0, r1)
+              if not args.no_parity else None)
+    Cs = last_sorted.row_ptr if (last_sorted is not None and not tri) else None
+    del last_sorted
+    torch.cuda.empty_cache()
+    ms_unsorted, _, _, last_unsorted = timed(False, args.steps)
     ms_fused = None
     if tri:
         step("fused")
-        ms_fused, _, _, _ = timed("fused", args.steps)
+        ms_fused, _, _, last_fused = timed("fused", args.steps)
         step("fused_deg")
-        ms_fused_deg, _, _, _ = timed("fused_deg", args.steps)
+        ms_fused_deg, _, _, last_fdeg = timed("fused_deg", args.steps)
+        counts = torch.tensor([float(last_unsorted), float(last_fused), float(last_fdeg)],
+                              dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(counts)
+        if parity is not None:
+            parity["triangles_unsorted_fused_degree"] = [int(round(x / 2)) for x in counts.tolist()]
+            parity["ok"] = parity["ok"] and all(
+                int(round(x / 2)) == parity["oracle_triangles"] for x in counts.tolist())
     clk = clocks.stop()
 
     # ---- per-kernel attribution: a separate profiled pass (outside the timed
     # steps) on a ctx whose bins run on one stream, so each kernel's events
     # bracket only that kernel
     recs = []
-    if rank == 0 and not tri:
+    if rank == 0:
         os.environ["SPG_SERIAL_BINS"] = "1"
         pctx = spg.Context(local)
         os.environ.pop("SPG_SERIAL_BINS")
-        spg.spgemm(Aloc, dB, sorted=True, ctx=pctx)
+
+        def prof_step():
+            if tri:  # the headline C5 step: row blocks of C = L*U, each masked by G
+                return spg.triangle_count_rows(dA, dB, dG, r0, r1, sorted=True, ctx=pctx)
+            return spg.spgemm(Aloc, dB, sorted=True, ctx=pctx)
+        out = prof_step()
+        del out
         nprof = max(1, min(args.steps, 3))
         torch.cuda.synchronize()
         _lib.spg_profile_reset(pctx.handle)
         _lib.spg_profile_enable(pctx.handle, True)
         for i in range(nprof):
             flush.fill_(i)
-            C = spg.spgemm(Aloc, dB, sorted=True, ctx=pctx)
-            del C
+            out = prof_step()
+            del out
         torch.cuda.synchronize()
         _lib.spg_profile_enable(pctx.handle, False)
         recs = _lib.spg_profile_records(pctx.handle)
@@ -426,7 +469,8 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (live per-launch events, sorted run)
     roof = None
-    if rank == 0 and recs and not tri:
+    nnz_rank0 = None
+    if rank == 0 and recs:
         agg = {}
         for n, t in recs:
             a = agg.setdefault(n, [0.0, 0])
@@ -436,10 +480,13 @@ def run_ours(args):
         tot_ms, cnt = agg[top]
         avg_ms = tot_ms / cnt
         a_nnz = np.diff(A.row_ptr)[r0:r1]
-        # per-row flop from the library's plan (last symbolic = last sorted step)
-        spg.spg_symbolic(Aloc, dB, ctx_attr)
+        # per-row flop and nnz(c_i) from the library's symbolic phase of the
+        # rank's whole row range (C5: C itself is only formed in row blocks)
+        rp_all, _, _ = spg.spg_symbolic(Aloc, dB, ctx_attr)
         f_row = spg.plan_export(ctx_attr, r1 - r0)[0].cpu().numpy()
-        c_nnz = np.diff(Cs.cpu().numpy()) if Cs is not None else np.zeros(r1 - r0, np.int64)
+        c_nnz = np.diff(rp_all.cpu().numpy())
+        nnz_rank0 = int(c_nnz.sum())
+        del rp_all
         byts = kernel_bytes(top, a_nnz, f_row, c_nnz, r1 - r0, int(a_nnz.sum()), dB.ncols, dB.nrows)
         launches_per_step = cnt / prof_steps
         if byts is not None:
@@ -447,13 +494,16 @@ def run_ours(args):
         peak, peak_src = measured_peak()
         step_ms_serial = sum(t for _, t in recs) / prof_steps
         step_share = tot_ms / prof_steps / step_ms_serial
-        roof = {"bound": "hbm", "kernel": top, "achieved": (byts / (avg_ms * 1e-3) / 1e9) if byts else None,
+        roof = {"bound": "hbm", "kernel": top,
+                "bytes_model": "numeric kernels: sum over their rows of 16 + 12 nnz(a_i) + 12 flop_i "
+                               "+ 12 nnz(c_i) (A row, gathered B rows, C row); DESIGN.md section 3", "achieved": (byts / (avg_ms * 1e-3) / 1e9) if byts else None,
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": (byts / (avg_ms * 1e-3) / 1e9 / peak) if byts else None,
                 "traffic": ncu_traffic(args.config, top), "algorithmic_bytes_per_launch": byts,
                 "avg_launch_ms": avg_ms, "launches_per_step": launches_per_step,
                 "share_of_step": step_share,
-                "attribution": f"separate profiled pass, {prof_steps} sorted steps, bins on one stream "
+                "attribution": f"separate profiled pass, {prof_steps} sorted steps, bins on one stream, "
+                               "per-launch CUDA events on the launching stream "
                                "(share = kernel time / sum of the step's kernel times)",
                 "kernels_ms_per_step": {n: v[0] / prof_steps for n, v in sorted(agg.items(), key=lambda x: -x[1][0])}}
 
@@ -464,6 +514,8 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(t)
         nnzC = int(t.item())
+    if tri and world == 1:
+        nnzC = nnz_rank0  # (C5: from the symbolic phase; C is only formed in row blocks)
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -499,6 +551,7 @@ def run_ours(args):
             "hbm_roofline_frac_step": (mb / (ms_sorted * 1e-3) / 1e9 / (world * measured_peak()[0]))
                                       if mb else None,
             "gpu_launches": launches,
+            "parity": parity,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -509,6 +562,73 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def bench_parity(args, A, B, out, tri, world, rank, dev, r0, r1):
+    """Checks the timed run's own output against the oracle, outside the
+    timed region.  C = A*B configs (rank 0's row block): sampled rows (the 8
+    heaviest + 120 drawn at random, seeded) of the last sorted C vs the
+    oracle's rows -- structure bit-exact, strictly increasing columns, values
+    within 1e-12 relative.  C5: the job's triangle count (sum over ranks) vs
+    the oracle's count in tests/golden/full_configs.json (written by
+    tools/oracle_goldens.py, which calls only oracle/)."""
+    import torch
+    import torch.distributed as dist
+    if tri:
+        cnt = torch.tensor([float(out)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(cnt)
+        if rank != 0:
+            return None
+        try:
+            gold = json.load(open(os.path.join(ROOT, "tests", "golden", "full_configs.json")))
+            want = int(gold[args.config]["triangles"])
+        except Exception:
+            want = None
+        got = int(round(cnt.item() / 2))
+        return {"what": "triangle count of the timed run (sum over ranks / 2) vs the oracle's "
+                        "(tests/golden/full_configs.json)",
+                "triangles": got, "oracle_triangles": want, "ok": want is not None and got == want}
+    if rank != 0 or out is None:
+        return None
+    import oracle
+    import synth
+    of, _ = oracle.flop(A, B)
+    m = r1 - r0
+    rng = np.random.default_rng(77)
+    f_loc = of[r0:r1]
+    nz = np.nonzero(f_loc)[0]
+    heavy = np.argsort(f_loc)[::-1][:8]
+    rnd = rng.choice(nz, size=min(120, len(nz)), replace=False) if len(nz) else np.zeros(0, np.int64)
+    rows = np.unique(np.r_[heavy, rnd]).astype(np.int64)
+    rows = rows[rows < m]
+    lens = np.diff(A.row_ptr)[r0 + rows]
+    rp = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    idx = np.repeat(A.row_ptr[r0 + rows] - rp[:-1], lens) + np.arange(int(rp[-1]), dtype=np.int64)
+    sub = synth.CSR(len(rows), A.ncols, rp, A.col[idx].astype(np.int32), A.val[idx])
+    o_rp, o_col, o_val = oracle.spgemm(sub, B)
+    g_rp = out.row_ptr.cpu().numpy()
+    ok, worst, nent = True, 0.0, 0
+    for q, r in enumerate(rows):
+        s, e = int(g_rp[r]), int(g_rp[r + 1])
+        os_, oe = int(o_rp[q]), int(o_rp[q + 1])
+        gc = out.col[s:e].cpu().numpy()
+        gv = out.val[s:e].cpu().numpy()
+        oc, ov = o_col[os_:oe], o_val[os_:oe]
+        if e - s != oe - os_ or not np.array_equal(gc, oc):
+            ok = False
+            continue
+        if len(gc) > 1 and not (np.diff(gc.astype(np.int64)) > 0).all():
+            ok = False
+        rel = np.abs(gv - ov) / np.maximum(np.abs(ov), 1e-300)
+        if len(rel):
+            worst = max(worst, float(rel.max()))
+        nent += len(gc)
+    ok = ok and worst <= 1e-12
+    return {"what": "sampled rows of the last timed sorted C (rank 0's block) vs the oracle",
+            "rows_checked": int(len(rows)), "entries_checked": int(nent),
+            "max_rel_err": worst, "ok": bool(ok)}
 
 
 def e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total):
@@ -589,6 +709,22 @@ def e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri,
             "timing": "max over ranks of per-rank device events; bytes summed over ranks"}
 
 
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-launch this
+    script as N ranks (one process per GPU) with torch.distributed.run on
+    127.0.0.1 and return its exit code (rank 0 prints the JSON line)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    log("self-launch: " + " ".join(cmd))
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -600,10 +736,16 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        log(f"--gpus {args.gpus} but WORLD_SIZE={world}: the job runs {world} rank(s)")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

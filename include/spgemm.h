@@ -78,6 +78,8 @@ typedef struct {
     int64_t max_row_nnz;    /* max_i nnz(c_i*)                                  */
     int64_t sym_bin_rows[12]; /* rows per symbolic bin    */
     int64_t num_bin_rows[12]; /* rows per numeric bin                           */
+    int64_t heap_rows;      /* rows the heap tier takes when sorted output is
+                               requested (spg_set_accumulator)                  */
 } spg_info;
 
 spg_status spg_ctx_create(spg_ctx **ctx, spg_alloc_fn alloc, spg_free_fn free_fn,
@@ -140,6 +142,25 @@ spg_status spg_numeric(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
                        const int64_t *C_row_ptr, int32_t *C_col_idx, double *C_val,
                        int sorted, void *stream);
 
+/* Accumulator of the rows of C when SORTED output is requested (PAPER.md
+ * §4.2.3 Heap SpGEMM P:340-352 and the cost model of §4.2.4 P:358-366;
+ * SURVEY.md §8(f) row 4).  Takes effect at the next spg_symbolic (the plan
+ * records which rows go where).
+ *   SPG_ACCUM_AUTO (default): a row of the warp tiers (nnz(c_i) <= 512) with
+ *       nnz(a_i) <= 16, flop_i <= 2048 and sorted B rows is merged by a
+ *       per-thread heap when T_heap = flop_i log2 nnz(a_i) (Eq:heap_est) is
+ *       below T_hash = flop_i c + nnz(c_i) log2 nnz(c_i) (Eq:hash_est), else
+ *       hashed and sorted;
+ *   SPG_ACCUM_HASH: every row hashed (the heap tier never runs);
+ *   SPG_ACCUM_HEAP: every row eligible as above is merged by the heap.
+ *   collision_factor: c of Eq:hash_est, >= 1 (default 1.3, the measured
+ *       average probes of the warp-tier tables).
+ * Unsorted output always uses the hash tiers.  Errors: SPG_ERR_INVALID_ARG. */
+#define SPG_ACCUM_AUTO 0
+#define SPG_ACCUM_HASH 1
+#define SPG_ACCUM_HEAP 2
+spg_status spg_set_accumulator(spg_ctx *ctx, int accum, double collision_factor);
+
 /* Summary of the last spg_symbolic on this ctx (host struct). */
 spg_status spg_get_info(const spg_ctx *ctx, spg_info *info);
 
@@ -163,9 +184,10 @@ spg_status spg_rows_to_parts(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
                              void *stream);
 
 /* Masked sum for triangle counting (Sec 5.6; BASELINE config 5):
- * sum over stored C(i,j) with (i,j) in pattern(G) of C(i,j), accumulated in
- * fp64 and rounded to the nearest int64 (exact for integer-valued C below
- * 2^53, e.g. the wedge counts of L*U).  C and G rows may be in any column
+ * sum over stored C(i,j) with (i,j) in pattern(G) of C(i,j).  Every warp sums
+ * its entries in fp64; the warp partials are reduced in int64 (exact) when
+ * each is an integer below 2^53 -- integer-valued C such as the wedge counts
+ * of L*U -- otherwise *sum is the fp64 total rounded to the nearest int64.  C and G rows may be in any column
  * order (G rows sorted ascending when G.ncols > 1.6M: binary search); row i
  * of C is row g_row_begin + i of G.  G's row is an smem hash set (short rows)
  * or bitmap (long rows) probed by every C entry.  Result to HOST *sum
@@ -186,6 +208,16 @@ spg_status spg_mask_sum(spg_ctx *ctx, const spg_csr *C, const spg_csr *G,
  *   sum  : host out.  Synchronizes `stream`. */
 spg_status spg_masked_sum(spg_ctx *ctx, const spg_csr *A, const spg_csr *B, const spg_csr *G,
                           int64_t g_row_begin, double *sum, void *stream);
+
+/* The same fused masked sum reduced EXACTLY in int64 (SURVEY.md §8(a) a9:
+ * triangle counts are integers): every warp's fp64 partial must be an integer
+ * below 2^53 (integer-valued A and B, e.g. L and U with values 1.0), and the
+ * partials are added as int64.  *sum: host out.  SPG_ERR_OVERFLOW if some
+ * partial is not such an integer (non-integer inputs).  Synchronizes
+ * `stream`. */
+spg_status spg_masked_sum_int(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
+                              const spg_csr *G, int64_t g_row_begin, int64_t *sum,
+                              void *stream);
 
 /* Degree-ascending relabelling for triangle counting (Sec 5.6,
  * "we reorder rows with increasing number of nonzeros.  The algorithm

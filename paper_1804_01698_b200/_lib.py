@@ -23,7 +23,7 @@ EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_co
            "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
            "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel",
-           "spg_probe_stats")
+           "spg_probe_stats", "spg_masked_sum_int", "spg_set_accumulator")
 
 
 class spg_csr(ct.Structure):
@@ -34,7 +34,8 @@ class spg_csr(ct.Structure):
 class spg_info(ct.Structure):
     _fields_ = [("nrows", ct.c_int64), ("flop_total", ct.c_int64), ("nnz_total", ct.c_int64),
                 ("max_row_flop", ct.c_int64), ("max_row_nnz", ct.c_int64),
-                ("sym_bin_rows", ct.c_int64 * 12), ("num_bin_rows", ct.c_int64 * 12)]
+                ("sym_bin_rows", ct.c_int64 * 12), ("num_bin_rows", ct.c_int64 * 12),
+                ("heap_rows", ct.c_int64)]
 
 
 class SpgError(RuntimeError):
@@ -78,6 +79,8 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_profile_record.argtypes = [vp, i64, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_float)]
     lib.spg_debug_counters.argtypes = [vp, i64p, vp]
     lib.spg_masked_sum.argtypes = [vp, csrp, csrp, csrp, i64, ct.POINTER(ct.c_double), vp]
+    lib.spg_masked_sum_int.argtypes = [vp, csrp, csrp, csrp, i64, i64p, vp]
+    lib.spg_set_accumulator.argtypes = [vp, ct.c_int, ct.c_double]
     lib.spg_degree_relabel.argtypes = [vp, csrp] + [vp] * 11
     lib.spg_probe_stats.argtypes = [vp, csrp, csrp, vp, i64p, vp]
     for name in EXPORTS:
@@ -128,7 +131,8 @@ def spg_get_info(ctx: int) -> dict:
     _check(ctx, "spg_get_info", load().spg_get_info(ctx, ct.byref(info)))
     return {"nrows": info.nrows, "flop_total": info.flop_total, "nnz_total": info.nnz_total,
             "max_row_flop": info.max_row_flop, "max_row_nnz": info.max_row_nnz,
-            "sym_bin_rows": list(info.sym_bin_rows), "num_bin_rows": list(info.num_bin_rows)}
+            "sym_bin_rows": list(info.sym_bin_rows), "num_bin_rows": list(info.num_bin_rows),
+            "heap_rows": info.heap_rows}
 
 
 def spg_plan_export(ctx: int, flop_out: int, tsize_out: int, stream: int) -> None:
@@ -188,6 +192,23 @@ def spg_masked_sum(ctx: int, A: spg_csr, B: spg_csr, G: spg_csr, g_row_begin: in
     _check(ctx, "spg_masked_sum",
            load().spg_masked_sum(ctx, ct.byref(A), ct.byref(B), ct.byref(G), g_row_begin,
                                  ct.byref(out), stream))
+    return out.value
+
+
+ACCUM = {"auto": 0, "hash": 1, "heap": 2}
+
+
+def spg_set_accumulator(ctx: int, accum: str = "auto", collision_factor: float = 1.3) -> None:
+    _check(ctx, "spg_set_accumulator",
+           load().spg_set_accumulator(ctx, ACCUM[accum], float(collision_factor)))
+
+
+def spg_masked_sum_int(ctx: int, A: spg_csr, B: spg_csr, G: spg_csr, g_row_begin: int,
+                       stream: int) -> int:
+    out = ct.c_int64(0)
+    _check(ctx, "spg_masked_sum_int",
+           load().spg_masked_sum_int(ctx, ct.byref(A), ct.byref(B), ct.byref(G), g_row_begin,
+                                     ct.byref(out), stream))
     return out.value
 
 

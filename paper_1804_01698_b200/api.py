@@ -79,6 +79,11 @@ class Context:
                 pass
             self.handle = None
 
+    def set_accumulator(self, accum: str = "auto", collision_factor: float = 1.3) -> None:
+        """Sorted-output accumulator: "auto" (cost model Eq:heap_est vs
+        Eq:hash_est per row), "hash" or "heap" (§4.2.3)."""
+        _lib.spg_set_accumulator(self.handle, accum, collision_factor)
+
     @property
     def launches(self) -> int:
         return _lib.spg_launch_count(self.handle)
@@ -169,14 +174,23 @@ def masked_sum(A: DeviceCSR, B: DeviceCSR, G: DeviceCSR, g_row_begin: int = 0,
     return _lib.spg_masked_sum(ctx.handle, A.c(), B.c(), G.c(), g_row_begin, _stream())
 
 
+def masked_sum_int(A: DeviceCSR, B: DeviceCSR, G: DeviceCSR, g_row_begin: int = 0,
+                   ctx: Context | None = None) -> int:
+    """The same sum reduced exactly in int64 (integer-valued inputs, e.g. the
+    triangle count's L*U with values 1.0); raises SpgError (OVERFLOW) if the
+    inputs are not integer-valued."""
+    ctx = ctx or default_context()
+    return _lib.spg_masked_sum_int(ctx.handle, A.c(), B.c(), G.c(), g_row_begin, _stream())
+
+
 def triangle_count_fused(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR,
                          ctx: Context | None = None) -> int:
     """Triangles = sum(L*U o G)/2 with the mask fused into the product (C is
-    never formed); values must be 1.0 (BASELINE config 5)."""
-    s = masked_sum(L, U, G, 0, ctx)
-    t = int(round(s))
-    if t != s or t % 2:
-        raise RuntimeError(f"masked sum {s!r} is not an even integer")
+    never formed), reduced in int64; values must be integers (BASELINE
+    config 5: 1.0)."""
+    t = masked_sum_int(L, U, G, 0, ctx)
+    if t % 2:
+        raise RuntimeError(f"masked sum {t} is odd: G is not symmetric")
     return t // 2
 
 

@@ -26,6 +26,20 @@ constexpr int kMaskWarpKeys = 256;             // G rows up to this size: warp t
 constexpr int kMaskWarpT = 4 * kMaskWarpKeys;  // warp hash-set slots (load <= 1/4: most
                                                // probes miss, and a miss walks to an empty slot)
 
+// Final reduction of one warp's fp64 partial (lane 0): into the fp64 sum and,
+// exactly, into an int64 sum (triangle counts are reduced in int64, SURVEY
+// §8(a) a9).  The int64 sum is exact when every partial is an integer below
+// 2^53 in magnitude (then the fp64 partial itself was exact: integer-valued
+// inputs); any other partial flags it inexact.
+__device__ __forceinline__ void mask_reduce(double acc, PlanInfo *info) {
+  if (acc == 0.0) return;
+  atomicAdd(&info->mask_acc, acc);
+  if (acc == rint(acc) && fabs(acc) < 9007199254740992.0)
+    atomicAdd(&info->mask_isum, (unsigned long long)(long long)acc);
+  else
+    atomicOr(&info->mask_inexact, 1ull);
+}
+
 // probe-only lookup in a warp-private smem hash set (no insertion)
 __device__ __forceinline__ bool set_contains(const uint32_t *tab, uint32_t c, int logT) {
   const uint32_t mask = (1u << logT) - 1u;
@@ -74,7 +88,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_mask_sum_warp(DevCSR A, DevCSR B
                                                               const int32_t *__restrict__ list,
                                                               const unsigned long long *nlist,
                                                               unsigned long long *row_counter,
-                                                              double *sum) {
+                                                              PlanInfo *info) {
   __shared__ uint32_t s_tab[WARPS][kMaskWarpT];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_tab[w];
@@ -109,7 +123,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_mask_sum_warp(DevCSR A, DevCSR B
     __syncwarp();
   }
   acc = warp_sum(acc);
-  if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
+  if (lane == 0) mask_reduce(acc, info);
 }
 
 template <int THREADS>
@@ -118,7 +132,7 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
                                                             const int32_t *__restrict__ list,
                                                             const unsigned long long *nlist,
                                                             unsigned long long *row_counter,
-                                                            double *sum, int use_bitmap) {
+                                                            PlanInfo *info, int use_bitmap) {
   extern __shared__ uint32_t s_bm[];
   __shared__ long long s_row;
   __shared__ double s_acc[THREADS / 32];
@@ -186,7 +200,7 @@ __global__ void __launch_bounds__(THREADS) k_mask_sum_block(DevCSR A, DevCSR B, 
     __syncthreads();
   }
   acc = warp_sum(acc);
-  if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
+  if (lane == 0) mask_reduce(acc, info);
 }
 
 // ---------------------------------------------------------------------------
@@ -202,7 +216,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevC
                                                                   const int32_t *__restrict__ list,
                                                                   const unsigned long long *nlist,
                                                                   unsigned long long *row_counter,
-                                                                  double *sum) {
+                                                                  PlanInfo *info) {
   __shared__ uint32_t s_tab[WARPS][kMaskWarpT];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_tab[w];
@@ -252,7 +266,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_csr_mask_sum_warp(DevCSR C, DevC
     __syncwarp();
   }
   acc = warp_sum(acc);
-  if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
+  if (lane == 0) mask_reduce(acc, info);
 }
 
 template <int THREADS>
@@ -261,7 +275,7 @@ __global__ void __launch_bounds__(THREADS) k_csr_mask_sum_block(DevCSR C, DevCSR
                                                                 const int32_t *__restrict__ list,
                                                                 const unsigned long long *nlist,
                                                                 unsigned long long *row_counter,
-                                                                double *sum, int use_bitmap) {
+                                                                PlanInfo *info, int use_bitmap) {
   extern __shared__ uint32_t s_bm[];
   __shared__ long long s_row;
   const int lane = threadIdx.x & 31;
@@ -322,7 +336,7 @@ __global__ void __launch_bounds__(THREADS) k_csr_mask_sum_block(DevCSR C, DevCSR
     __syncthreads();
   }
   acc = warp_sum(acc);
-  if (lane == 0 && acc != 0.0) atomicAdd(sum, acc);
+  if (lane == 0) mask_reduce(acc, info);
 }
 
 }  // namespace spg

@@ -261,6 +261,122 @@ __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Heap tier (§4.2.3 "Heap SpGEMM"):
+// one THREAD per row of C.  "To construct c_i*, a heap of size nnz(a_i*) is
+// allocated.  For every nonzero a_ik, the first nonzero entry in b_k* along
+// with its column index is inserted into the heap.  The algorithm iteratively
+// extracts an entry with the minimum column index from the heap, accumulates
+// it to c_i*, and inserts the next nonzero entry from the last extracted row
+// of B into the heap".  The heap lives in shared memory,
+// interleaved by thread (entry e of thread t at [e * T + t]: conflict-free);
+// key = column << 32 | entry index, so equal columns leave the heap in the
+// stored order of their a_ik and every c_ij is summed in the oracle's
+// canonical order with separate multiply and add roundings (bit-exact).
+// Output is produced in ascending column order (no sort) straight into C at
+// C_row_ptr[i] -- the symbolic phase fixed nnz(c_i).  Needs sorted B rows;
+// rows are chosen by heap_pick (cost model Eq:heap_est vs Eq:hash_est).
+// ---------------------------------------------------------------------------
+struct HeapSegs {
+  long long off[2];  // first row-list position of the heap rows of bins W256, W1024
+  long long n[2];
+};
+
+template <int T>
+__global__ void __launch_bounds__(T) k_num_heap(const int32_t *__restrict__ rows, HeapSegs segs,
+                                                DevCSR A, DevCSR B,
+                                                const int64_t *__restrict__ c_rp,
+                                                int32_t *__restrict__ c_col,
+                                                double *__restrict__ c_val) {
+  extern __shared__ unsigned long long s_heap[];
+  unsigned long long *hk = s_heap;                                         // heap keys
+  long long *hp = reinterpret_cast<long long *>(s_heap + kHeapMax * T);    // head position
+  long long *he = hp + kHeapMax * T;                                       // end of the B row
+  double *ha = reinterpret_cast<double *>(he + kHeapMax * T);              // a_ik
+  double *hb = ha + kHeapMax * T;                                          // head value b_kj
+  const int t = threadIdx.x;
+#define SPG_H(arr, e) arr[(e) * T + t]
+  const long long total = segs.n[0] + segs.n[1];
+  for (long long r = int64_t(blockIdx.x) * T + t; r < total; r += int64_t(gridDim.x) * T) {
+    const int i = r < segs.n[0] ? rows[segs.off[0] + r] : rows[segs.off[1] + (r - segs.n[0])];
+    const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    int n = 0;
+    for (int64_t q = as; q < ae; ++q) {  // insert the head of every nonempty b_k*
+      const int k = __ldg(A.col + q);
+      const int64_t bs = __ldg(B.rp + k), be = __ldg(B.rp + k + 1);
+      if (bs >= be) continue;
+      const int j = n++;
+      SPG_H(hp, j) = bs;
+      SPG_H(he, j) = be;
+      SPG_H(ha, j) = __ldg(A.val + q);
+      SPG_H(hb, j) = __ldg(B.val + bs);
+      const unsigned long long key = (unsigned long long)(uint32_t)__ldg(B.col + bs) << 32 | (unsigned)j;
+      int pos = j;  // sift up
+      while (pos > 0) {
+        const int par = (pos - 1) >> 1;
+        const unsigned long long kp = SPG_H(hk, par);
+        if (kp <= key) break;
+        SPG_H(hk, pos) = kp;
+        pos = par;
+      }
+      SPG_H(hk, pos) = key;
+    }
+    int64_t out = c_rp[i];
+    long long cur = -1;
+    double acc = 0.0;
+    while (n > 0) {
+      const unsigned long long top = SPG_H(hk, 0);
+      const int j = (int)(top & 0xFFFFu);
+      const long long c = (long long)(top >> 32);
+      const double v = __dmul_rn(SPG_H(ha, j), SPG_H(hb, j));  // a_ik * b_kj (Fig:code_spgemm l.5)
+      if (c == cur) {
+        acc = __dadd_rn(acc, v);  // accumulate to c_i*
+      } else {
+        if (cur >= 0) {
+          c_col[out] = (int32_t)cur;
+          c_val[out] = acc;
+          ++out;
+        }
+        cur = c;
+        acc = v;
+      }
+      // next entry of the extracted B row replaces the top, else the last leaf does
+      const long long p = SPG_H(hp, j) + 1;
+      unsigned long long key;
+      if (p < SPG_H(he, j)) {
+        SPG_H(hp, j) = p;
+        SPG_H(hb, j) = __ldg(B.val + p);
+        key = (unsigned long long)(uint32_t)__ldg(B.col + p) << 32 | (unsigned)j;
+      } else {
+        --n;
+        key = SPG_H(hk, n);
+      }
+      int pos = 0;  // sift down
+      while (true) {
+        const int l = 2 * pos + 1;
+        if (l >= n) break;
+        int m = l;
+        unsigned long long km = SPG_H(hk, l);
+        if (l + 1 < n) {
+          const unsigned long long kr = SPG_H(hk, l + 1);
+          if (kr < km) { m = l + 1; km = kr; }
+        }
+        if (km >= key) break;
+        SPG_H(hk, pos) = km;
+        pos = m;
+      }
+      if (n > 0) SPG_H(hk, pos) = key;
+    }
+    if (cur >= 0) {
+      c_col[out] = (int32_t)cur;
+      c_val[out] = acc;
+    }
+  }
+#undef SPG_H
+}
+constexpr int kHeapThreads = 64;
+constexpr size_t kHeapSmem = size_t(kHeapMax) * kHeapThreads * 40;
+
 // Block-wide unordered compaction of occupied slots of a table into C row.
 __device__ __forceinline__ void block_emit_unsorted(const uint32_t *keys, const double *vals,
                                                     int64_t T, int64_t rp0, int32_t *c_col,
@@ -596,18 +712,37 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 
 // ---------------------------------------------------------------------------
 // G tier, column-tile parts (B rows sorted; parts from the BM symbolic, tile
-// offsets from k_tile_offsets).  Every part is an independent work item taken
-// from a global counter: the part's products are, for each a_ik of the row,
-// the segment [toff[k][t0], toff[k][t1]) of B row k (two loads, no search).
-// A single-tile part accumulates into a dense smem window of kTileCols values
-// + an occupancy bitmap (sorted by construction); a multi-tile part (<=
-// kTPartKeys keys) into an smem hash table with an insertion list, emitted in
-// list order, or bucket-sorted (a7).  The row's a_ik are staged kTEnt at a
-// time; products are enumerated in flat rounds of 32 (owner entry by a window
-// search of the prefix of segment lengths).  Output position: C_row_ptr[i] +
-// keys of the row before the part.  No global atomics.
+// offsets from k_tile_offsets).  The blocked SPA the paper cites for long
+// rows, on one SM per part: a long row of C is cut into PARTS =
+// column ranges [t0, t1) of 8192-column tiles (one tile holding > kTPartKeys
+// keys, or a run of tiles holding <= kTPartKeys), and every part is an
+// independent work item taken from a global counter.  The part's products
+// are, for each a_ik of the row, the segment [toff[t0][k], toff[t1][k]) of B
+// row k (two loads from the TILE-MAJOR offset table, no search).
+//
+// Parts are processed in the order (dense parts, then hash parts; tile t0
+// ascending), so the tile-major offsets of one tile column (4 bytes per B
+// row) and the B entries of that tile stay L2-resident while its parts run.
+//
+// Per part, the row's a_ik are staged kTEnt at a time and split by segment
+// length:
+//   * long segments (>= kTLongSeg products): warp-sequential rounds, a round
+//     = 32 consecutive products of ONE segment (distinct columns, full lanes);
+//   * short segments: flattened rounds of 32 consecutive products of the
+//     compacted short list (owner entry from a window of segment starts).
+// Both lists are cut into contiguous round ranges, one per warp.
+// Accumulation (Fig:hash_spgemm numeric; Fig:code_spgemm l.8):
+//   * single-tile part: dense smem window of kTileCols fp64 + an occupancy
+//     bitmap; emitted in column order (sorted by construction) with the slots
+//     reset on the way (the window is zeroed once per block);
+//   * multi-tile part: chunked smem hash of 4096 slots + an
+//     insertion list; emitted in list order, or sorted by a bitmap rank over
+//     the part's span / a bucket sort (a7).
+// Output position: C_row_ptr[i] + keys of the row before the part.  No global
+// atomics besides the part counter.
 // ---------------------------------------------------------------------------
 constexpr int kTEnt = 1024;                 // a_ik staged per chunk
+constexpr int kTLongSeg = 16;               // segments of >= this many products run warp-sequential
 constexpr int kTPartLogT = 12;
 constexpr int kTPartT = 1 << kTPartLogT;      // hash slots of a multi-tile part
 static_assert(4 * kTPartKeys <= 3 * kTPartT, "multi-tile part: load <= 3/4");
@@ -615,42 +750,70 @@ constexpr int64_t kTRankCols = int64_t(32) * kTileCols;  // sorted emit by bitma
 constexpr size_t kTDenseBytes = size_t(kTileCols) * 8 + size_t(kTileCols) / 8;
 constexpr size_t kTHashBytes = size_t(kTPartT) * 12 + size_t(kTPartKeys) * 2;
 constexpr size_t kTUnion = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;
-constexpr size_t kTEntBytes = size_t(kTPartKeys) * 12 > 24576 ? size_t(kTPartKeys) * 12 : 24576;
-                                            // es i64 + ea f64 + epre i32 [kTEnt(+1)]; sorted gather
-static_assert(size_t(kTEnt) * 20 + 4 <= kTEntBytes, "entry stage");
+// entry stage (byte offsets): short list es i32 / ea f64 / epre i32[+1];
+// long list ls i32 / ll i32 (length) / la f64 / lpre i32[+1] (round prefix)
+constexpr size_t kOffEa = 0;
+constexpr size_t kOffLa = kOffEa + size_t(kTEnt) * 8;
+constexpr size_t kOffEs = kOffLa + size_t(kTEnt) * 8;
+constexpr size_t kOffLs = kOffEs + size_t(kTEnt) * 4;
+constexpr size_t kOffLl = kOffLs + size_t(kTEnt) * 4;
+constexpr size_t kOffEpre = kOffLl + size_t(kTEnt) * 4;
+constexpr size_t kOffLpre = kOffEpre + size_t(kTEnt + 4) * 4;
+constexpr size_t kTEntBytes = kOffLpre + size_t(kTEnt + 4) * 4;
 static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
-static_assert(kTEnt <= 32 * 32, "for_tpart_rounds: 32-ary owner search");
+static_assert(kTEnt <= 32 * 32, "32-ary owner search");
 
-// Rounds [g0, g1) of 32 consecutive products of the staged entries (all
-// NONEMPTY: segment of entry j = [es[j], es[j] + pre[j+1] - pre[j]) of B,
-// multiplier ea[j], pre strictly increasing, pre[n] = P).  The owner entry of
+// last j < n with pre[j] <= x (pre[0] = 0 <= x, pre nondecreasing, n <= 1024):
+// a 32-ary search, two ballots over strided then consecutive entries
+__device__ __forceinline__ int tpart_find(const int32_t *pre, int n, int x) {
+  const int lane = lane_id();
+  const int c1 = lane * 32;
+  const unsigned b1 = __ballot_sync(kFull, c1 < n && pre[c1] <= x);
+  const int blk = 31 - __clz(b1);
+  const int c2 = blk * 32 + lane;
+  const unsigned b2 = __ballot_sync(kFull, c2 < n && pre[c2] <= x);
+  return blk * 32 + 31 - __clz(b2);
+}
+
+// fp64 add into shared memory with the native 64-bit CAS (ATOMS.CAS.64; an
+// atomicAdd(double) on shared memory is a CAS loop on sm_100a anyway, with a
+// load before its first attempt).  The first attempt assumes the slot still
+// holds +0.0 (a first touch: one round trip, storing v itself); on a mismatch
+// the returned value seeds the loop.  Returns true when the slot held +0.0
+// bits (a first touch, or an exactly-zero partial sum: idempotent for the
+// caller's occupancy bit).
+__device__ __forceinline__ bool smem_add_f64_cas(double *addr, double v) {
+  unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
+  unsigned long long old = atomicCAS(a, 0ull, (unsigned long long)__double_as_longlong(v));
+  if (old == 0ull) return true;
+  while (true) {
+    const unsigned long long nw =
+        (unsigned long long)__double_as_longlong(__longlong_as_double((long long)old) + v);
+    const unsigned long long r = atomicCAS(a, old, nw);
+    if (r == old) return false;
+    old = r;
+  }
+}
+
+// Rounds [g0, g1) of 32 consecutive products of the staged SHORT entries (all
+// nonempty: products [pre[j], pre[j+1]) (pre[n] = P implied) are the
+// segment [es[j], ...) of B, multiplier ea[j], pre strictly increasing).  The owner entry of
 // product x is tracked per warp: `cur` owns the round's first product; the
 // <= 32 entries that start inside the round are found from a window of the
 // next 32 entry starts (one smem load per lane), their start positions
 // OR-ed into a 32-bit mask, and lane t's owner = cur + (starts at or before
 // t).  Owners and gather addresses of kD rounds first, then the kD gathers,
 // then the kD updates f(active, column, a_ik * b_kj).
-template <int kD = 4, typename F>
-__device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t *es,
+template <int kD = 2, typename F>
+__device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int32_t *es,
                                                  const double *ea, const int32_t *pre, int n,
                                                  int P, int g0, int g1, F &&f) {
   if (g0 >= g1) return;
   const int lane = lane_id();
   const unsigned le = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // lanes <= this one
-  int cur;
-  {
-    // last j < n with pre[j] <= x (pre[0] = 0): a 32-ary search, two
-    // ballots over strided then consecutive starts (n <= kTEnt = 32 * 32)
-    const int x = g0 * 32;
-    const int c1 = lane * 32;
-    const unsigned b1 = __ballot_sync(kFull, c1 < n && pre[c1] <= x);
-    const int blk = 31 - __clz(b1);
-    const int c2 = blk * 32 + lane;
-    const unsigned b2 = __ballot_sync(kFull, c2 < n && pre[c2] <= x);
-    cur = blk * 32 + 31 - __clz(b2);
-  }
+  int cur = tpart_find(pre, n, g0 * 32);
   for (int g = g0; g < g1; g += kD) {
     uint32_t c[kD];
     double v[kD], a[kD];
@@ -665,7 +828,7 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t 
       const unsigned pos = __reduce_or_sync(kFull, st < x0 + 32 ? (1u << (st - x0)) : 0u);
       const int j = cur + __popc(pos & le);
       cur += __popc(__ballot_sync(kFull, st <= x0 + 32));  // owner of the next round's first product
-      q[d] = act[d] ? es[j] + (x - pre[j]) : 0;
+      q[d] = act[d] ? int64_t(es[j]) + (x - pre[j]) : 0;
       a[d] = act[d] ? ea[j] : 0.0;
     }
 #pragma unroll
@@ -678,17 +841,95 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int64_t 
   }
 }
 
+// Rounds [g0, g1) of the staged LONG entries: entry j covers rounds
+// [lpre[j], lpre[j+1]) = ceil(ll[j] / 32) rounds; round r of entry j is the
+// products ls[j] + 32 r + lane of ONE B row segment (distinct columns).  Two
+// rounds per step (both gathers issued before either update).
+template <typename F>
+__device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *ls,
+                                                const int32_t *ll, const double *la,
+                                                const int32_t *lpre, int n, int R, int g0,
+                                                int g1, F &&f) {
+  if (g0 >= g1) return;
+  const int lane = lane_id();
+  int cur = tpart_find(lpre, n, g0);
+  int rbeg = lpre[cur], rend = cur + 1 < n ? lpre[cur + 1] : R, s0 = ls[cur], L = ll[cur];
+  double a = la[cur];
+  auto at = [&](int g, bool &act, int64_t &q, double &av) {
+    while (g >= rend) {  // warp-uniform: next entry
+      ++cur;
+      rbeg = rend;
+      rend = cur + 1 < n ? lpre[cur + 1] : R;
+      s0 = ls[cur];
+      L = ll[cur];
+      a = la[cur];
+    }
+    const int t = (g - rbeg) * 32 + lane;
+    act = t < L;
+    q = int64_t(s0) + t;
+    av = a;
+  };
+  for (int g = g0; g < g1; g += 2) {
+    bool act0, act1 = false;
+    int64_t q0, q1 = 0;
+    double a0, a1 = 0.0;
+    at(g, act0, q0, a0);
+    if (g + 1 < g1) at(g + 1, act1, q1, a1);
+    const uint32_t c0 = act0 ? (uint32_t)__ldg(B.col + q0) : 0u;
+    const double v0 = act0 ? __ldg(B.val + q0) : 0.0;
+    const uint32_t c1 = act1 ? (uint32_t)__ldg(B.col + q1) : 0u;
+    const double v1 = act1 ? __ldg(B.val + q1) : 0.0;
+    f(act0, c0, a0 * v0);  // a_ik * b_kj (Fig:code_spgemm l.5)
+    f(act1, c1, a1 * v1);
+  }
+}
+
+// Three exclusive block scans sharing their barriers (s_w: >= 3 * 33 ints).
+// No trailing barrier: the caller's next barrier protects s_w.
+__device__ __forceinline__ void block_excl_scan3(const int (&v)[3], int (&ex)[3], int (&tot)[3],
+                                                 int *s_w) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  int inc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    inc[k] = warp_incl_scan(v[k]);
+    if (lane == 31) s_w[k * 33 + w] = inc[k];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int x = lane < NW ? s_w[k * 33 + lane] : 0;
+      const int xi = warp_incl_scan(x);
+      if (lane < NW) s_w[k * 33 + lane] = xi - x;
+      if (lane == 31) s_w[k * 33 + 32] = xi;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ex[k] = s_w[k * 33 + w] + inc[k] - v[k];
+    tot[k] = s_w[k * 33 + 32];
+  }
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     DevCSR A, DevCSR B, const int64_t *__restrict__ c_rp, int32_t *__restrict__ c_col,
-    double *__restrict__ c_val, int sorted, const int2 *__restrict__ parts,
-    const int32_t *__restrict__ part_row, int64_t nparts, const int32_t *__restrict__ toff,
-    int ntiles, unsigned long long *counter, int tune, unsigned long long *dbg) {
+    double *__restrict__ c_val, int sorted, const int4 *__restrict__ parts, int64_t nparts,
+    const int32_t *__restrict__ toff, int64_t nB, unsigned long long *counter, int tune,
+    unsigned long long *dbg) {
   extern __shared__ double s_dyn_f64[];
-  __shared__ int s_warp[33], s_warp2[33];
+  __shared__ int s_warp[33];
   __shared__ int s_red[66];
-  __shared__ int s_cnt, s_next;
-  __shared__ long long s_q;
+  __shared__ int s_cnt;
+  // staging reservations, double-buffered by chunk parity: [short, long] =
+  // (entries << 32) | (products or rounds)
+  __shared__ unsigned long long s_res[2][2];
+  // the current part, prefetched at the previous part's end
+  __shared__ long long s_q, s_rp0, s_as;
+  __shared__ int4 s_P;
+  __shared__ int s_na;
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char *base = reinterpret_cast<char *>(s_dyn_f64);
@@ -698,57 +939,70 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   uint32_t *hk = reinterpret_cast<uint32_t *>(base + size_t(kTPartT) * 8);
   uint16_t *slot_of = reinterpret_cast<uint16_t *>(base + size_t(kTPartT) * 12);
   char *eb = base + kTUnion;                                              // staged entries
-  int64_t *es = reinterpret_cast<int64_t *>(eb);
-  double *ea = reinterpret_cast<double *>(eb + size_t(kTEnt) * 8);
-  int32_t *epre = reinterpret_cast<int32_t *>(eb + size_t(kTEnt) * 16);
-  if (threadIdx.x == 0) s_q = (long long)atomicAdd(counter, 1ull);
+  double *ea = reinterpret_cast<double *>(eb + kOffEa);
+  double *la = reinterpret_cast<double *>(eb + kOffLa);
+  int32_t *es = reinterpret_cast<int32_t *>(eb + kOffEs);
+  int32_t *ls = reinterpret_cast<int32_t *>(eb + kOffLs);
+  int32_t *ll = reinterpret_cast<int32_t *>(eb + kOffLl);
+  int32_t *epre = reinterpret_cast<int32_t *>(eb + kOffEpre);
+  int32_t *lpre = reinterpret_cast<int32_t *>(eb + kOffLpre);
+  // the dense window starts clean; every dense part resets what it used
+  for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
+  for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
+  // part metadata: thread 0 fetches (part, C row start, A row) ahead of use
+  auto fetch = [&](long long q) {
+    s_q = q;
+    if (q < nparts) {
+      const int4 P = parts[q];
+      s_P = P;
+      s_rp0 = c_rp[P.x];
+      const int64_t as = A.rp[P.x];
+      s_as = as;
+      s_na = (int)(A.rp[P.x + 1] - as);
+    }
+  };
+  if (threadIdx.x == 0) {
+    s_res[0][0] = s_res[0][1] = s_res[1][0] = s_res[1][1] = 0ull;
+    fetch((long long)atomicAdd(counter, 1ull));
+  }
   __syncthreads();
+  const bool instr = (tune & 8) && threadIdx.x == 0;
+  int par = 0;  // staging buffer parity (alternates per chunk)
   while (true) {
     const int64_t q = s_q;
     if (q >= nparts) break;
-    // the next part is reserved now; its index is published at the part's
-    // last barrier (the atomic's latency hides behind this part's work)
+    // the next part is reserved now (its fetch completes during this part)
     long long q_next = 0;
     if (threadIdx.x == 0) q_next = (long long)atomicAdd(counter, 1ull);
-    const int i = part_row[q];
-    const int2 P = parts[q];
-    const int64_t rp0 = c_rp[i];
-    const int nnz_i = (int)(c_rp[i + 1] - rp0);
-    const bool has_next = q + 1 < nparts && part_row[q + 1] == i;
-    const int2 N = has_next ? parts[q + 1] : make_int2(0, nnz_i);
-    const int t0 = P.x >> kTileLog, t1 = has_next ? (N.x >> kTileLog) : ntiles;
-    const int64_t lo = P.x;
-    const int cnt = N.y - P.y;
+    const int4 P = s_P;
+    const int t0 = P.y & 0xFFFF, t1 = P.y >> 16;
+    const int cnt = P.w;
     const bool dense = t1 == t0 + 1;
-    const bool instr = (tune & 8) && threadIdx.x == 0;
+    const int64_t rp0 = s_rp0, as = s_as;
+    const int na = s_na;
+    const int64_t lo = int64_t(t0) << kTileLog;
     const long long c0 = instr ? clock64() : 0;
     long long c_stage = 0, c_rounds = 0;
     unsigned long long prods = 0;
     const int logT = dense ? 0 : min(num_log2(cnt), kTPartLogT);
     const int T = 1 << logT;
-    if (dense) {
-      for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
-      for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
-    } else {
+    if (!dense)
       for (int s = threadIdx.x; s < T; s += THREADS) { hk[s] = kEmpty; hv[s] = 0.0; }
-    }
-    if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
-    const int64_t as = A.rp[i];
-    const int na = (int)(A.rp[i + 1] - as);
-    auto acc = [&](bool act, uint32_t c, double v) {
-      if (dense) {
-        if (act) {
-          const uint32_t off = c - (uint32_t)lo;
-          atomicAdd(dv + off, v);  // c_ij <- c_ij + value (l.8), dense window
-          atomicOr(dbm + (off >> 5), 1u << (off & 31u));
-        }
-        return;
+    if (threadIdx.x == 0) s_cnt = 0;
+    const int32_t *tk0 = toff + int64_t(t0) * nB, *tk1 = toff + int64_t(t1) * nB;
+    auto acc_dense = [&](bool act, uint32_t c, double v) {
+      if (act) {
+        const uint32_t off = c - (uint32_t)lo;
+        if (smem_add_f64_cas(dv + off, v))  // c_ij <- c_ij + value (l.8), dense window
+          atomicOr(dbm + (off >> 5), 1u << (off & 31u));  // first touch: occupied
       }
+    };
+    auto acc_hash = [&](bool act, uint32_t c, double v) {
       bool isnew = false;
       uint32_t slot = 0;
       if (act) {
         slot = probe_chunk(hk, c, logT, &isnew);
-        atomicAdd(hv + slot, v);  // c_ij <- c_ij + value (l.8)
+        smem_add_f64_cas(hv + slot, v);  // c_ij <- c_ij + value (l.8)
       }
       const unsigned m = __ballot_sync(kFull, isnew);
       if (m) {
@@ -762,71 +1016,107 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     for (int cb = 0; cb < na; cb += kTEnt) {
       const int n = min(kTEnt, na - cb);
       __syncthreads();  // table init / the previous chunk's rounds are done
+      // (the other parity's reservations were last read before this barrier)
+      if (threadIdx.x == 0) s_res[par ^ 1][0] = s_res[par ^ 1][1] = 0ull;
       const long long ca = instr ? clock64() : 0;
-      // stage: thread owns entries [t*per, t*per + per), per <= 2; the
-      // entries with a nonempty segment in the part's tiles are compacted
-      // (the round owner search needs strictly increasing starts)
+      // stage: thread owns entries [t*per, t*per + per), per <= 2; entries
+      // with a nonempty segment in [t0, t1) go to the short or the long
+      // list.  Each warp reserves its slots with one packed (entries,
+      // products/rounds) atomic per list, so within a list the products /
+      // rounds prefix increases with the slot (round owner searches)
       constexpr int kPer = (kTEnt + THREADS - 1) / THREADS;
       const int per = (n + THREADS - 1) / THREADS;
       const int jlo = min(n, (int)threadIdx.x * per), jhi = min(n, jlo + per);
-      int mine = 0, mine_n = 0;
-      int Ls[kPer];
-      int s0s[kPer];
+      int Ls[kPer], s0s[kPer];
       double avs[kPer];
+      unsigned long long vS = 0, vL = 0;  // (entries << 32) | products (short) / rounds (long)
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         const int j = jlo + u;
         Ls[u] = 0;
         if (j < jhi) {
           const int k = __ldg(A.col + as + cb + j);
-          const int32_t *tk = toff + int64_t(k) * (ntiles + 1);
-          const int s0 = __ldg(tk + t0), e0 = __ldg(tk + t1);
+          const int s0 = __ldg(tk0 + k), e0 = __ldg(tk1 + k);
           s0s[u] = s0;
           Ls[u] = e0 - s0;
           avs[u] = __ldg(A.val + as + cb + j);
-          mine += e0 - s0;
-          mine_n += e0 > s0;
+          if (Ls[u] >= kTLongSeg) vL += (1ull << 32) | (unsigned long long)((Ls[u] + 31) >> 5);
+          else if (Ls[u] > 0) vS += (1ull << 32) | (unsigned long long)Ls[u];
         }
       }
-      int Pn, nn, exn;
-      int ex = block_excl_scan_int2(mine, mine_n, s_warp, s_warp2, &Pn, &nn, &exn);  // (barriers)
+      unsigned long long iS = vS, iL = vL;  // warp inclusive scans
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long tS = __shfl_up_sync(kFull, iS, o), tL = __shfl_up_sync(kFull, iL, o);
+        if (lane >= o) { iS += tS; iL += tL; }
+      }
+      unsigned long long bS = 0, bL = 0;
+      if (lane == 31) {
+        if (iS) bS = atomicAdd(&s_res[par][0], iS);
+        if (iL) bL = atomicAdd(&s_res[par][1], iL);
+      }
+      bS = __shfl_sync(kFull, bS, 31) + iS - vS;
+      bL = __shfl_sync(kFull, bL, 31) + iL - vL;
+      int xs = (int)(bS >> 32), xp = (int)(bS & 0xFFFFFFFFu);
+      int xl = (int)(bL >> 32), xr = (int)(bL & 0xFFFFFFFFu);
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        if (Ls[u] > 0) {
-          es[exn] = s0s[u];
-          ea[exn] = avs[u];
-          epre[exn] = ex;
-          ++exn;
-          ex += Ls[u];
+        if (Ls[u] >= kTLongSeg) {
+          ls[xl] = s0s[u];
+          ll[xl] = Ls[u];
+          la[xl] = avs[u];
+          lpre[xl] = xr;
+          xr += (Ls[u] + 31) >> 5;
+          ++xl;
+        } else if (Ls[u] > 0) {
+          es[xs] = s0s[u];
+          ea[xs] = avs[u];
+          epre[xs] = xp;
+          xp += Ls[u];
+          ++xs;
         }
       }
-      if (threadIdx.x == 0) epre[nn] = Pn;
+      if (tune & 8) {  // (measurement: products of the long segments)
+        unsigned long long lp = 0;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) lp += Ls[u] >= kTLongSeg ? (unsigned long long)Ls[u] : 0ull;
+        if (lp) atomicAdd(dbg + (dense ? 12 : 13), lp);
+      }
       __syncthreads();
+      const unsigned long long tS = s_res[par][0], tL = s_res[par][1];
+      par ^= 1;
+      const int nS = (int)(tS >> 32), PS = (int)(tS & 0xFFFFFFFFu);
+      const int nL = (int)(tL >> 32), RL = (int)(tL & 0xFFFFFFFFu);
       const long long cbk = instr ? clock64() : 0;
-      const int R = (Pn + 31) >> 5;
-      for_tpart_rounds<2>(B, es, ea, epre, nn, Pn, (int)((int64_t)R * w / NW),
-                          (int)((int64_t)R * (w + 1) / NW), acc);
+      const int RS = (PS + 31) >> 5;
+      const int gs0 = (int)((int64_t)RS * w / NW), gs1 = (int)((int64_t)RS * (w + 1) / NW);
+      const int gl0 = (int)((int64_t)RL * w / NW), gl1 = (int)((int64_t)RL * (w + 1) / NW);
+      if (dense) {
+        for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_dense);
+        for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_dense);
+      } else {
+        for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_hash);
+        for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_hash);
+      }
       if (instr) {
         c_stage += cbk - ca;
         c_rounds += clock64() - cbk;  // (thread 0's own rounds; the barrier wait lands in the next stage)
-        prods += (unsigned long long)Pn;
+        prods += (unsigned long long)PS;
       }
     }
     __syncthreads();
     const long long ce = instr ? clock64() : 0;
-    const int64_t out = rp0 + P.y;
-    if (tune & 16) {
-      // measurement only (C left unwritten): no emit
-    } else if (dense) {
+    const int64_t out = rp0 + P.z;
+    if (dense) {
       // keys before each 32-column word (block scan of the word popcounts),
       // then a warp per word: lane l emits column 32 qw + l if present
-      // (coalesced stores, ascending columns)
+      // (coalesced stores, ascending columns) and resets its slot
       static_assert(kTileCols / 32 <= THREADS, "one word per thread");
       int32_t *wcum = reinterpret_cast<int32_t *>(eb);
       const int nwd = kTileCols / 32;
       const int pc = (int)threadIdx.x < nwd ? __popc(dbm[threadIdx.x]) : 0;
-      int tot;
-      const int wx = block_excl_scan_int(pc, s_warp, &tot);
+      int totw;
+      const int wx = block_excl_scan_int(pc, s_warp, &totw);
       if ((int)threadIdx.x < nwd) wcum[threadIdx.x] = wx;
       __syncthreads();
       for (int qw = w; qw < nwd; qw += NW) {
@@ -835,7 +1125,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
           const int64_t o = out + wcum[qw] + __popc(word & ((1u << lane) - 1u));
           c_col[o] = (int32_t)(lo + qw * 32 + lane);
           c_val[o] = dv[qw * 32 + lane];
+          dv[qw * 32 + lane] = 0.0;
         }
+        __syncwarp();
+        if (lane == 0) dbm[qw] = 0u;
       }
     } else if (!sorted) {
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
@@ -844,8 +1137,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         c_val[out + p] = hv[s];
       }
     } else {
-      // gather the pairs into the entry stage, bucket-sort them with the
-      // table region as scratch
+      // gather the pairs into the entry stage, sort them with the table
+      // region as scratch
       uint32_t *gk = reinterpret_cast<uint32_t *>(eb);
       double *gv = reinterpret_cast<double *>(eb + size_t(kTPartKeys) * 4);
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
@@ -862,7 +1155,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         uint32_t *rbm = reinterpret_cast<uint32_t *>(base);
         int32_t *rpre = reinterpret_cast<int32_t *>(base + size_t(kTRankCols / 32) * 4);
         const int nw = (int)(span >> 5);
-        for (int q = threadIdx.x; q < nw; q += THREADS) rbm[q] = 0u;
+        for (int q2 = threadIdx.x; q2 < nw; q2 += THREADS) rbm[q2] = 0u;
         __syncthreads();
         for (int p = threadIdx.x; p < cnt; p += THREADS) {
           const uint32_t off = gk[p] - (uint32_t)lo;
@@ -872,12 +1165,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         const int per = (nw + THREADS - 1) / THREADS;
         const int q0 = min(nw, (int)threadIdx.x * per), q1 = min(nw, q0 + per);
         int mine = 0;
-        for (int q = q0; q < q1; ++q) mine += __popc(rbm[q]);
-        int tot;
-        int ex = block_excl_scan_int(mine, s_warp, &tot);
-        for (int q = q0; q < q1; ++q) {
-          rpre[q] = ex;
-          ex += __popc(rbm[q]);
+        for (int q2 = q0; q2 < q1; ++q2) mine += __popc(rbm[q2]);
+        int totr;
+        int exr = block_excl_scan_int(mine, s_warp, &totr);
+        for (int q2 = q0; q2 < q1; ++q2) {
+          rpre[q2] = exr;
+          exr += __popc(rbm[q2]);
         }
         __syncthreads();
         for (int p = threadIdx.x; p < cnt; p += THREADS) {
@@ -895,17 +1188,17 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
                              c_val, s_red);
       }
     }
-    if (threadIdx.x == 0) s_q = q_next;  // every thread has read q
+    if (threadIdx.x == 0) fetch(q_next);  // (every thread has read this part's metadata)
     __syncthreads();
     if (instr) {
       const long long cz = clock64();
       atomicAdd(dbg + 0, 1ull);
       atomicAdd(dbg + 1, (unsigned long long)dense);
       atomicAdd(dbg + (dense ? 2 : 3), (unsigned long long)(cz - c0));
-      atomicAdd(dbg + (dense ? 4 : 5), prods);
+      atomicAdd(dbg + (dense ? 4 : 5), prods);  // (short-segment products; long ones in dbg[12])
       atomicAdd(dbg + 6, (unsigned long long)c_stage);
       atomicAdd(dbg + 7, (unsigned long long)c_rounds);
-      atomicAdd(dbg + 8, (unsigned long long)(cz - ce));   // emit
+      atomicAdd(dbg + (dense ? 8 : 11), (unsigned long long)(cz - ce));   // emit
       atomicAdd(dbg + 9, (unsigned long long)na);
       atomicAdd(dbg + 10, (unsigned long long)cnt);
     }

@@ -332,34 +332,45 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
                                                      const int64_t *__restrict__ arp,
                                                      int64_t ncols, int mode, PlanInfo *info,
                                                      int32_t *__restrict__ rows_out,
-                                                     int64_t *__restrict__ row_nnz) {
-  __shared__ unsigned s_cnt[kMaxBins];
-  __shared__ unsigned long long s_base[kMaxBins];
-  if (threadIdx.x < kMaxBins) s_cnt[threadIdx.x] = 0;
+                                                     int64_t *__restrict__ row_nnz,
+                                                     const int64_t *__restrict__ flop = nullptr,
+                                                     int accum = ACC_HASH, float cfac = 1.0f) {
+  // mode 1: rows the heap tier takes (heap_pick) go to the BACK of their
+  // bin's segment, the others to the front
+  __shared__ unsigned s_cnt[kMaxBins], s_hcnt[kMaxBins];
+  __shared__ unsigned long long s_base[kMaxBins], s_hbase[kMaxBins];
+  if (threadIdx.x < kMaxBins) { s_cnt[threadIdx.x] = 0; s_hcnt[threadIdx.x] = 0; }
   __syncthreads();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   int b = 0;
+  bool hp = false;
   unsigned local = 0;
   if (i < m) {
     if (mode == 0) {
       b = sym_bin(key[i], ncols, arp[i + 1] - arp[i]);
       if (b == SB_SKIP) row_nnz[i] = 0;
     } else {
-      b = num_bin(key[i + 1] - key[i], arp[i + 1] - arp[i]);
+      const int64_t nz = key[i + 1] - key[i], na = arp[i + 1] - arp[i];
+      b = num_bin(nz, na);
+      hp = flop != nullptr && heap_pick(b, flop[i], na, nz, accum, cfac, info->b_unsorted == 0);
     }
-    if (b != 0) local = atomicAdd(&s_cnt[b], 1u);
+    if (b != 0) local = atomicAdd(hp ? &s_hcnt[b] : &s_cnt[b], 1u);
   }
   __syncthreads();
   const int t = threadIdx.x;
-  if (t > 0 && t < kMaxBins && s_cnt[t]) {
+  if (t > 0 && t < kMaxBins && (s_cnt[t] || s_hcnt[t])) {
     const unsigned long long *cnt = mode == 0 ? info->sym_count : info->num_count;
     unsigned long long off = 0;
     for (int u = 1; u < t; ++u) off += cnt[u];
-    s_base[t] = off + atomicAdd(&(mode == 0 ? info->cursor : info->num_cursor)[t],
-                                (unsigned long long)s_cnt[t]);
+    if (s_cnt[t])
+      s_base[t] = off + atomicAdd(&(mode == 0 ? info->cursor : info->num_cursor)[t],
+                                  (unsigned long long)s_cnt[t]);
+    if (s_hcnt[t])
+      s_hbase[t] = off + cnt[t] - atomicAdd(&info->heap_cursor[t], (unsigned long long)s_hcnt[t]) -
+                   s_hcnt[t];
   }
   __syncthreads();
-  if (b != 0) rows_out[s_base[b] + local] = (int32_t)i;
+  if (b != 0) rows_out[(hp ? s_hbase[b] : s_base[b]) + local] = (int32_t)i;
 }
 
 // ---------------------------------------------------------------------------
@@ -435,11 +446,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partials(int64_t *__restr
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict__ data, int64_t n,
                                                             const int64_t *__restrict__ partial,
                                                             PlanInfo *info,
-                                                            const int64_t *__restrict__ arp) {
+                                                            const int64_t *__restrict__ arp,
+                                                            const int64_t *__restrict__ flop = nullptr,
+                                                            int accum = ACC_HASH,
+                                                            float cfac = 1.0f) {
   __shared__ long long s_warp[33];
-  __shared__ unsigned s_bins[kMaxBins];
+  __shared__ unsigned s_bins[kMaxBins], s_hbins[kMaxBins];
   __shared__ unsigned long long s_max;
-  if (threadIdx.x < kMaxBins) s_bins[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxBins) { s_bins[threadIdx.x] = 0; s_hbins[threadIdx.x] = 0; }
   if (threadIdx.x == 0) s_max = 0;
   const int64_t base = int64_t(blockIdx.x) * kScanTile + int64_t(threadIdx.x) * kScanItems;
   long long v[kScanItems];
@@ -453,10 +467,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
     mx = (unsigned long long)v[t] > mx ? (unsigned long long)v[t] : mx;
   }
   __syncthreads();
+  const bool b_sorted = info->b_unsorted == 0;
 #pragma unroll
   for (int t = 0; t < kScanItems; ++t)
-    if (arp && base + t < n && v[t] > 0)
-      atomicAdd(&s_bins[num_bin(v[t], arp[base + t + 1] - arp[base + t])], 1u);
+    if (arp && base + t < n && v[t] > 0) {
+      const int64_t na = arp[base + t + 1] - arp[base + t];
+      const int b = num_bin(v[t], na);
+      atomicAdd(&s_bins[b], 1u);
+      if (flop && heap_pick(b, flop[base + t], na, v[t], accum, cfac, b_sorted))
+        atomicAdd(&s_hbins[b], 1u);
+    }
   long long tot;
   long long ex = block_excl_scan_1024(s, s_warp, &tot) + partial[blockIdx.x];
 #pragma unroll
@@ -471,6 +491,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
   if (threadIdx.x == 0) atomicMax(&info->max_nnz, s_max);
   if (threadIdx.x > 0 && threadIdx.x < kMaxBins && s_bins[threadIdx.x])
     atomicAdd(&info->num_count[threadIdx.x], (unsigned long long)s_bins[threadIdx.x]);
+  if (threadIdx.x > 0 && threadIdx.x < kMaxBins && s_hbins[threadIdx.x])
+    atomicAdd(&info->heap_count[threadIdx.x], (unsigned long long)s_hbins[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
@@ -478,44 +500,121 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
 // the numeric G tier, which binary-search B rows.)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_check_sorted(DevCSR B, PlanInfo *info) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  bool bad = false;
-  for (int64_t i = warp; i < B.nrows && !bad; i += nwarps) {
-    const int64_t s = B.rp[i], e = B.rp[i + 1];
-    for (int64_t q = s + 1 + lane; q < e; q += 32) bad |= __ldg(B.col + q - 1) >= __ldg(B.col + q);
-    bad = __any_sync(kFull, bad);
+  // info->b_unsorted += (descents col[q-1] >= col[q] over all q) - (descents
+  // at the first entry of a nonempty row): nonzero iff some row is not
+  // strictly increasing.  Two coalesced grid-stride passes (entries, rows)
+  // instead of a warp per row.
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  const int64_t q0 = B.rp[0], q1 = B.rp[B.nrows];
+  long long d = 0;
+  for (int64_t q = q0 + 1 + tid; q < q1; q += nth) d += __ldg(B.col + q - 1) >= __ldg(B.col + q);
+  for (int64_t r = tid; r < B.nrows; r += nth) {
+    const int64_t s = B.rp[r];
+    if (s > q0 && s < B.rp[r + 1]) d -= __ldg(B.col + s - 1) >= __ldg(B.col + s);
   }
-  if (bad && lane == 0) atomicOr(&info->b_unsorted, 1ull);
+  d = warp_sum(d);
+  if ((threadIdx.x & 31) == 0 && d != 0) atomicAdd(&info->b_unsorted, (unsigned long long)d);
 }
 
 // ---------------------------------------------------------------------------
-// Column-tile offsets of B (long-row tier): toff[k*(ntiles+1) + t] = absolute
-// position of the first entry of B row k with column >= t*kTileCols (B.rp[k+1]
-// if none); needs strictly increasing rows.  Warp per row: lane l looks at
-// entry q and fills the tiles that begin after the previous entry's column and
-// at or before its own.  Positions fit int32 (checked by the host).
+// Column-tile offsets of B (long-row tier; needs strictly increasing rows;
+// positions fit int32, checked by the host).
 // ---------------------------------------------------------------------------
+// toff[t * nB + k] = first position of B row k (sorted) with column >= t *
+// kTileCols, t in [0, ntiles] (TILE-MAJOR: the parts of one tile read one
+// contiguous column of the table).  A block takes 32 consecutive B rows: a
+// warp per row, lane l lower-bounds tiles l, l + 32, ... in the row (no
+// serial walk over the tiles an entry skips) into smem, then the block
+// writes each tile's 32 offsets as one coalesced 128-byte store.
+constexpr int kToffRows = 32;
 __global__ void __launch_bounds__(256) k_tile_offsets(DevCSR B, int ntiles, int32_t *__restrict__ toff) {
-  // toff[k][t] = first position of B row k (sorted) with column >= t * kTileCols:
-  // a warp per row, lane l searches tiles l, l + 32, ... (lower bound in the
-  // row; coalesced stores, no serial walk over the tiles an entry skips)
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t k = warp; k < B.nrows; k += nwarps) {
-    const int64_t s = B.rp[k], e = B.rp[k + 1];
-    int32_t *o = toff + k * (ntiles + 1);
-    for (int t = lane; t <= ntiles; t += 32) {
-      const int64_t key = int64_t(t) << kTileLog;
-      int64_t lo = s, hi = e;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if ((int64_t)__ldg(B.col + mid) < key) lo = mid + 1; else hi = mid;
+  extern __shared__ int32_t s_toff[];  // [(ntiles + 1) * 33]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nB = B.nrows;
+  for (int64_t k0 = int64_t(blockIdx.x) * kToffRows; k0 < nB; k0 += int64_t(gridDim.x) * kToffRows) {
+    for (int kk = w; kk < kToffRows; kk += 8) {
+      const int64_t k = k0 + kk;
+      if (k >= nB) break;
+      const int64_t s = B.rp[k], e = B.rp[k + 1];
+      for (int t = lane; t <= ntiles; t += 32) {
+        const int64_t key = int64_t(t) << kTileLog;
+        int64_t lo = s, hi = e;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if ((int64_t)__ldg(B.col + mid) < key) lo = mid + 1; else hi = mid;
+        }
+        s_toff[t * 33 + kk] = (int32_t)lo;
       }
-      o[t] = (int32_t)lo;
     }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (ntiles + 1) * kToffRows; idx += blockDim.x) {
+      const int t = idx / kToffRows, kk = idx % kToffRows;
+      if (k0 + kk < nB) toff[int64_t(t) * nB + k0 + kk] = s_toff[t * 33 + kk];
+    }
+    __syncthreads();
+  }
+}
+
+// Parts in processing order: bucket = t0 for single-tile (dense-window)
+// parts, kMaxTiles + t0 for multi-tile (hash) parts; dense parts first, tile
+// ascending (see k_num_tpart).  Counting sort: per-block smem histograms
+// merged into hist[2 * kMaxTiles], one block scans it, then a scatter with a
+// per-block reservation in every bucket.
+constexpr int kPartBuckets = 2 * kMaxTiles;
+__device__ __forceinline__ int part_bucket(int4 p) {
+  const int t0 = p.y & 0xFFFF, t1 = p.y >> 16;
+  return (t1 == t0 + 1 ? 0 : kMaxTiles) + t0;
+}
+
+__global__ void __launch_bounds__(256) k_parts_hist(const int4 *__restrict__ parts,
+                                                    const PlanInfo *__restrict__ info,
+                                                    unsigned *__restrict__ hist) {
+  __shared__ unsigned h[kPartBuckets];
+  for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x) h[b] = 0u;
+  __syncthreads();
+  const int64_t n = (int64_t)info->parts_used;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&h[part_bucket(parts[p])], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x)
+    if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+__global__ void __launch_bounds__(kPartBuckets) k_parts_scan(unsigned *__restrict__ hist) {
+  __shared__ int s_w[33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int v = (int)hist[threadIdx.x];
+  const int inc = warp_incl_scan(v);
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int x = lane < kPartBuckets / 32 ? s_w[lane] : 0;
+    const int xi = warp_incl_scan(x);
+    if (lane < kPartBuckets / 32) s_w[lane] = xi - x;
+  }
+  __syncthreads();
+  hist[threadIdx.x] = (unsigned)(s_w[w] + inc - v);  // exclusive: the bucket's first slot (cursor)
+}
+
+__global__ void __launch_bounds__(256) k_parts_scatter(const int4 *__restrict__ parts,
+                                                       const PlanInfo *__restrict__ info,
+                                                       unsigned *__restrict__ cursor,
+                                                       int4 *__restrict__ out) {
+  __shared__ unsigned h[kPartBuckets];
+  for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x) h[b] = 0u;
+  __syncthreads();
+  const int64_t n = (int64_t)info->parts_used;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride)
+    atomicAdd(&h[part_bucket(parts[p])], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x)
+    if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);  // this block's first slot in bucket b
+  __syncthreads();
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride) {
+    const int4 v = parts[p];
+    out[atomicAdd(&h[part_bucket(v)], 1u)] = v;
   }
 }
 

@@ -44,7 +44,7 @@ struct PlanInfo {
   unsigned long long mask_sum;
   unsigned long long flags;
   unsigned long long max_arow;    // max nnz(a_i)
-  unsigned long long b_unsorted;  // 1 if some B row is not strictly increasing
+  unsigned long long b_unsorted;  // nonzero iff some B row is not strictly increasing
   unsigned long long parts_used;  // bump allocator of the parts buffer
   unsigned long long parts_overflow;
   unsigned long long row_counter;   // dynamic work queue of the numeric G tier
@@ -55,6 +55,10 @@ struct PlanInfo {
   unsigned long long mask_ctr[2];   // row queues of the fused mask-and-sum kernels
   double mask_acc;                  // their fp64 sum
   unsigned long long mask_n[2];     // lengths of their row lists (warp tier, block tier)
+  unsigned long long mask_isum;     // exact int64 sum of the warp partials (two's complement)
+  unsigned long long mask_inexact;  // nonzero: some warp partial was not an integer below 2^53
+  unsigned long long heap_count[kMaxBins];   // rows of each numeric bin taken by the heap tier
+  unsigned long long heap_cursor[kMaxBins];  // (scatter cursors, from the back of the bin)
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)
 };
 
@@ -135,6 +139,29 @@ __device__ __forceinline__ int num_bin(int64_t nnz, int64_t na) {
   if (n <= 10) return NB_W1024;
   if (n <= 14) return NB_B2K + (n - 11);
   return NB_G;
+}
+
+// Heap tier (§4.2.3 Heap SpGEMM):
+// with sorted output, a warp-tier row whose B rows are sorted, with nnz(a_i)
+// <= kHeapMax and flop_i <= kHeapMaxFlop, is computed by a per-thread k-way
+// heap merge when the paper's cost model says so (accumulator mode AUTO):
+//   T_heap = flop_i * log2 nnz(a_i)                          (Eq:heap_est)
+//   T_hash = flop_i * c + nnz(c_i) * log2 nnz(c_i)           (Eq:hash_est)
+// with c the collision factor (measured: DESIGN.md §9c).  Mode HASH never,
+// HEAP always (for the eligible rows).
+enum AccumMode { ACC_AUTO = 0, ACC_HASH = 1, ACC_HEAP = 2 };
+constexpr int kHeapMax = 16;
+constexpr int64_t kHeapMaxFlop = 2048;  // bounds one thread's serial merge
+
+__device__ __forceinline__ bool heap_pick(int bin, int64_t flop, int64_t na, int64_t nnz,
+                                          int accum, float cfac, bool b_sorted) {
+  if (accum == ACC_HASH || !b_sorted || nnz <= 0 || na > kHeapMax || flop > kHeapMaxFlop ||
+      (bin != NB_W256 && bin != NB_W1024))
+    return false;
+  if (accum == ACC_HEAP) return true;
+  const float th = (float)flop * log2f((float)na);
+  const float tc = (float)flop * cfac + (float)nnz * log2f((float)nnz);
+  return th < tc;
 }
 
 // Fibonacci hashing: HIGH bits of col*H (reading R5 of DESIGN.md; the paper's

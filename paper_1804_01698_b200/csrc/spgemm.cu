@@ -42,7 +42,7 @@ struct spg_ctx {
   void *user = nullptr;
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
-  Buf parts, part_row, part_n, toff;  // column-tile parts of long rows (BM tier), B tile offsets
+  Buf parts, parts2, part_hist, toff;  // column-tile parts of long rows (BM tier), sorted copy, B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
   Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (keys, ranks, unsorted rows, CUB temp)
@@ -59,6 +59,8 @@ struct spg_ctx {
   int64_t launches = 0;
   int serial = 0;  // SPG_SERIAL_BINS=1: all bins on the caller's stream (diagnosis)
   int tune = 0;    // SPG_TUNE=<bits>: kernel variant switches for A/B measurements (default 0)
+  int accum = ACC_AUTO;   // accumulator choice for sorted output (spg_set_accumulator)
+  float cfac = 1.3f;      // collision factor c of Eq:hash_est (measured)
   // optional per-launch timing (events on the stream each kernel runs on)
   int profiling = 0;
   struct Rec { const char *name; cudaEvent_t a, b; };
@@ -228,7 +230,7 @@ spg_status launch_flop(spg_ctx *c, const spg_csr *A, const spg_csr *B, int count
 
 // scan of data[0..n) in place (int64), numeric-bin counting in the last pass
 spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
-                       const int64_t *arp = nullptr) {
+                       const int64_t *arp = nullptr, const int64_t *flop = nullptr) {
   if (n == 0) return SPG_OK;
   const int64_t nb = ceil_div(n, kScanTile);
   SPG_CUDA(c, cudaGetLastError());
@@ -247,7 +249,8 @@ spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
   SPG_LAUNCHED(c, "k_scan_partials");
   {
     ProfScope _ps(c, s, "k_scan_down");
-    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p, arp);
+    k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p, arp,
+                                                      flop, c->accum, c->cfac);
   }
   SPG_LAUNCHED(c, "k_scan_down");
   return SPG_OK;
@@ -257,6 +260,18 @@ spg_status read_info(spg_ctx *c, cudaStream_t s) {
   SPG_CUDA(c, cudaMemcpyAsync(c->host_info, c->info.p, sizeof(PlanInfo), cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
   return SPG_OK;
+}
+
+// Workspace budget of the global-hash slabs: a quarter of the free device
+// memory (plus what the slab buffer already holds), at most 16 GiB.
+int64_t slab_budget(spg_ctx *c) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    free_b = size_t(1) << 32;
+  }
+  const int64_t b = int64_t(free_b / 4 + c->slab.bytes);
+  return std::min<int64_t>(b, int64_t(16) << 30);
 }
 
 int64_t bin_offset(const unsigned long long *cnt, int b) {
@@ -320,7 +335,8 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_num_tpart<512>, kTPartSmem) == SPG_OK &&
          set_smem(c, k_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_csr_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
-         set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK;
+         set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK &&
+         set_smem(c, k_num_heap<kHeapThreads>, kHeapSmem) == SPG_OK;
   }
   if (!ok) {
     cudaGetLastError();
@@ -335,7 +351,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
   if (!c) return SPG_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
   Buf *bufs[] = {&c->flop,      &c->rows_sym,  &c->rows_num,  &c->partial,   &c->slab,
-                 &c->info,      &c->scratch,   &c->parts,     &c->part_row,  &c->part_n,
+                 &c->info,      &c->scratch,   &c->parts,     &c->parts2,    &c->part_hist,
                  &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
                  &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
                  &c->rl_tmp,    &c->rl_cub,    &c->mask_rows, &c->useful_bits};
@@ -398,6 +414,7 @@ spg_status spg_get_info(const spg_ctx *c, spg_info *o) {
     o->sym_bin_rows[b] = (int64_t)p.sym_count[b];
     o->num_bin_rows[b] = (int64_t)p.num_count[b];
   }
+  o->heap_rows = (int64_t)(p.heap_count[NB_W256] + p.heap_count[NB_W1024]);
   o->sym_bin_rows[0] = c->plan_m;  // skip bin = the rest
   o->num_bin_rows[0] = c->plan_m;
   for (int b = 1; b < kMaxBins; ++b) {
@@ -448,6 +465,15 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       bnz = (const uint32_t *)c->bnz.p;
     }
     SPG_LAUNCHED(c, "k_b_rowmask");
+    // are B's rows strictly increasing?  (column-tile parts and the heap tier
+    // need it; decided on the device, also visible at the first host read)
+    {
+      ProfScope _ps(c, s, "k_check_sorted");
+      const int64_t gridc = std::min<int64_t>(ceil_div(std::max<int64_t>(B->nrows, 1), 256),
+                                              int64_t(c->num_sms) * 8);
+      k_check_sorted<<<(unsigned)std::max<int64_t>(gridc, 1), 256, 0, s>>>(dev(B), info);
+    }
+    SPG_LAUNCHED(c, "k_check_sorted");
     // a1 + a2: flop, symbolic bins (+ per-row useful a_ik counts when most B
     // rows are empty, for the pruning below)
     if ((st = buf_ensure(c, c->prune_cnt, size_t(m) * 8, s)) != SPG_OK) return st;
@@ -512,6 +538,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         h2.b_end = h.b_end;
         h2.b_empty = h.b_empty;
         h2.useful = h.useful;
+        h2.b_unsorted = h.b_unsorted;
         h2.a_nnz = (unsigned long long)nu;
         *c->host_info = h2;  // (pinned; consumed by the copy before the next read_info)
         SPG_CUDA(c, cudaMemcpyAsync(info, c->host_info, sizeof(PlanInfo), cudaMemcpyHostToDevice, s));
@@ -535,23 +562,15 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       return fail(c, SPG_ERR_OVERFLOW, "a row of B has more than 2^26 entries");
     // BM tier: is B row-sorted (column-range parts need it)?  parts buffers
     c->plan_parts = false;
-    int2 *parts = nullptr;
+    int4 *parts = nullptr;
     int64_t parts_cap = 0;
-    if (h.sym_count[SB_BM]) {
-      const int64_t gridc = std::min<int64_t>(ceil_div(B->nrows, 8), int64_t(c->num_sms) * 16);
-      {
-        ProfScope _ps(c, s, "k_check_sorted");
-        k_check_sorted<<<(unsigned)std::max<int64_t>(gridc, 1), 256, 0, s>>>(dev(B), info);
-      }
-      SPG_LAUNCHED(c, "k_check_sorted");
+    if (h.sym_count[SB_BM] && h.b_unsorted == 0) {
       // parts per row <= 2 nnz / kTPartKeys + 1 (consecutive parts hold > kTPartKeys keys)
       parts_cap = (int64_t)(2 * h.flop_total / kTPartKeys) + (int64_t)h.sym_count[SB_BM] + 16;
       const int64_t ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       parts_cap = std::min<int64_t>(parts_cap, (int64_t)h.sym_count[SB_BM] * ntiles + 16);
-      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * sizeof(int2), s)) != SPG_OK) return st;
-      if ((st = buf_ensure(c, c->part_row, size_t(parts_cap) * 4, s)) != SPG_OK) return st;
-      if ((st = buf_ensure(c, c->part_n, size_t(m) * 4, s)) != SPG_OK) return st;
-      parts = (int2 *)c->parts.p;
+      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * sizeof(int4), s)) != SPG_OK) return st;
+      parts = (int4 *)c->parts.p;
       c->plan_parts = true;
     }
     // a3: symbolic per bin, bins on concurrent internal streams
@@ -608,19 +627,22 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
           k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(
-              rb, n, a, b, flop, row_nnz, info, parts, parts_cap, (int32_t *)c->part_row.p,
-              (int32_t *)c->part_n.p);
+              rb, n, a, b, flop, row_nnz, info, parts, parts_cap);
         }
         SPG_LAUNCHED(c, "k_sym_bitmap");
       } else {  // SB_G
         {
-          const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
+          int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
           int lg = 0;
           {
             const int64_t mn = std::min<int64_t>((int64_t)h.max_flop, B->ncols);
             while ((int64_t(1) << lg) <= mn) ++lg;
           }
           const int64_t slabT = int64_t(1) << std::max(lg, kMinLogT);
+          // one table per block, sized for the largest row: cap the grid so
+          // the slabs fit the workspace budget (the kernel's row loop is
+          // grid-strided, so fewer blocks only costs time)
+          grid = std::max<int64_t>(1, std::min<int64_t>(grid, slab_budget(c) / (slabT * 4)));
           if ((st = buf_ensure(c, c->slab, size_t(grid) * size_t(slabT) * 4, s)) != SPG_OK) return st;
           {
             ProfScope _ps(c, ss, "k_sym_global<1024>");
@@ -636,12 +658,14 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     SPG_CUDA(c, cudaMemsetAsync(row_nnz, 0, size_t(m) * 8, s));
   }
   // a4: C_row_ptr = exclusive scan of row nnz (+ numeric bin counts)
-  if ((st = launch_scan(c, row_nnz, m, s, A->row_ptr)) != SPG_OK) return st;
+  if ((st = launch_scan(c, row_nnz, m, s, A->row_ptr, (const int64_t *)c->flop.p)) != SPG_OK) return st;
   if (m > 0) {
     {
       ProfScope _ps(c, s, "k_bin_scatter_num");
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, A->row_ptr, 0, 1, info,
-                                                               (int32_t *)c->rows_num.p, nullptr);
+                                                               (int32_t *)c->rows_num.p, nullptr,
+                                                               (const int64_t *)c->flop.p, c->accum,
+                                                               c->cfac);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(num)");
   }
@@ -702,26 +726,68 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       if ((st = buf_ensure(c, c->toff, size_t(B->nrows) * size_t(ntiles + 1) * 4, s)) != SPG_OK)
         return st;
-      SPG_CUDA(c, cudaMemsetAsync(&((PlanInfo *)c->info.p)->row_counter, 0, 8, s));
+      if ((st = buf_ensure(c, c->parts2, size_t(h.parts_used) * sizeof(int4), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->part_hist, size_t(kPartBuckets) * 4, s)) != SPG_OK) return st;
+      PlanInfo *dinfo = (PlanInfo *)c->info.p;
+      SPG_CUDA(c, cudaMemsetAsync(&dinfo->row_counter, 0, 8, s));
+      SPG_CUDA(c, cudaMemsetAsync(c->part_hist.p, 0, size_t(kPartBuckets) * 4, s));
       {
         ProfScope _ps(c, s, "k_tile_offsets");
-        const int64_t grid = std::min<int64_t>(ceil_div(B->nrows, 8), int64_t(c->num_sms) * 16);
-        k_tile_offsets<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, s>>>(b, (int)ntiles,
-                                                                          (int32_t *)c->toff.p);
+        const int64_t grid = std::min<int64_t>(ceil_div(B->nrows, kToffRows), int64_t(c->num_sms) * 8);
+        k_tile_offsets<<<(unsigned)std::max<int64_t>(grid, 1), 256, size_t(ntiles + 1) * 33 * 4, s>>>(
+            b, (int)ntiles, (int32_t *)c->toff.p);
       }
       SPG_LAUNCHED(c, "k_tile_offsets");
+      // parts in processing order (dense first, tile ascending)
+      const unsigned pgrid = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>(ceil_div((int64_t)h.parts_used, 256), int64_t(c->num_sms) * 4));
+      {
+        ProfScope _ps(c, s, "k_parts_hist");
+        k_parts_hist<<<pgrid, 256, 0, s>>>((const int4 *)c->parts.p, dinfo, (unsigned *)c->part_hist.p);
+      }
+      SPG_LAUNCHED(c, "k_parts_hist");
+      {
+        ProfScope _ps(c, s, "k_parts_scan");
+        k_parts_scan<<<1, kPartBuckets, 0, s>>>((unsigned *)c->part_hist.p);
+      }
+      SPG_LAUNCHED(c, "k_parts_scan");
+      {
+        ProfScope _ps(c, s, "k_parts_scatter");
+        k_parts_scatter<<<pgrid, 256, 0, s>>>((const int4 *)c->parts.p, dinfo, (unsigned *)c->part_hist.p,
+                                              (int4 *)c->parts2.p);
+      }
+      SPG_LAUNCHED(c, "k_parts_scatter");
     } else {
       g_grid = std::min<int64_t>((int64_t)h.num_count[NB_G], int64_t(c->num_sms));
       int lg = log2_ceil64(2 * h.max_nnz);
       slabT = int64_t(1) << std::max(lg, kMinLogT);
+      g_grid = std::max<int64_t>(1, std::min<int64_t>(g_grid, slab_budget(c) / (slabT * 12)));
       if ((st = buf_ensure(c, c->slab, size_t(g_grid) * size_t(slabT) * 12, s)) != SPG_OK) return st;
     }
   }
   if ((st = fork(c, s)) != SPG_OK) return st;
   int sidx = 0;
+  // heap tier (sorted output only): the rows heap_pick chose sit at the back
+  // of the W256 / W1024 bin segments
+  const bool use_heap = sorted && (h.heap_count[NB_W256] + h.heap_count[NB_W1024]) > 0;
+  if (use_heap) {
+    HeapSegs hs;
+    hs.n[0] = (long long)h.heap_count[NB_W256];
+    hs.n[1] = (long long)h.heap_count[NB_W1024];
+    hs.off[0] = bin_offset(h.num_count, NB_W256) + (long long)h.num_count[NB_W256] - hs.n[0];
+    hs.off[1] = bin_offset(h.num_count, NB_W1024) + (long long)h.num_count[NB_W1024] - hs.n[1];
+    const int64_t nh = hs.n[0] + hs.n[1];
+    cudaStream_t ss = c->serial ? s : c->sub[sidx++ % kSubStreams];
+    {
+      ProfScope _ps(c, ss, "k_num_heap<64>");
+      k_num_heap<kHeapThreads><<<(unsigned)std::min<int64_t>(ceil_div(nh, kHeapThreads), int64_t(c->num_sms) * 5),
+                                 kHeapThreads, kHeapSmem, ss>>>(rows, hs, a, b, C_row_ptr, C_col_idx, C_val);
+    }
+    SPG_LAUNCHED(c, "k_num_heap");
+  }
   // largest bins first so the long rows start early
   for (int bin = NB_COUNT - 1; bin >= 1; --bin) {
-    const int64_t n = (int64_t)h.num_count[bin];
+    const int64_t n = (int64_t)h.num_count[bin] - (use_heap ? (int64_t)h.heap_count[bin] : 0);
     if (n == 0) continue;
     const int32_t *rb = rows + bin_offset(h.num_count, bin);
     cudaStream_t ss = c->serial ? s : c->sub[sidx++ % kSubStreams];
@@ -775,10 +841,9 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       {
         ProfScope _ps(c, ss, "k_num_tpart<512>");
         k_num_tpart<512><<<(unsigned)(2 * c->num_sms), 512, kTPartSmem, ss>>>(
-            a, b, C_row_ptr, C_col_idx, C_val, sorted, (const int2 *)c->parts.p,
-            (const int32_t *)c->part_row.p, (int64_t)h.parts_used, (const int32_t *)c->toff.p,
-            (int)ntiles, &((PlanInfo *)c->info.p)->row_counter, c->tune,
-            ((PlanInfo *)c->info.p)->dbg);
+            a, b, C_row_ptr, C_col_idx, C_val, sorted, (const int4 *)c->parts2.p,
+            (int64_t)h.parts_used, (const int32_t *)c->toff.p, B->nrows,
+            &((PlanInfo *)c->info.p)->row_counter, c->tune, ((PlanInfo *)c->info.p)->dbg);
       }
       SPG_LAUNCHED(c, "k_num_tpart");
     } else {  // NB_G
@@ -793,6 +858,17 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
     }
   }
   return join(c, s);
+}
+
+spg_status spg_set_accumulator(spg_ctx *c, int accum, double collision_factor) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  if (accum < SPG_ACCUM_AUTO || accum > SPG_ACCUM_HEAP)
+    return fail(c, SPG_ERR_INVALID_ARG, "accumulator must be SPG_ACCUM_AUTO, _HASH or _HEAP");
+  if (!(collision_factor >= 1.0) || collision_factor > 1e6)
+    return fail(c, SPG_ERR_INVALID_ARG, "collision factor must be >= 1");
+  c->accum = accum;
+  c->cfac = (float)collision_factor;
+  return SPG_OK;
 }
 
 spg_status spg_debug_counters(spg_ctx *c, int64_t *out, void *stream) {
@@ -872,8 +948,8 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
   SPG_CUDA(c, cudaSetDevice(c->device));
   if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
-  // both queues, the fp64 sum and the list lengths
-  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 5 * 8, s));
+  // both queues, the fp64 sum, the list lengths, the int64 sum and its flag
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 7 * 8, s));
   if (C->nrows > 0) {
     if ((st = buf_ensure(c, c->mask_rows, size_t(C->nrows) * 8, s)) != SPG_OK) return st;
     int32_t *list_w = (int32_t *)c->mask_rows.p, *list_b = list_w + C->nrows;
@@ -886,8 +962,7 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
     {
       ProfScope _ps(c, s, "k_csr_mask_sum_warp<8>");
       k_csr_mask_sum_warp<kWarps><<<(unsigned)(c->num_sms * 8), kWarps * 32, 0, s>>>(
-          dev(C), dev(G), g_row_begin, list_w, &info->mask_n[0], &info->mask_ctr[0],
-          &info->mask_acc);
+          dev(C), dev(G), g_row_begin, list_w, &info->mask_n[0], &info->mask_ctr[0], info);
     }
     SPG_LAUNCHED(c, "k_csr_mask_sum_warp");
     const int use_bitmap = G->ncols <= kBitmapMaxCols ? 1 : 0;
@@ -895,19 +970,22 @@ spg_status spg_mask_sum(spg_ctx *c, const spg_csr *C, const spg_csr *G, int64_t 
     {
       ProfScope _ps(c, s, "k_csr_mask_sum_block<1024>");
       k_csr_mask_sum_block<1024><<<(unsigned)c->num_sms, 1024, smem, s>>>(
-          dev(C), dev(G), g_row_begin, list_b, &info->mask_n[1], &info->mask_ctr[1],
-          &info->mask_acc, use_bitmap);
+          dev(C), dev(G), g_row_begin, list_b, &info->mask_n[1], &info->mask_ctr[1], info,
+          use_bitmap);
     }
     SPG_LAUNCHED(c, "k_csr_mask_sum_block");
   }
-  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 5 * 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
-  *sum = (int64_t)llround(c->host_info->mask_acc);
+  // exact int64 reduction for integer-valued C (triangle counts); else the
+  // fp64 sum rounded
+  *sum = c->host_info->mask_inexact ? (int64_t)llround(c->host_info->mask_acc)
+                                    : (int64_t)c->host_info->mask_isum;
   return SPG_OK;
 }
 
-spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const spg_csr *G,
-                          int64_t g_row_begin, double *sum, void *stream) {
+static spg_status masked_sum_impl(spg_ctx *c, const spg_csr *A, const spg_csr *B, const spg_csr *G,
+                                  int64_t g_row_begin, double *sum, int64_t *isum, void *stream) {
   if (!c) return SPG_ERR_INVALID_ARG;
   spg_status st;
   if ((st = check_csr(c, A, "A", true)) != SPG_OK) return st;
@@ -915,13 +993,13 @@ spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const 
   if ((st = check_csr(c, G, "G", false)) != SPG_OK) return st;
   if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
   if (G->ncols != B->ncols) return fail(c, SPG_ERR_DIM_MISMATCH, "G.ncols != B.ncols");
-  if (!sum || g_row_begin < 0 || g_row_begin + A->nrows > G->nrows)
+  if ((!sum && !isum) || g_row_begin < 0 || g_row_begin + A->nrows > G->nrows)
     return fail(c, SPG_ERR_INVALID_ARG, "bad mask row range or NULL sum");
   cudaStream_t s = (cudaStream_t)stream;
   SPG_CUDA(c, cudaSetDevice(c->device));
   if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
-  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 5 * 8, s));  // queues, sum, list lengths
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 7 * 8, s));  // queues, sums, list lengths, flag
   if (A->nrows > 0 && B->nrows > 0) {
     DevCSR a = dev(A), b = dev(B), g = dev(G);
     if ((st = buf_ensure(c, c->mask_rows, size_t(A->nrows) * 8, s)) != SPG_OK) return st;
@@ -935,7 +1013,7 @@ spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const 
     {
       ProfScope _ps(c, s, "k_mask_sum_warp<8>");
       k_mask_sum_warp<kWarps><<<(unsigned)(c->num_sms * 8), kWarps * 32, 0, s>>>(
-          a, b, g, g_row_begin, list_w, &info->mask_n[0], &info->mask_ctr[0], &info->mask_acc);
+          a, b, g, g_row_begin, list_w, &info->mask_n[0], &info->mask_ctr[0], info);
     }
     SPG_LAUNCHED(c, "k_mask_sum_warp");
     const int use_bitmap = B->ncols <= kBitmapMaxCols ? 1 : 0;
@@ -943,16 +1021,36 @@ spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const 
     {
       ProfScope _ps(c, s, "k_mask_sum_block<1024>");
       k_mask_sum_block<1024><<<(unsigned)c->num_sms, 1024, smem, s>>>(
-          a, b, g, g_row_begin, list_b, &info->mask_n[1], &info->mask_ctr[1], &info->mask_acc,
-          use_bitmap);
+          a, b, g, g_row_begin, list_b, &info->mask_n[1], &info->mask_ctr[1], info, use_bitmap);
     }
     SPG_LAUNCHED(c, "k_mask_sum_block");
   }
-  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaMemcpyAsync(&c->host_info->mask_acc, &info->mask_acc, 5 * 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
-  *sum = c->host_info->mask_acc;
+  if (sum) *sum = c->host_info->mask_acc;
+  if (isum) {
+    if (c->host_info->mask_inexact)
+      return fail(c, SPG_ERR_OVERFLOW,
+                  "masked sum is not an exact integer (non-integer values or a partial >= 2^53)");
+    *isum = (int64_t)c->host_info->mask_isum;
+  }
   return SPG_OK;
 }
+
+spg_status spg_masked_sum(spg_ctx *c, const spg_csr *A, const spg_csr *B, const spg_csr *G,
+                          int64_t g_row_begin, double *sum, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  if (!sum) return fail(c, SPG_ERR_INVALID_ARG, "NULL sum");
+  return masked_sum_impl(c, A, B, G, g_row_begin, sum, nullptr, stream);
+}
+
+spg_status spg_masked_sum_int(spg_ctx *c, const spg_csr *A, const spg_csr *B, const spg_csr *G,
+                              int64_t g_row_begin, int64_t *sum, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  if (!sum) return fail(c, SPG_ERR_INVALID_ARG, "NULL sum");
+  return masked_sum_impl(c, A, B, G, g_row_begin, nullptr, sum, stream);
+}
+
 
 spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64_t *L_rp,
                               int32_t *L_col, double *L_val, int64_t *U_rp, int32_t *U_col,

@@ -464,26 +464,24 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
 // sorted it also cuts rows with nnz > kPartMinKeys into column-tile parts for
-// the numeric G tier (spg_internal.cuh): part = (first column = first tile *
-// kTileCols, keys of the row before it), its row id in part_row, the row's
-// part count in part_n.
+// the numeric G tier (spg_internal.cuh): part = int4 {row, first tile | end
+// tile << 16, keys of the row before the part, keys in the part}.
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restrict__ rows,
                                                         int64_t nrows, DevCSR A, DevCSR B,
                                                         const int64_t *__restrict__ flop,
                                                         int64_t *__restrict__ row_nnz,
-                                                        PlanInfo *info, int2 *__restrict__ parts,
-                                                        int64_t parts_cap,
-                                                        int32_t *__restrict__ part_row,
-                                                        int32_t *__restrict__ part_n) {
+                                                        PlanInfo *info, int4 *__restrict__ parts,
+                                                        int64_t parts_cap) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
   __shared__ DeferList s_dl;  // long B rows walked by the whole block
   __shared__ long long s_pbase;
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
-  __shared__ int s_cut[kMaxTiles];       // first tile of each part
+  __shared__ int s_cut[kMaxTiles];       // first | (end tile << 16) of each part
+  __shared__ int s_nne[kMaxTiles + 1];   // first nonempty tile at or after each tile
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwords = (int)((B.ncols + 31) >> 5);
@@ -537,34 +535,41 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     if (want_parts && nnz > kPartMinKeys) {
       // parts: greedy runs of consecutive tiles holding <= kTPartKeys keys; a
       // tile holding more stands alone (dense window in the numeric phase).
-      // The greedy run starting at tile t ends before u(t), found by a search
-      // of the tile prefix P = s_tile: x = first x >= t + 2 with P(x) > P(t) +
-      // kTPartKeys; u = x - 1, or x when tiles t .. x - 2 are empty (the
-      // greedy run never cuts before its first key).  One thread per tile,
-      // then the chain 0 -> u(0) -> ... (one step per part).
+      // Runs start at nonempty tiles only.  With the tile prefix P = s_tile:
+      //   u(t)   = end of the greedy run starting at t = x - 1 for the first
+      //            x >= t + 2 with P(x) > P(t) + kTPartKeys (else ntiles), so a
+      //            run of >= 2 tiles never holds more than kTPartKeys keys;
+      //   nne(t) = first nonempty tile >= t (first x > t with P(x) > P(t),
+      //            minus one; ntiles if none).
+      // One thread per tile, then the chain nne(0) -> nne(u(.)) -> ... (one
+      // step per part).
       int *s_nxt = s_tcnt;  // (tile counts are consumed)
-      for (int t = threadIdx.x; t < ntiles; t += THREADS) {
+      for (int t = threadIdx.x; t <= ntiles; t += THREADS) {
+        if (t == ntiles) { s_nne[t] = ntiles; continue; }
         const int lim = s_tile[t] + kTPartKeys;
         int lo = t + 2, hi = ntiles + 1;  // first x in [t + 2, ntiles] with P(x) > lim, else ntiles + 1
         while (lo < hi) {
           const int m = (lo + hi) >> 1;
           if (s_tile[m] > lim) hi = m; else lo = m + 1;
         }
-        int u = lo - 1;
-        if (lo <= ntiles && s_tile[lo - 1] == s_tile[t]) u = lo;
-        s_nxt[t] = u > ntiles ? ntiles : u;
+        s_nxt[t] = min(lo - 1, ntiles);
+        const int p0 = s_tile[t];
+        lo = t + 1, hi = ntiles + 1;  // first x in [t + 1, ntiles] with P(x) > P(t)
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (s_tile[m] > p0) hi = m; else lo = m + 1;
+        }
+        s_nne[t] = lo - 1;  // (ntiles when no key at or after t)
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         int np = 0;
-        for (int t = 0; t < ntiles; t = s_nxt[t]) s_cut[np++] = t;
+        for (int t = s_nne[0]; t < ntiles; t = s_nne[s_nxt[t]]) s_cut[np++] = t | (s_nxt[t] << 16);
         const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
         if (base + np > parts_cap) {
           atomicAdd(&info->parts_overflow, 1ull);
-          part_n[i] = 0;
           s_cnt = -1;
         } else {
-          part_n[i] = np;
           s_cnt = np;
           s_pbase = base;
         }
@@ -572,11 +577,9 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       __syncthreads();
       const int np = s_cnt;
       for (int p = threadIdx.x; p < np; p += THREADS) {
-        parts[s_pbase + p] = make_int2(s_cut[p] << kTileLog, s_tile[s_cut[p]]);
-        part_row[s_pbase + p] = i;
+        const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
+        parts[s_pbase + p] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
       }
-    } else if (threadIdx.x == 0 && part_n != nullptr) {
-      part_n[i] = 0;  // no parts: a B-tier row
     }
     __syncthreads();
   }

@@ -98,13 +98,12 @@ def triangle_count_dist(L, U, G, group=None, ctx: Context | None = None,
     """Triangle count of BASELINE config 5 over the ranks: each rank counts
     sum(C o G) on its flop-balanced row block of C = L*U, then all_reduce(SUM).
     fused=True sums the masked products without forming C (spg_masked_sum)."""
-    from .api import masked_sum, triangle_count_rows
+    from .api import masked_sum_int, triangle_count_rows
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     offs, _ = partition_rows(L, U, world, ctx)
     r0, r1 = offs[rank], offs[rank + 1]
     if fused:
-        s = masked_sum(L.rows(r0, r1), U, G, r0, ctx) if r1 > r0 else 0.0
-        part = int(round(s))
+        part = masked_sum_int(L.rows(r0, r1), U, G, r0, ctx) if r1 > r0 else 0
     else:
         part = triangle_count_rows(L, U, G, r0, r1, ctx=ctx)
     t = torch.tensor([part], dtype=torch.int64, device=L.row_ptr.device)

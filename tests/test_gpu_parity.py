@@ -131,6 +131,86 @@ def test_column_parts(spg, ctx, sorted_out, shuffle):
     gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what="column parts")
 
 
+def _tile_rows(tile_keys, ntiles, seed, overlap=3):
+    """(A, B) with ONE row of A*B whose keys per 8192-column tile are exactly
+    tile_keys (column-part cutter cases); B rows sorted, each key reached from
+    1..overlap B rows (CR > 1)."""
+    rng = np.random.default_rng(seed)
+    cols = []
+    for t, kcount in enumerate(tile_keys):
+        if kcount:
+            cols.append(t * 8192 + np.sort(rng.choice(8192, size=kcount, replace=False)))
+    S = np.concatenate(cols).astype(np.int64)
+    b_rows, b_cols = [], []
+    for r in range(overlap):  # B row r holds every key with (key index % overlap) <= r
+        keep = (np.arange(len(S)) % overlap) <= r
+        b_rows.append(np.full(int(keep.sum()), r, np.int64))
+        b_cols.append(S[keep])
+    B = synth.from_coo(overlap, ntiles * 8192, np.concatenate(b_rows), np.concatenate(b_cols))
+    B = synth.with_values(B, seed + 1, 0.5, 1.5)
+    A = synth.from_coo(1, overlap, np.zeros(overlap, np.int64), np.arange(overlap))
+    A = synth.with_values(A, seed + 2, 0.5, 1.5)
+    return A, B
+
+
+@pytest.mark.parametrize("tile_keys", [
+    [0, 8192, 100],              # empty tile, then a full tile (> 4096 keys)
+    [3000, 0, 5000, 500],        # empty tile between two (the advisor's case)
+    [0, 0, 0, 6000, 0, 3000],    # leading empty tiles, heavy tile, trailing gap
+    [2000, 100, 0, 4500, 2100, 2048, 1, 0, 0, 2047],
+    [1500] * 6,                  # runs of tiles that fill a 2048-key part
+])
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_part_cutter_tile_patterns(spg, ctx, tile_keys, sorted_out):
+    """Column-tile part cuts (advisor r01 finding): a heavy tile always stands
+    alone, runs of >= 2 tiles hold <= 2048 keys, parts start at nonempty
+    tiles -- whatever the pattern of empty tiles.  Exact vs the oracle."""
+    assert sum(tile_keys) > 8192  # a long row: column-tile parts
+    A, B = _tile_rows(tile_keys, max(len(tile_keys), 8), 31)
+    gpu_vs_oracle(A, B, sorted_out, ctx=ctx, what=f"tiles {tile_keys}")
+
+
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_signed_values_cancellation(spg, ctx, sorted_out):
+    """Reading R1: numerically cancelled entries stay in the structure.  Rows
+    of A pick pairs of B rows with equal patterns and equal values, with a_ik
+    = +x and -x, so those entries of C sum to exactly 0.0 (two terms, any
+    order) and must still be present.  Other entries mix signs: values within
+    1e-12 of the sum of |terms| (the error bound of a signed sum), computed by
+    the oracle on |A|*|B|."""
+    rng = np.random.default_rng(5)
+    n, k, m = 4000, 3000, 600
+    B0 = synth.random_sparse(k // 2, n, 0.01, 8, -1.0, 1.0)
+    # B = [B0; B0] (rows k/2 + r duplicate rows r)
+    B = synth.CSR(k, n, np.r_[B0.row_ptr, B0.row_ptr[1:] + B0.row_ptr[-1]].astype(np.int64),
+                  np.r_[B0.col, B0.col].astype(np.int32), np.r_[B0.val, B0.val])
+    rows, cols, vals = [], [], []
+    for i in range(m):
+        picks = rng.choice(k // 2, size=int(rng.integers(1, 40)), replace=False)
+        x = rng.uniform(0.5, 2.0, size=len(picks))
+        ncancel = len(picks) // 2
+        rows += [i] * (len(picks) + ncancel)
+        cols += list(picks) + list(picks[:ncancel] + k // 2)
+        vals += list(x) + list(-x[:ncancel])
+    A = synth.from_coo(m, k, np.array(rows), np.array(cols), np.array(vals))
+    import paper_1804_01698_b200 as spgm
+    dA, dB = spgm.DeviceCSR.from_host(A), spgm.DeviceCSR.from_host(B)
+    C = spgm.spgemm(dA, dB, sorted=sorted_out, ctx=ctx)
+    g_rp, g_col, g_val = C.to_host()
+    o_rp, o_col, o_val = oracle.spgemm(A, B)
+    assert np.array_equal(g_rp - g_rp[0], o_rp)
+    if not sorted_out:
+        from parity import sort_rows
+        g_col, g_val = sort_rows(g_rp, g_col, g_val)
+    assert np.array_equal(g_col, o_col)
+    absA = synth.CSR(A.nrows, A.ncols, A.row_ptr, A.col, np.abs(A.val))
+    absB = synth.CSR(B.nrows, B.ncols, B.row_ptr, B.col, np.abs(B.val))
+    _, a_col, mag = oracle.spgemm(absA, absB)
+    assert np.array_equal(a_col, o_col)
+    assert (np.abs(g_val - o_val) <= 1e-12 * mag).all()
+    assert (o_val == 0.0).sum() > 100  # cancelled entries exist and are kept
+
+
 @pytest.mark.parametrize("ncols", [1, 2, 16])
 def test_small_ncols_cap(spg, ctx, ncols):
     """min(N_col, flop) cap of the table size: large flop, tiny ncols."""
@@ -447,3 +527,99 @@ def test_c4_pruned_bitmask_growth(spg):
         A, B, _ = synth.workload("c4_tallskinny", scale=scale)
         assert A.nnz >= (1 << 20)
         gpu_vs_oracle(A, B, True, ctx=ctx, what=f"C4 s{scale} bitmask growth")
+
+
+# ------------------------------------------------------------------ heap tier
+def _heap_ctx(spg, mode):
+    c = spg.Context()
+    c.set_accumulator(mode)
+    return c
+
+
+def test_heap_tier_bitexact_c1(spg):
+    """Heap SpGEMM on C1 with the heap forced for every eligible
+    row: ascending columns by construction, and every entry summed in the
+    oracle's canonical order with separate mul/add roundings -- BIT-exact."""
+    A, B, _ = synth.workload("c1_er4096")
+    ctx = _heap_ctx(spg, "heap")
+    dA = spg.DeviceCSR.from_host(A)
+    C = spg.spgemm(dA, dA, sorted=True, ctx=ctx)
+    assert ctx.info()["heap_rows"] > 0.9 * A.nrows
+    g_rp, g_col, g_val = C.to_host()
+    o_rp, o_col, o_val = oracle.spgemm(A, B)
+    assert np.array_equal(g_rp, o_rp) and np.array_equal(g_col, o_col)
+    assert np.array_equal(g_val, o_val)  # bit-exact
+
+
+def test_heap_auto_selector_cost_model(spg):
+    """AUTO picks the heap exactly where Eq:heap_est < Eq:hash_est (P:358-366,
+    c = 1.3) among the eligible rows (warp tiers, nnz(a_i) <= 16, flop_i <=
+    2048, sorted B); C1 (low CR, short rows) goes mostly to the heap, C2's
+    stencil's interior rows (nnz(a_i) = 27) are not eligible; results exact
+    vs the oracle."""
+    for name, want_some in (("c1_er4096", True), ("c2_stencil64", False)):
+        A, B, _ = synth.workload(name, scale=None if name == "c1_er4096" else 16)
+        ctx = _heap_ctx(spg, "auto")
+        gpu_vs_oracle(A, B, True, ctx=ctx, what=f"{name} auto")
+        f, _ = oracle.flop(A, B)
+        nz = oracle.row_nnz(A, B)
+        na = np.diff(A.row_ptr)
+        two_nz = np.maximum(2 * nz, 1)
+        warp = (nz > 0) & (np.ceil(np.log2(two_nz)) <= 10) & ~((na > 512))
+        elig = warp & (na <= 16) & (f <= 2048)
+        th = f.astype(np.float32) * np.log2(np.maximum(na, 1).astype(np.float32))
+        tc = f.astype(np.float32) * np.float32(1.3) + nz.astype(np.float32) * np.log2(
+            np.maximum(nz, 1).astype(np.float32))
+        pick = elig & (th < tc)
+        near = elig & (np.abs(th - tc) <= 1e-5 * np.maximum(np.abs(tc), 1))
+        got = ctx.info()["heap_rows"]
+        assert abs(got - int(pick.sum())) <= int(near.sum()), (name, got, int(pick.sum()))
+        if want_some:
+            assert got > 0.5 * A.nrows
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_heap_tier_random_and_boundaries(spg, seed):
+    """Forced heap on random shapes (empty rows, rectangular) and on rows at
+    the eligibility edges (nnz(a_i) 16 / 17, flop 2048 / 2049): exact."""
+    rng = np.random.default_rng(100 + seed)
+    m, n, k = (int(x) for x in rng.integers(1, 400, size=3))
+    A = synth.random_sparse(m, n, float(rng.uniform(0.005, 0.05)), seed, -1.0, 1.0, empty_rows=0.2)
+    B = synth.random_sparse(n, k, float(rng.uniform(0.005, 0.1)), seed + 9, -1.0, 1.0, empty_rows=0.1)
+    ctx = _heap_ctx(spg, "heap")
+    g = spg.spgemm(spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B), sorted=True, ctx=ctx)
+    o = oracle.spgemm(A, B)
+    g_rp, g_col, g_val = g.to_host()
+    assert np.array_equal(g_rp, o[0]) and np.array_equal(g_col, o[1])
+    heap = ctx.info()["heap_rows"]
+    assert heap > 0
+    # heap rows are bit-exact, hashed rows within the signed-sum bound
+    absA = synth.CSR(A.nrows, A.ncols, A.row_ptr, A.col, np.abs(A.val))
+    absB = synth.CSR(B.nrows, B.ncols, B.row_ptr, B.col, np.abs(B.val))
+    mag = oracle.spgemm(absA, absB)[2]
+    assert (np.abs(g_val - o[2]) <= 1e-12 * mag).all()
+    # eligibility edges
+    specs = [(2048, 300), (2049, 300), (16 * 3, 16), (17 * 3, 17), (5, 5), (0, 0)]
+    A2, B2 = synth.crafted_rows(specs, 5000, 40 + seed)
+    gpu_vs_oracle(A2, B2, True, ctx=ctx, what="heap edges")
+
+
+def test_heap_never_with_unsorted_b(spg):
+    """The heap merge needs sorted B rows: with B's storage order shuffled
+    the forced heap mode must fall back to hashing (and stay exact)."""
+    A, B, _ = synth.workload("c1_er4096")
+    Bs = synth.shuffle_within_rows(B, 3)
+    ctx = _heap_ctx(spg, "heap")
+    gpu_vs_oracle(A, Bs, True, ctx=ctx, what="heap, unsorted B")
+    assert ctx.info()["heap_rows"] == 0
+    ctx.set_accumulator("auto")
+    gpu_vs_oracle(A, B, False, ctx=ctx, what="unsorted output: hash tiers")
+
+
+def test_set_accumulator_errors(spg):
+    from paper_1804_01698_b200 import _lib
+    ctx = spg.Context()
+    with pytest.raises(_lib.SpgError, match="INVALID_ARG"):
+        _lib._check(ctx.handle, "x", _lib.load().spg_set_accumulator(ctx.handle, 7, 1.3))
+    with pytest.raises(_lib.SpgError, match="INVALID_ARG"):
+        ctx.set_accumulator("auto", 0.5)
