@@ -161,6 +161,30 @@ spg_status spg_numeric(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
 #define SPG_ACCUM_HEAP 2
 spg_status spg_set_accumulator(spg_ctx *ctx, int accum, double collision_factor);
 
+/* One-phase multiply (§2, the
+ * one-phase alternative: "allocate large enough memory space for output
+ * matrix and compute").  No symbolic pass: every row's hash table is sized
+ * by the flop upper bound (lowest 2^n > min(N_col, flop_i)), the
+ * numeric kernels run on those bins with their row counts read on the device
+ * (persistent launches) and write row i into a flop-sized ctx workspace (12
+ * bytes per product, grow-only) while counting nnz(c_i); a scan gives
+ * C_row_ptr.  Blocks ONCE, for the 8-byte nnz(C) (plus a rerun when the
+ * workspace had to grow).  Then the caller allocates C and calls
+ * spg_onephase_emit, which compacts the rows into it (async).
+ *   A, B        : device CSR with values; A.ncols == B.nrows.
+ *   C_row_ptr   : device, caller-allocated int64[A.nrows + 1].
+ *   nnz_C       : host out.   flop_total: host out (may be NULL).
+ *   sorted      : 0/1 as for spg_numeric.
+ * Errors: SPG_ERR_OVERFLOW when a row needs a table beyond 8192 slots
+ * (flop_i >= 8192 and N_col >= 8192) -- use the two-phase calls for such
+ * matrices; SPG_ERR_WORKSPACE when flop * 12 bytes cannot be allocated. */
+spg_status spg_onephase(spg_ctx *ctx, const spg_csr *A, const spg_csr *B, int64_t *C_row_ptr,
+                        int64_t *nnz_C, int64_t *flop_total, int sorted, void *stream);
+/* Copies the rows of the last spg_onephase into C (C_col_idx int32[nnz_C],
+ * C_val f64[nnz_C], device, caller-allocated; NULL allowed when nnz_C = 0).
+ * Asynchronous on `stream`.  SPG_ERR_STATE without a pending spg_onephase. */
+spg_status spg_onephase_emit(spg_ctx *ctx, int32_t *C_col_idx, double *C_val, void *stream);
+
 /* Summary of the last spg_symbolic on this ctx (host struct). */
 spg_status spg_get_info(const spg_ctx *ctx, spg_info *info);
 

@@ -23,7 +23,8 @@ EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_co
            "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
            "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel",
-           "spg_probe_stats", "spg_masked_sum_int", "spg_set_accumulator")
+           "spg_probe_stats", "spg_masked_sum_int", "spg_set_accumulator", "spg_onephase",
+           "spg_onephase_emit")
 
 
 class spg_csr(ct.Structure):
@@ -81,6 +82,8 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_masked_sum.argtypes = [vp, csrp, csrp, csrp, i64, ct.POINTER(ct.c_double), vp]
     lib.spg_masked_sum_int.argtypes = [vp, csrp, csrp, csrp, i64, i64p, vp]
     lib.spg_set_accumulator.argtypes = [vp, ct.c_int, ct.c_double]
+    lib.spg_onephase.argtypes = [vp, csrp, csrp, vp, i64p, i64p, ct.c_int, vp]
+    lib.spg_onephase_emit.argtypes = [vp, vp, vp, vp]
     lib.spg_degree_relabel.argtypes = [vp, csrp] + [vp] * 11
     lib.spg_probe_stats.argtypes = [vp, csrp, csrp, vp, i64p, vp]
     for name in EXPORTS:
@@ -196,6 +199,17 @@ def spg_masked_sum(ctx: int, A: spg_csr, B: spg_csr, G: spg_csr, g_row_begin: in
 
 
 ACCUM = {"auto": 0, "hash": 1, "heap": 2}
+
+
+def spg_onephase(ctx: int, A: spg_csr, B: spg_csr, c_row_ptr: int, sorted: bool, stream: int):
+    nnz, flop = ct.c_int64(0), ct.c_int64(0)
+    _check(ctx, "spg_onephase", load().spg_onephase(ctx, ct.byref(A), ct.byref(B), c_row_ptr,
+                                                    ct.byref(nnz), ct.byref(flop), int(sorted), stream))
+    return nnz.value, flop.value
+
+
+def spg_onephase_emit(ctx: int, c_col: int, c_val: int, stream: int) -> None:
+    _check(ctx, "spg_onephase_emit", load().spg_onephase_emit(ctx, c_col, c_val, stream))
 
 
 def spg_set_accumulator(ctx: int, accum: str = "auto", collision_factor: float = 1.3) -> None:

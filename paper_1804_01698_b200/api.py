@@ -134,12 +134,33 @@ def spg_numeric(A: DeviceCSR, B: DeviceCSR, C_row_ptr: torch.Tensor, nnz: int,
     return DeviceCSR(A.nrows, B.ncols, C_row_ptr, col, val)
 
 
+def spgemm_onephase(A: DeviceCSR, B: DeviceCSR, sorted: bool = True,
+                    ctx: Context | None = None) -> DeviceCSR:
+    """C = A*B in ONE phase (tables sized by flop, no symbolic pass, one host
+    round trip).  Raises SpgError (OVERFLOW) for rows
+    with flop_i >= 8192 -- use spgemm() for those."""
+    ctx = ctx or default_context()
+    dev = A.row_ptr.device
+    rp = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
+    nnz, _ = _lib.spg_onephase(ctx.handle, A.c(), B.c(), rp.data_ptr(), sorted, _stream())
+    col = torch.empty(nnz, dtype=torch.int32, device=dev)
+    val = torch.empty(nnz, dtype=torch.float64, device=dev)
+    _lib.spg_onephase_emit(ctx.handle, col.data_ptr() if nnz else 0, val.data_ptr() if nnz else 0,
+                           _stream())
+    return DeviceCSR(A.nrows, B.ncols, rp, col, val)
+
+
 def spgemm(A: DeviceCSR, B: DeviceCSR, sorted: bool = True,
-           ctx: Context | None = None) -> DeviceCSR:
-    """C = A*B (Gustavson, hash accumulator, two phases)."""
+           ctx: Context | None = None, method: str = "two_phase") -> DeviceCSR:
+    """C = A*B (Gustavson, hash accumulator): method "two_phase"
+    (symbolic + numeric) or "one_phase" (spgemm_onephase)."""
     if A.ncols != B.nrows:
         raise ValueError(f"dimension mismatch: A is {A.nrows}x{A.ncols}, B is {B.nrows}x{B.ncols}")
     ctx = ctx or default_context()
+    if method == "one_phase":
+        return spgemm_onephase(A, B, sorted, ctx)
+    if method != "two_phase":
+        raise ValueError(f"unknown method {method!r}")
     rp, nnz, _ = spg_symbolic(A, B, ctx)
     return spg_numeric(A, B, rp, nnz, sorted, ctx)
 

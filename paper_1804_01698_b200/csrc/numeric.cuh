@@ -30,6 +30,22 @@ __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int lo
   }
 }
 
+// Bank spreading of the fp64 accumulators (shared-memory CAS adds serialise
+// per bank; measured 26 wavefronts per 32-lane ATOMS.CAST.64 on C3):
+//  * dense window: column offset -> slot off ^ (bits 4-7) ^ (bits 8-11) ^
+//    (bit 12) in the low 4 bits (a bijection on [0, 8192)); R-MAT columns
+//    have each bit set with probability 0.24, so a third of them end in
+//    0000 -- one bank pair -- without it;
+//  * hash table values: slot s of chunk c = s >> 2, position e = s & 3 lives
+//    at e * (T / 4) + c, so the first slots of the chunks (e = 0, the common
+//    case) spread over all banks instead of every fourth.
+__device__ __forceinline__ uint32_t dense_slot(uint32_t off) {
+  return off ^ (((off >> 4) ^ (off >> 8) ^ (off >> 12)) & 15u);
+}
+__device__ __forceinline__ uint32_t hash_vslot(uint32_t s, int logT) {
+  return ((s & 3u) << (logT - 2)) + (s >> 2);
+}
+
 // Lanes of a round holding the same key c combine their values into the
 // lowest such lane; returns true for the lanes that then hold a key to apply
 // (active, first of their key).  Summation order inside a round is free
@@ -216,24 +232,55 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
 // plain read-modify-write; lanes that share a key in a round (found with
 // __match_any_sync) use the atomic add.  Rounds are separated by __syncwarp.
 // ---------------------------------------------------------------------------
-template <int TMAX, int WARPS, int SORTED>
+// One-phase mode (§2, "allocate large
+// enough memory space for output matrix and compute"): the numeric kernels
+// run on the SYMBOLIC bins (table T = lowest 2^n > min(flop_i, ncols),
+// P:302-305, so no symbolic pass is needed), read their bin's row count and
+// offset from the device plan (persistent launch, no host round trip), write
+// row i at the flop prefix fofs[i] of a flop-sized workspace and record
+// nnz(c_i); a copy kernel later compacts the rows into the caller's C.
+struct OnePhase {
+  const PlanInfo *info;     // sym_count[] (device), flop_total
+  const int64_t *fofs;      // exclusive prefix of flop (workspace row offsets)
+  int64_t *row_nnz;         // out: nnz(c_i) (C_row_ptr + 1, scanned afterwards)
+  unsigned long long cap;   // workspace capacity (products); larger flop: skip
+  int bin;                  // symbolic bin this launch handles
+};
+
+// this launch's row-list offset (and *nrows); -1 when the workspace overflows
+// (the host then grows it and reruns)
+__device__ __forceinline__ long long onephase_rows(const OnePhase &op, int64_t *nrows) {
+  if (op.info->flop_total > op.cap) return -1;
+  long long off = 0;
+  for (int u = 1; u < op.bin; ++u) off += (long long)op.info->sym_count[u];
+  *nrows = (int64_t)op.info->sym_count[op.bin];
+  return off;
+}
+
+template <int TMAX, int WARPS, int SORTED, bool ONEP = false>
 __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_warp(const int32_t *__restrict__ rows,
                                                          int64_t nrows, DevCSR A, DevCSR B,
                                                          const int64_t *__restrict__ flop,
                                                          const int64_t *__restrict__ c_rp,
                                                          int32_t *__restrict__ c_col,
-                                                         double *__restrict__ c_val) {
+                                                         double *__restrict__ c_val,
+                                                         OnePhase op = OnePhase{}) {
   constexpr int sorted = SORTED;  // (separate instantiations: the sorted emit costs registers)
   extern __shared__ double s_dyn_f64[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *vals = s_dyn_f64 + w * TMAX;
   uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + w * TMAX;
   uint32_t *cnt = reinterpret_cast<uint32_t *>(s_dyn_f64 + WARPS * TMAX) + WARPS * TMAX + w * TMAX;
+  if (ONEP) {
+    const long long off = onephase_rows(op, &nrows);
+    if (off < 0) return;
+    rows += off;
+  }
   for (int64_t r = int64_t(blockIdx.x) * WARPS + w; r < nrows; r += int64_t(gridDim.x) * WARPS) {
     const int i = rows[r];
-    const int64_t rp0 = c_rp[i];
-    const int nnz = (int)(c_rp[i + 1] - rp0);
-    const int logT = num_log2(nnz);
+    const int64_t rp0 = ONEP ? op.fofs[i] : c_rp[i];
+    int nnz = ONEP ? 0 : (int)(c_rp[i + 1] - rp0);
+    const int logT = ONEP ? sym_log2_gpu(flop[i], B.ncols) : num_log2(nnz);
     const int T = 1 << logT;
     for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
     __syncwarp();
@@ -255,6 +302,10 @@ __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_
         }
         __syncwarp();
       });
+    }
+    if (ONEP) {  // nnz(c_i) = occupied slots
+      for (int s0 = 0; s0 < T; s0 += 32) nnz += __popc(__ballot_sync(kFull, keys[s0 + lane] != kEmpty));
+      if (lane == 0) op.row_nnz[i] = nnz;
     }
     warp_emit(keys, vals, cnt, T, logT, nnz, rp0, c_col, c_val, sorted);
     __syncwarp();
@@ -377,10 +428,11 @@ __global__ void __launch_bounds__(T) k_num_heap(const int32_t *__restrict__ rows
 constexpr int kHeapThreads = 64;
 constexpr size_t kHeapSmem = size_t(kHeapMax) * kHeapThreads * 40;
 
-// Block-wide unordered compaction of occupied slots of a table into C row.
+// Block-wide unordered compaction of occupied slots of a table into C row
+// (vlog > 0: the values are in the chunk-spread layout hash_vslot(., vlog)).
 __device__ __forceinline__ void block_emit_unsorted(const uint32_t *keys, const double *vals,
                                                     int64_t T, int64_t rp0, int32_t *c_col,
-                                                    double *c_val, int *s_cnt) {
+                                                    double *c_val, int *s_cnt, int vlog = 0) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int64_t s0 = int64_t(threadIdx.x & ~31); s0 < T; s0 += blockDim.x) {
@@ -394,7 +446,7 @@ __device__ __forceinline__ void block_emit_unsorted(const uint32_t *keys, const 
     if (occ) {
       const int64_t o = rp0 + base + __popc(bal & lt_mask);
       c_col[o] = (int32_t)k;
-      c_val[o] = vals[s];
+      c_val[o] = vals[vlog ? hash_vslot((uint32_t)s, vlog) : (uint32_t)s];
     }
   }
 }
@@ -532,14 +584,14 @@ __device__ __forceinline__ void block_bucket_sort_store(const uint32_t *keys, co
 // the block (atomic CAS for keys, atomic fp64 add for values).  Sorted output:
 // emit unordered into C, reload the row into smem, bucket-sort it into C (a7).
 // ---------------------------------------------------------------------------
-template <int THREADS>
+template <int THREADS, bool ONEP = false>
 __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict__ rows,
                                                        int64_t nrows, DevCSR A, DevCSR B,
                                                        const int64_t *__restrict__ flop,
                                                        const int64_t *__restrict__ c_rp,
                                                        int32_t *__restrict__ c_col,
                                                        double *__restrict__ c_val, int sorted,
-                                                       int tmax) {
+                                                       int tmax, OnePhase op = OnePhase{}) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_cnt, s_next;
   __shared__ DeferList s_dl;  // long B rows walked by the whole block
@@ -548,28 +600,38 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
   const int w = threadIdx.x >> 5;
   double *vals = s_dyn_f64;
   uint32_t *keys = reinterpret_cast<uint32_t *>(s_dyn_f64 + tmax);
+  if (ONEP) {
+    const long long off = onephase_rows(op, &nrows);
+    if (off < 0) return;
+    rows += off;
+  }
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int i = rows[r];
-    const int64_t rp0 = c_rp[i];
-    const int nnz = (int)(c_rp[i + 1] - rp0);
-    const int logT = num_log2(nnz);
+    const int64_t rp0 = ONEP ? op.fofs[i] : c_rp[i];
+    int nnz = ONEP ? 0 : (int)(c_rp[i + 1] - rp0);
+    const int logT = ONEP ? sym_log2_gpu(flop[i], B.ncols) : num_log2(nnz);
     const int T = 1 << logT;
     for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
     if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
     __syncthreads();
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
-      auto acc = [&](bool act, uint32_t c, double v) {
-        if (act) atomicAdd(vals + num_probe_smem(keys, c, logT), v);  // c_ij <- c_ij + value (l.8)
+      auto acc = [&](bool act, uint32_t c, double v) {  // c_ij <- c_ij + value (l.8)
+        if (act) atomicAdd(vals + hash_vslot(num_probe_smem(keys, c, logT), logT), v);
       };
       auto acc_comb = [&](bool act, uint32_t c, double v) {  // keys may repeat in a round
-        if (warp_combine(act, c, v)) atomicAdd(vals + num_probe_smem(keys, c, logT), v);
+        if (warp_combine(act, c, v)) atomicAdd(vals + hash_vslot(num_probe_smem(keys, c, logT), logT), v);
       };
       if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next, &s_dl);
       else for_row<false, true>(A, B, as, ae, w, NW, acc_comb, &s_next, &s_dl);
     }
     __syncthreads();
-    block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt);
+    block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt, logT);
+    if (ONEP) {  // nnz(c_i) = the emitted count
+      __syncthreads();
+      nnz = s_cnt;
+      if (threadIdx.x == 0) op.row_nnz[i] = nnz;
+    }
     if (sorted) {
       __syncthreads();
       for (int s = threadIdx.x; s < nnz; s += THREADS) {
@@ -765,6 +827,19 @@ static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in t
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
 static_assert(kTEnt <= 32 * 32, "32-ary owner search");
 
+// Asynchronous global -> shared copies (cp.async; Ampere+ LDGSTS, no
+// registers held while in flight).
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // last j < n with pre[j] <= x (pre[0] = 0 <= x, pre nondecreasing, n <= 1024):
 // a 32-ary search, two ballots over strided then consecutive entries
 __device__ __forceinline__ int tpart_find(const int32_t *pre, int n, int x) {
@@ -775,26 +850,6 @@ __device__ __forceinline__ int tpart_find(const int32_t *pre, int n, int x) {
   const int c2 = blk * 32 + lane;
   const unsigned b2 = __ballot_sync(kFull, c2 < n && pre[c2] <= x);
   return blk * 32 + 31 - __clz(b2);
-}
-
-// fp64 add into shared memory with the native 64-bit CAS (ATOMS.CAS.64; an
-// atomicAdd(double) on shared memory is a CAS loop on sm_100a anyway, with a
-// load before its first attempt).  The first attempt assumes the slot still
-// holds +0.0 (a first touch: one round trip, storing v itself); on a mismatch
-// the returned value seeds the loop.  Returns true when the slot held +0.0
-// bits (a first touch, or an exactly-zero partial sum: idempotent for the
-// caller's occupancy bit).
-__device__ __forceinline__ bool smem_add_f64_cas(double *addr, double v) {
-  unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
-  unsigned long long old = atomicCAS(a, 0ull, (unsigned long long)__double_as_longlong(v));
-  if (old == 0ull) return true;
-  while (true) {
-    const unsigned long long nw =
-        (unsigned long long)__double_as_longlong(__longlong_as_double((long long)old) + v);
-    const unsigned long long r = atomicCAS(a, old, nw);
-    if (r == old) return false;
-    old = r;
-  }
 }
 
 // Rounds [g0, g1) of 32 consecutive products of the staged SHORT entries (all
@@ -926,10 +981,11 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   // staging reservations, double-buffered by chunk parity: [short, long] =
   // (entries << 32) | (products or rounds)
   __shared__ unsigned long long s_res[2][2];
-  // the current part, prefetched at the previous part's end
-  __shared__ long long s_q, s_rp0, s_as;
-  __shared__ int4 s_P;
-  __shared__ int s_na;
+  __shared__ long long s_rp0;
+  // part pipeline (thread 0): the part after next is reserved and the next
+  // part's records are loaded while this part runs; published at its end
+  __shared__ long long s_q;
+  __shared__ int4 s_P, s_P1, s_Pn[2];
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char *base = reinterpret_cast<char *>(s_dyn_f64);
@@ -949,21 +1005,16 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   // the dense window starts clean; every dense part resets what it used
   for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
   for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
-  // part metadata: thread 0 fetches (part, C row start, A row) ahead of use
-  auto fetch = [&](long long q) {
-    s_q = q;
-    if (q < nparts) {
-      const int4 P = parts[q];
-      s_P = P;
-      s_rp0 = c_rp[P.x];
-      const int64_t as = A.rp[P.x];
-      s_as = as;
-      s_na = (int)(A.rp[P.x + 1] - as);
-    }
-  };
+  long long q_next = 0;  // (thread 0) reserved part after the current one
   if (threadIdx.x == 0) {
     s_res[0][0] = s_res[0][1] = s_res[1][0] = s_res[1][1] = 0ull;
-    fetch((long long)atomicAdd(counter, 1ull));
+    const long long q = (long long)atomicAdd(counter, 1ull);
+    s_q = q;
+    if (q < nparts) {
+      s_P = parts[2 * q];
+      s_P1 = parts[2 * q + 1];
+    }
+    q_next = (long long)atomicAdd(counter, 1ull);
   }
   __syncthreads();
   const bool instr = (tune & 8) && threadIdx.x == 0;
@@ -971,15 +1022,25 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   while (true) {
     const int64_t q = s_q;
     if (q >= nparts) break;
-    // the next part is reserved now (its fetch completes during this part)
-    long long q_next = 0;
-    if (threadIdx.x == 0) q_next = (long long)atomicAdd(counter, 1ull);
-    const int4 P = s_P;
+    const int4 P = s_P, P1 = s_P1;
+    // thread 0: async copies (cp.async, no registers held) of the next
+    // part's records (q_next was reserved one part ago) and of this part's
+    // C row start (used at the emit); reserve the part after next
+    long long q_after = 0;
+    if (threadIdx.x == 0) {
+      cp_async8(&s_rp0, c_rp + P.x);
+      if (q_next < nparts) {
+        cp_async16(&s_Pn[0], parts + 2 * q_next);
+        cp_async16(&s_Pn[1], parts + 2 * q_next + 1);
+      }
+      cp_async_commit();
+      q_after = q_next < nparts ? (long long)atomicAdd(counter, 1ull) : q_next;
+    }
     const int t0 = P.y & 0xFFFF, t1 = P.y >> 16;
     const int cnt = P.w;
     const bool dense = t1 == t0 + 1;
-    const int64_t rp0 = s_rp0, as = s_as;
-    const int na = s_na;
+    const int64_t as = (int64_t)(((unsigned long long)(unsigned)P1.y << 32) | (unsigned)P1.x);
+    const int na = P1.z;
     const int64_t lo = int64_t(t0) << kTileLog;
     const long long c0 = instr ? clock64() : 0;
     long long c_stage = 0, c_rounds = 0;
@@ -993,8 +1054,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     auto acc_dense = [&](bool act, uint32_t c, double v) {
       if (act) {
         const uint32_t off = c - (uint32_t)lo;
-        if (smem_add_f64_cas(dv + off, v))  // c_ij <- c_ij + value (l.8), dense window
-          atomicOr(dbm + (off >> 5), 1u << (off & 31u));  // first touch: occupied
+        atomicAdd(dv + dense_slot(off), v);  // c_ij <- c_ij + value (l.8), dense window
+        atomicOr(dbm + bm_word(off >> 5), 1u << (off & 31u));
       }
     };
     auto acc_hash = [&](bool act, uint32_t c, double v) {
@@ -1002,7 +1063,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       uint32_t slot = 0;
       if (act) {
         slot = probe_chunk(hk, c, logT, &isnew);
-        smem_add_f64_cas(hv + slot, v);  // c_ij <- c_ij + value (l.8)
+        atomicAdd(hv + hash_vslot(slot, logT), v);  // c_ij <- c_ij + value (l.8)
       }
       const unsigned m = __ballot_sync(kFull, isnew);
       if (m) {
@@ -1104,9 +1165,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         prods += (unsigned long long)PS;
       }
     }
+    if (threadIdx.x == 0) cp_async_wait_all();
     __syncthreads();
     const long long ce = instr ? clock64() : 0;
-    const int64_t out = rp0 + P.z;
+    const int64_t out = s_rp0 + P.z;
     if (dense) {
       // keys before each 32-column word (block scan of the word popcounts),
       // then a warp per word: lane l emits column 32 qw + l if present
@@ -1114,27 +1176,28 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       static_assert(kTileCols / 32 <= THREADS, "one word per thread");
       int32_t *wcum = reinterpret_cast<int32_t *>(eb);
       const int nwd = kTileCols / 32;
-      const int pc = (int)threadIdx.x < nwd ? __popc(dbm[threadIdx.x]) : 0;
+      const int pc = (int)threadIdx.x < nwd ? __popc(dbm[bm_word(threadIdx.x)]) : 0;
       int totw;
       const int wx = block_excl_scan_int(pc, s_warp, &totw);
       if ((int)threadIdx.x < nwd) wcum[threadIdx.x] = wx;
       __syncthreads();
       for (int qw = w; qw < nwd; qw += NW) {
-        const uint32_t word = dbm[qw];
+        const uint32_t word = dbm[bm_word(qw)];
         if ((word >> lane) & 1u) {
           const int64_t o = out + wcum[qw] + __popc(word & ((1u << lane) - 1u));
           c_col[o] = (int32_t)(lo + qw * 32 + lane);
-          c_val[o] = dv[qw * 32 + lane];
-          dv[qw * 32 + lane] = 0.0;
+          const uint32_t ds = dense_slot(qw * 32 + lane);
+          c_val[o] = dv[ds];
+          dv[ds] = 0.0;
         }
         __syncwarp();
-        if (lane == 0) dbm[qw] = 0u;
+        if (lane == 0) dbm[bm_word(qw)] = 0u;
       }
     } else if (!sorted) {
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
         const int s = slot_of[p];
         c_col[out + p] = (int32_t)hk[s];
-        c_val[out + p] = hv[s];
+        c_val[out + p] = hv[hash_vslot(s, logT)];
       }
     } else {
       // gather the pairs into the entry stage, sort them with the table
@@ -1144,7 +1207,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
         const int s = slot_of[p];
         gk[p] = hk[s];
-        gv[p] = hv[s];
+        gv[p] = hv[hash_vslot(s, logT)];
       }
       __syncthreads();
       const int64_t span = (int64_t(t1 - t0)) << kTileLog;
@@ -1188,7 +1251,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
                              c_val, s_red);
       }
     }
-    if (threadIdx.x == 0) fetch(q_next);  // (every thread has read this part's metadata)
+    if (threadIdx.x == 0) {  // publish the next part (every thread has read this one)
+      s_q = q_next;
+      s_P = s_Pn[0];
+      s_P1 = s_Pn[1];
+      q_next = q_after;
+    }
     __syncthreads();
     if (instr) {
       const long long cz = clock64();
@@ -1201,6 +1269,26 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       atomicAdd(dbg + (dense ? 8 : 11), (unsigned long long)(cz - ce));   // emit
       atomicAdd(dbg + 9, (unsigned long long)na);
       atomicAdd(dbg + 10, (unsigned long long)cnt);
+    }
+  }
+}
+
+// One-phase compaction: row i of the workspace (at the flop prefix fofs[i],
+// nnz(c_i) entries) to C at C_row_ptr[i].  A warp per row, coalesced.
+__global__ void __launch_bounds__(256) k_onephase_copy(int64_t m, const int64_t *__restrict__ fofs,
+                                                       const int64_t *__restrict__ c_rp,
+                                                       const int32_t *__restrict__ t_col,
+                                                       const double *__restrict__ t_val,
+                                                       int32_t *__restrict__ c_col,
+                                                       double *__restrict__ c_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < m; i += nwarps) {
+    const int64_t s = fofs[i], d = c_rp[i], n = c_rp[i + 1] - d;
+    for (int64_t q = lane; q < n; q += 32) {
+      c_col[d + q] = __ldg(t_col + s + q);
+      c_val[d + q] = __ldg(t_val + s + q);
     }
   }
 }

@@ -48,6 +48,10 @@ struct spg_ctx {
   Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (keys, ranks, unsorted rows, CUB temp)
   Buf mask_rows;                     // row lists of the mask-and-sum tiers
   Buf useful_bits;                   // useful-entry bitmask of k_flop_nz (pruning), grow-only
+  Buf one_fofs, one_col, one_val;    // one-phase: flop prefix, flop-sized row workspace (grow-only)
+  bool have_one = false;             // a one-phase result waits in the workspace
+  int64_t one_m = 0;
+  const int64_t *one_rp = nullptr;
   bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
   int64_t prune_n = 0;
   spg_csr Ap{};
@@ -336,7 +340,11 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_csr_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_num_global<1024>, kRankSmem) == SPG_OK &&
-         set_smem(c, k_num_heap<kHeapThreads>, kHeapSmem) == SPG_OK;
+         set_smem(c, k_num_heap<kHeapThreads>, kHeapSmem) == SPG_OK &&
+         set_smem(c, k_num_warp<1024, 4, 0, true>, s_num_w1024) == SPG_OK &&
+         set_smem(c, k_num_warp<1024, 4, 1, true>, s_num_w1024) == SPG_OK &&
+         set_smem(c, k_num_block<128, true>, size_t(2048) * 12) == SPG_OK &&
+         set_smem(c, k_num_block<512, true>, size_t(8192) * 12) == SPG_OK;
   }
   if (!ok) {
     cudaGetLastError();
@@ -354,7 +362,8 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
                  &c->info,      &c->scratch,   &c->parts,     &c->parts2,    &c->part_hist,
                  &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
                  &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
-                 &c->rl_tmp,    &c->rl_cub,    &c->mask_rows, &c->useful_bits};
+                 &c->rl_tmp,    &c->rl_cub,    &c->mask_rows, &c->useful_bits, &c->one_fofs,
+                 &c->one_col,   &c->one_val};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {
@@ -569,7 +578,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       parts_cap = (int64_t)(2 * h.flop_total / kTPartKeys) + (int64_t)h.sym_count[SB_BM] + 16;
       const int64_t ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       parts_cap = std::min<int64_t>(parts_cap, (int64_t)h.sym_count[SB_BM] * ntiles + 16);
-      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * sizeof(int4), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * 2 * sizeof(int4), s)) != SPG_OK) return st;
       parts = (int4 *)c->parts.p;
       c->plan_parts = true;
     }
@@ -622,7 +631,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
           }
         SPG_LAUNCHED(c, "k_sym_block");
       } else if (bin == SB_BM) {
-        const size_t nwords = size_t((B->ncols + 31) / 32);
+        const size_t nwords = (size_t((B->ncols + 31) / 32) + 31) & ~size_t(31);  // whole groups (bm_word)
         const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
@@ -726,7 +735,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       if ((st = buf_ensure(c, c->toff, size_t(B->nrows) * size_t(ntiles + 1) * 4, s)) != SPG_OK)
         return st;
-      if ((st = buf_ensure(c, c->parts2, size_t(h.parts_used) * sizeof(int4), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->parts2, size_t(h.parts_used) * 2 * sizeof(int4), s)) != SPG_OK) return st;
       if ((st = buf_ensure(c, c->part_hist, size_t(kPartBuckets) * 4, s)) != SPG_OK) return st;
       PlanInfo *dinfo = (PlanInfo *)c->info.p;
       SPG_CUDA(c, cudaMemsetAsync(&dinfo->row_counter, 0, 8, s));
@@ -840,10 +849,11 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
     } else if (use_parts) {  // NB_G: column-tile parts, independent work items
       {
         ProfScope _ps(c, ss, "k_num_tpart<512>");
+        PlanInfo *dinfo = (PlanInfo *)c->info.p;
         k_num_tpart<512><<<(unsigned)(2 * c->num_sms), 512, kTPartSmem, ss>>>(
             a, b, C_row_ptr, C_col_idx, C_val, sorted, (const int4 *)c->parts2.p,
-            (int64_t)h.parts_used, (const int32_t *)c->toff.p, B->nrows,
-            &((PlanInfo *)c->info.p)->row_counter, c->tune, ((PlanInfo *)c->info.p)->dbg);
+            (int64_t)h.parts_used, (const int32_t *)c->toff.p, B->nrows, &dinfo->row_counter,
+            c->tune, dinfo->dbg);
       }
       SPG_LAUNCHED(c, "k_num_tpart");
     } else {  // NB_G
@@ -868,6 +878,132 @@ spg_status spg_set_accumulator(spg_ctx *c, int accum, double collision_factor) {
     return fail(c, SPG_ERR_INVALID_ARG, "collision factor must be >= 1");
   c->accum = accum;
   c->cfac = (float)collision_factor;
+  return SPG_OK;
+}
+
+// One-phase multiply, step 1: see include/spgemm.h.
+spg_status spg_onephase(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t *C_row_ptr,
+                        int64_t *nnz_C, int64_t *flop_total, int sorted, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  c->have_one = false;
+  c->have_plan = false;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", true)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", true)) != SPG_OK) return st;
+  if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
+  if (!C_row_ptr || !nnz_C) return fail(c, SPG_ERR_INVALID_ARG, "C_row_ptr / nnz_C is NULL");
+  if (sorted != 0 && sorted != 1) return fail(c, SPG_ERR_INVALID_ARG, "sorted must be 0 or 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  const int64_t m = A->nrows;
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->flop, size_t(std::max<int64_t>(m, 1)) * 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rows_sym, size_t(std::max<int64_t>(m, 1)) * 4, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->one_fofs, size_t(m + 1) * 8, s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  int64_t *row_nnz = C_row_ptr + 1;
+  int64_t *fofs = (int64_t *)c->one_fofs.p;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    // workspace: grow-only, sized by the last flop total seen (>= 1M products)
+    const unsigned long long cap = (unsigned long long)(c->one_col.bytes / 4);
+    SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
+    SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, size_t(m + 1) * 8, s));
+    if (m > 0 && B->nrows > 0) {
+      // a1 + a2: flop, symbolic bins (the tables are sized by the flop bound)
+      if ((st = launch_flop(c, A, B, 1, s)) != SPG_OK) return st;
+      {
+        ProfScope _ps(c, s, "k_bin_scatter_sym");
+        k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, (const int64_t *)c->flop.p, A->row_ptr,
+                                                                 B->ncols, 0, info, (int32_t *)c->rows_sym.p,
+                                                                 row_nnz);
+      }
+      SPG_LAUNCHED(c, "k_bin_scatter(sym)");
+      // workspace row offsets: exclusive prefix of flop
+      SPG_CUDA(c, cudaMemsetAsync(fofs, 0, 8, s));
+      SPG_CUDA(c, cudaMemcpyAsync(fofs + 1, c->flop.p, size_t(m) * 8, cudaMemcpyDeviceToDevice, s));
+      if ((st = launch_scan(c, fofs + 1, m, s)) != SPG_OK) return st;
+      if (cap > 0) {
+        // a6 (+ a7) on the symbolic bins, counts read on the device
+        DevCSR a = dev(A), b = dev(B);
+        const int32_t *rows = (const int32_t *)c->rows_sym.p;
+        const int64_t *flop = (const int64_t *)c->flop.p;
+        int32_t *tc = (int32_t *)c->one_col.p;
+        double *tv = (double *)c->one_val.p;
+        OnePhase op{info, fofs, row_nnz, cap, SB_W128};
+        const unsigned gw = (unsigned)(c->num_sms * 16);
+        {
+          ProfScope _ps(c, s, "k_num_warp<256>(1p)");
+          if (sorted)
+            k_num_warp<256, kWarps, 1, true><<<gw, kWarps * 32, kWarps * 256 * 16, s>>>(rows, 0, a, b, flop, nullptr, tc, tv, op);
+          else
+            k_num_warp<256, kWarps, 0, true><<<gw, kWarps * 32, kWarps * 256 * 16, s>>>(rows, 0, a, b, flop, nullptr, tc, tv, op);
+        }
+        SPG_LAUNCHED(c, "k_num_warp(1p)");
+        op.bin = SB_W1024;
+        {
+          ProfScope _ps(c, s, "k_num_warp<1024>(1p)");
+          if (sorted)
+            k_num_warp<1024, 4, 1, true><<<gw, 4 * 32, 4 * 1024 * 16, s>>>(rows, 0, a, b, flop, nullptr, tc, tv, op);
+          else
+            k_num_warp<1024, 4, 0, true><<<gw, 4 * 32, 4 * 1024 * 16, s>>>(rows, 0, a, b, flop, nullptr, tc, tv, op);
+        }
+        SPG_LAUNCHED(c, "k_num_warp(1p)");
+        for (int bin = SB_B2K; bin <= SB_B8K; ++bin) {
+          op.bin = bin;
+          const int tmax = 2048 << (bin - SB_B2K);
+          ProfScope _ps(c, s, "k_num_block(1p)");
+          if (tmax == 2048)
+            k_num_block<128, true><<<(unsigned)(c->num_sms * 8), 128, size_t(tmax) * 12, s>>>(
+                rows, 0, a, b, flop, nullptr, tc, tv, sorted, tmax, op);
+          else
+            k_num_block<512, true><<<(unsigned)(c->num_sms * 4), 512, size_t(tmax) * 12, s>>>(
+                rows, 0, a, b, flop, nullptr, tc, tv, sorted, tmax, op);
+          SPG_LAUNCHED(c, "k_num_block(1p)");
+        }
+      }
+    }
+    // a4: C_row_ptr = exclusive scan of nnz(c_i)
+    if ((st = launch_scan(c, row_nnz, m, s)) != SPG_OK) return st;
+    if ((st = read_info(c, s)) != SPG_OK) return st;  // the one host round trip
+    const PlanInfo &h = *c->host_info;
+    if (h.sym_count[SB_B16K] || h.sym_count[SB_B32K] || h.sym_count[SB_G] || h.sym_count[SB_BM])
+      return fail(c, SPG_ERR_OVERFLOW,
+                  "one-phase: rows need tables beyond 8192 slots (flop_i >= 8192); use "
+                  "spg_symbolic + spg_numeric");
+    if ((int64_t)h.max_brow > kMaxBRow) return fail(c, SPG_ERR_OVERFLOW, "a row of B has more than 2^26 entries");
+    if (h.flop_total <= cap || h.flop_total == 0) {
+      *nnz_C = (int64_t)h.nnz_total;
+      if (flop_total) *flop_total = (int64_t)h.flop_total;
+      c->have_one = true;
+      c->one_m = m;
+      c->one_rp = C_row_ptr;
+      return SPG_OK;
+    }
+    // the workspace was too small: grow it to this flop total and rerun once
+    const size_t want = size_t(h.flop_total) + (size_t(h.flop_total) >> 3);
+    if (want > size_t(1) << 40) return fail(c, SPG_ERR_WORKSPACE, "one-phase workspace too large");
+    if ((st = buf_ensure(c, c->one_col, want * 4, s)) != SPG_OK) return st;
+    if ((st = buf_ensure(c, c->one_val, want * 8, s)) != SPG_OK) return st;
+  }
+  return fail(c, SPG_ERR_WORKSPACE, "one-phase workspace could not be sized");
+}
+
+// One-phase multiply, step 2: compact the rows into the caller's C.
+spg_status spg_onephase_emit(spg_ctx *c, int32_t *C_col_idx, double *C_val, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  if (!c->have_one) return fail(c, SPG_ERR_STATE, "spg_onephase_emit without a matching spg_onephase");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  const int64_t m = c->one_m;
+  if (m > 0 && (C_col_idx || C_val)) {
+    if (!C_col_idx || !C_val) return fail(c, SPG_ERR_INVALID_ARG, "C_col_idx / C_val is NULL");
+    ProfScope _ps(c, s, "k_onephase_copy");
+    k_onephase_copy<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), int64_t(c->num_sms) * 16), 256, 0, s>>>(
+        m, (const int64_t *)c->one_fofs.p, c->one_rp, (const int32_t *)c->one_col.p,
+        (const double *)c->one_val.p, C_col_idx, C_val);
+    SPG_LAUNCHED(c, "k_onephase_copy");
+  }
+  c->have_one = false;
   return SPG_OK;
 }
 

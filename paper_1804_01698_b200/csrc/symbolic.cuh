@@ -35,6 +35,15 @@ __device__ __forceinline__ int sym_insert_smem(uint32_t *tab, uint32_t c, int lo
   return isnew ? 1 : 0;
 }
 
+// Bank spreading of a bitmap: word w of the column bitmap is stored at
+// w ^ ((w >> 5) ^ (w >> 10) ^ (w >> 15)) & 31, a permutation inside each
+// group of 32 words (so a tile's 256 words stay in place as a set).  R-MAT
+// columns have each bit set with probability 0.24, so without it a quarter
+// of the atomicOr's of a round hit bank 0 (words with bits 5-9 clear).
+__device__ __forceinline__ uint32_t bm_word(uint32_t w) {
+  return w ^ (((w >> 5) ^ (w >> 10) ^ (w >> 15)) & 31u);
+}
+
 // Bitmap variant for very long rows: column c -> bit c of an ncols-bit set.
 __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
   const uint32_t bit = 1u << (c & 31u);
@@ -464,8 +473,9 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
 // sorted it also cuts rows with nnz > kPartMinKeys into column-tile parts for
-// the numeric G tier (spg_internal.cuh): part = int4 {row, first tile | end
-// tile << 16, keys of the row before the part, keys in the part}.
+// the numeric G tier (spg_internal.cuh): part = two int4 records {row, first
+// tile | end tile << 16, keys of the row before the part, keys in the part}
+// and {A.row_ptr[row] (lo, hi), nnz(a_row), 0}.
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restrict__ rows,
@@ -484,7 +494,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   __shared__ int s_nne[kMaxTiles + 1];   // first nonempty tile at or after each tile
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwords = (int)((B.ncols + 31) >> 5);
+  // (words rounded up to whole 32-word groups: bm_word permutes inside a group)
+  const int nwords = (int)((((B.ncols + 31) >> 5) + 31) & ~31);
   const int ntiles = (int)((B.ncols + kTileCols - 1) >> kTileLog);
   uint32_t *bm = s_dyn_u32;
   const bool want_parts = parts != nullptr && info->b_unsorted == 0;
@@ -497,7 +508,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     // set the bit of every product's column (the old value is not used: no
     // dependency on the atomic's return), then count the set bits once
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) atomicOr(bm + (c >> 5), 1u << (c & 31u));
+      if (act) atomicOr(bm + bm_word(c >> 5), 1u << (c & 31u));
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
@@ -578,7 +589,10 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       const int np = s_cnt;
       for (int p = threadIdx.x; p < np; p += THREADS) {
         const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
-        parts[s_pbase + p] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
+        parts[2 * (s_pbase + p)] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
+        parts[2 * (s_pbase + p) + 1] =
+            make_int4((int)(unsigned)(unsigned long long)as, (int)(unsigned)((unsigned long long)as >> 32),
+                      (int)(ae - as), 0);
       }
     }
     __syncthreads();

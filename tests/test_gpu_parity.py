@@ -623,3 +623,35 @@ def test_set_accumulator_errors(spg):
         _lib._check(ctx.handle, "x", _lib.load().spg_set_accumulator(ctx.handle, 7, 1.3))
     with pytest.raises(_lib.SpgError, match="INVALID_ARG"):
         ctx.set_accumulator("auto", 0.5)
+
+
+# ------------------------------------------------------------------ one-phase
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_onephase_every_bin(spg, sorted_out):
+    """One-phase multiply (tables sized by flop, no symbolic pass) on rows
+    spanning every warp / block bin up to 8191 products (flop at T-1 / T /
+    T+1 boundaries), shuffled and sorted B, plus C1 and a small C2: exact vs
+    the oracle; rows beyond the block tier are refused (OVERFLOW)."""
+    ctx = spg.Context()
+    specs = []
+    for h in [16, 32, 128, 256, 1024, 2048, 4096]:
+        for f in (h - 1, h, h + 1):
+            specs += [(f, max(1, f // 3)), (f, f)]
+    specs += [(8191, 4000), (1, 1), (0, 0), (600, 2)]
+    for shuffle in (False, True):
+        A, B = synth.crafted_rows(specs, 1 << 16, 51, shuffle=shuffle)
+        dA, dB = spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B)
+        for rep in range(2):  # 1st call grows the workspace (rerun), 2nd is one round trip
+            C = spg.spgemm(dA, dB, sorted=sorted_out, ctx=ctx, method="one_phase")
+            compare(*C.to_host(), *oracle.spgemm(A, B), sorted_out, f"one-phase shuffle={shuffle}")
+    for name, sc in (("c1_er4096", None), ("c2_stencil64", 12)):
+        A, B, _ = synth.workload(name, scale=sc)
+        dA = spg.DeviceCSR.from_host(A)
+        C = spg.spgemm(dA, dA, sorted=sorted_out, ctx=ctx, method="one_phase")
+        compare(*C.to_host(), *oracle.spgemm(A, B), sorted_out, f"one-phase {name}")
+    A, B = synth.crafted_rows([(20000, 5000)], 1 << 16, 52)
+    from paper_1804_01698_b200 import _lib
+    with pytest.raises(_lib.SpgError, match="OVERFLOW"):
+        spg.spgemm(spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B), ctx=ctx, method="one_phase")
+    with pytest.raises(_lib.SpgError, match="STATE"):
+        _lib.spg_onephase_emit(ctx.handle, 0, 0, 0)
