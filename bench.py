@@ -307,34 +307,41 @@ def run_ours(args):
     log(f"[rank {rank}] workload {args.config} generated in {time.perf_counter() - t0:.1f}s")
     same = args.config in ("c1_er4096", "c2_stencil64", "c3_rmat20")
 
-    def bcast_csr(M):
-        if world == 1:
-            return spg.DeviceCSR.from_host(M)
-        meta = torch.zeros(3, dtype=torch.int64, device=dev)
-        if rank == 0:
-            meta[:] = torch.tensor([M.nrows, M.ncols, int(M.row_ptr[-1])])
-        dist.broadcast(meta, 0)
-        n, k, nz = (int(x) for x in meta.tolist())
-        if rank == 0:
-            d = spg.DeviceCSR.from_host(M)
-        else:
-            d = spg.DeviceCSR(n, k, torch.empty(n + 1, dtype=torch.int64, device=dev),
-                              torch.empty(nz, dtype=torch.int32, device=dev),
-                              torch.empty(nz, dtype=torch.float64, device=dev))
-        for t in (d.row_ptr, d.col, d.val):
-            dist.broadcast(t, 0)
-        return d
-
-    dA = bcast_csr(A if rank == 0 else None)
-    dB = dA if same else bcast_csr(B if rank == 0 else None)
-    dG = bcast_csr(extra["G"] if rank == 0 else None) if args.config == "c5_triangle" else None
-    ctx = spg.Context(local)
-
-    # ---- a8: flop-balanced row split (RowsToThreads on the GPU)
-    offs, flop_total = spg.rows_to_parts(dA, dB, world, ctx)
-    r0, r1 = offs[rank], offs[rank + 1]
-    Aloc = dA.rows(r0, r1)
     tri = args.config == "c5_triangle"
+    ctx = spg.Context(local)
+    if world == 1:
+        dA = spg.DeviceCSR.from_host(A)
+        dB = dA if same else spg.DeviceCSR.from_host(B)
+        dG = spg.DeviceCSR.from_host(extra["G"]) if tri else None
+        # ---- a8: flop-balanced row split (RowsToThreads on the GPU)
+        offs, flop_total = spg.rows_to_parts(dA, dB, world, ctx)
+        Aloc = dA
+    else:
+        # inputs from rank 0 with the library's distribution (paper_1804_01698_b200/dist.py,
+        # tested with gloo): B broadcast (row_ptr first, col / val async), A row-scattered by
+        # the flop-balanced split computed on rank 0's GPU; C5's mask G broadcast whole (the
+        # degree-order variant relabels all of G on every rank)
+        from paper_1804_01698_b200 import dist as sdist
+        hA = spg.DeviceCSR.from_host(A) if rank == 0 else None
+        hB = (hA if same else spg.DeviceCSR.from_host(B)) if rank == 0 else None
+        dB, works = sdist.broadcast_csr(hB, 0, dev, async_values=True)
+        meta = torch.zeros(world + 2, dtype=torch.int64, device=dev)
+        if rank == 0:
+            o, t = spg.rows_to_parts(hA, hB, world, ctx)
+            meta[:] = torch.tensor(o + [t], dtype=torch.int64)
+        dist.broadcast(meta, 0)
+        offs, flop_total = [int(x) for x in meta[:world + 1].tolist()], int(meta[world].item())
+        for w_ in works:
+            w_.wait()
+        if same:
+            dA = dB
+            Aloc = dB.rows(offs[rank], offs[rank + 1])
+        else:
+            dA = None
+            Aloc = sdist.scatter_rows(hA, offs, 0, dev)
+        dG = sdist.broadcast_csr(spg.DeviceCSR.from_host(extra["G"]) if (tri and rank == 0) else None,
+                                 0, dev) if tri else None
+    r0, r1 = offs[rank], offs[rank + 1]
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
@@ -349,14 +356,33 @@ def run_ours(args):
         deg = {"L": L2.rows(q0, q1), "U": U2, "G": G2, "q0": q0, "q1": q1, "flop": flop_deg,
                "relabel_s": time.perf_counter() - t_rl}
 
+    # accumulator A/B: sorted output with every eligible row
+    # hashed, or merged by the heap (the default ctx runs the cost model, AUTO)
+    acc_ctx = {}
+    for mode in ("hash", "heap"):
+        acc_ctx[mode] = spg.Context(local)
+        acc_ctx[mode].set_accumulator(mode)
+
     def step(sorted_out):
+        if isinstance(sorted_out, str) and sorted_out.startswith("acc_"):  # acc_<mode>[_deg]
+            mode = sorted_out.split("_")[1]
+            if sorted_out.endswith("_deg"):  # L'*U' formed (sorted) in the degree order + mask
+                return (spg.triangle_count_rows(deg["L"], deg["U"], deg["G"], 0, deg["q1"] - deg["q0"],
+                                                sorted=True, ctx=acc_ctx[mode], g_shift=deg["q0"])
+                        if deg["q1"] > deg["q0"] else 0)
+            return spg.spgemm(Aloc, dB, sorted=True, ctx=acc_ctx[mode])
+        if sorted_out == "deg_formed":  # the same with the default (AUTO) accumulator
+            return (spg.triangle_count_rows(deg["L"], deg["U"], deg["G"], 0, deg["q1"] - deg["q0"],
+                                            sorted=True, ctx=ctx, g_shift=deg["q0"])
+                    if deg["q1"] > deg["q0"] else 0)
         if sorted_out == "fused":  # C5 variant: mask fused into the product (C never formed)
-            return spg.masked_sum(Aloc, dB, dG, r0, ctx) if r1 > r0 else 0.0
+            return spg.masked_sum_int(Aloc, dB, dG, r0, ctx) if r1 > r0 else 0
         if sorted_out == "fused_deg":  # the same on the degree-ordered split
-            return (spg.masked_sum(deg["L"], deg["U"], deg["G"], deg["q0"], ctx)
-                    if deg["q1"] > deg["q0"] else 0.0)
+            return (spg.masked_sum_int(deg["L"], deg["U"], deg["G"], deg["q0"], ctx)
+                    if deg["q1"] > deg["q0"] else 0)
         if tri:  # rows [r0, r1) of C = L*U, masked by the same rows of G, in row blocks
-            return spg.triangle_count_rows(dA, dB, dG, r0, r1, sorted=sorted_out, ctx=ctx)
+            return spg.triangle_count_rows(Aloc, dB, dG, 0, r1 - r0, sorted=sorted_out, ctx=ctx,
+                                           g_shift=r0)
         C = spg.spgemm(Aloc, dB, sorted=sorted_out, ctx=ctx)
         return C
 
@@ -422,12 +448,22 @@ def run_ours(args):
         ms_fused, _, _, last_fused = timed("fused", args.steps)
         step("fused_deg")
         ms_fused_deg, _, _, last_fdeg = timed("fused_deg", args.steps)
-        counts = torch.tensor([float(last_unsorted), float(last_fused), float(last_fdeg)],
+    acc_ab, acc_counts = {}, []
+    if not args.no_accum_ab:
+        kinds = (("deg_formed", "acc_hash_deg", "acc_heap_deg") if tri else ("acc_hash", "acc_heap"))
+        for kname in kinds:
+            step(kname)
+            ms_k, _, _, last_k = timed(kname, max(1, min(args.steps, 5)))
+            acc_ab[kname] = ms_k
+            if tri:
+                acc_counts.append(float(last_k))
+    if tri:
+        counts = torch.tensor([float(last_unsorted), float(last_fused), float(last_fdeg)] + acc_counts,
                               dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(counts)
         if parity is not None:
-            parity["triangles_unsorted_fused_degree"] = [int(round(x / 2)) for x in counts.tolist()]
+            parity["triangles_unsorted_fused_degree_and_ab"] = [int(round(x / 2)) for x in counts.tolist()]
             parity["ok"] = parity["ok"] and all(
                 int(round(x / 2)) == parity["oracle_triangles"] for x in counts.tolist())
     clk = clocks.stop()
@@ -443,7 +479,8 @@ def run_ours(args):
 
         def prof_step():
             if tri:  # the headline C5 step: row blocks of C = L*U, each masked by G
-                return spg.triangle_count_rows(dA, dB, dG, r0, r1, sorted=True, ctx=pctx)
+                return spg.triangle_count_rows(Aloc, dB, dG, 0, r1 - r0, sorted=True, ctx=pctx,
+                                               g_shift=r0)
             return spg.spgemm(Aloc, dB, sorted=True, ctx=pctx)
         out = prof_step()
         del out
@@ -465,7 +502,7 @@ def run_ours(args):
 
     # ---- e2e: through the public API with HOST buffers (H2D of A,B from pinned
     # memory, the multiply, D2H of C) inside the timed region
-    e2e = e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total)
+    e2e = e2e_measure(args, spg, ctx, Aloc, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total)
 
     # ---- roofline of the dominant kernel (live per-launch events, sorted run)
     roof = None
@@ -539,6 +576,16 @@ def run_ours(args):
                                             "note": "sum(L*U o G) with the mask fused into the "
                                                     "product (SURVEY 8(f) row 1); C not formed"}}
                             if ms_fused is not None else {}),
+                         **({k: {"ms_per_step": v,
+                                 "note": "sorted C, accumulator A/B (SURVEY 8(f) row 4): "
+                                         + {"acc_hash": "every row hashed + sorted",
+                                            "acc_heap": "heap merge for every eligible row (P:340-352)",
+                                            "deg_formed": "degree order, L'*U' formed sorted, cost model "
+                                                          "(AUTO) accumulator, + mask",
+                                            "acc_hash_deg": "degree order, L'*U' formed sorted, all hashed",
+                                            "acc_heap_deg": "degree order, L'*U' formed sorted, heap where "
+                                                            "eligible"}[k]}
+                             for k, v in acc_ab.items()}),
                          **({"fused_mask_degree_order": {
                              "ms_per_step": ms_fused_deg, "flop": deg["flop"],
                              "gflops_own_flop": 2.0 * deg["flop"] / (ms_fused_deg * 1e-3) / 1e9,
@@ -631,7 +678,7 @@ def bench_parity(args, A, B, out, tri, world, rank, dev, r0, r1):
             "max_rel_err": worst, "ok": bool(ok)}
 
 
-def e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total):
+def e2e_measure(args, spg, ctx, Aloc, dB, dG, same, dev, world, rank, r0, r1, tri, flop_total):
     """Same metric through the public API with host (pinned) buffers: every
     rank uploads ITS inputs (rows [r0, r1) of A, all of B, and for C5 the same
     rows of G) from pinned host memory, multiplies (C5: counts), and reads its
@@ -647,7 +694,7 @@ def e2e_measure(args, spg, ctx, dA, dB, dG, same, dev, world, rank, r0, r1, tri,
         return ((rp - s).cpu().pin_memory(), M.col[s:e].cpu().pin_memory(),
                 M.val[s:e].cpu().pin_memory(), M.ncols)
 
-    hA = host_rows(dA, r0, r1)
+    hA = host_rows(Aloc, 0, Aloc.nrows)
     hB = host_rows(dB, 0, dB.nrows) if not (same and world == 1) else hA
     hG = host_rows(dG, r0, r1) if tri else None
     m = r1 - r0
@@ -737,6 +784,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-accum-ab", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")

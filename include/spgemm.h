@@ -148,23 +148,28 @@ spg_status spg_numeric(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
  * records which rows go where).
  *   SPG_ACCUM_AUTO (default): a row of the warp tiers (nnz(c_i) <= 512) with
  *       nnz(a_i) <= 16, flop_i <= 2048 and sorted B rows is merged by a
- *       per-thread heap when T_heap = flop_i log2 nnz(a_i) (Eq:heap_est) is
+ *       per-thread heap when T_heap = h flop_i log2 nnz(a_i) (Eq:heap_est) is
  *       below T_hash = flop_i c + nnz(c_i) log2 nnz(c_i) (Eq:hash_est), else
  *       hashed and sorted;
  *   SPG_ACCUM_HASH: every row hashed (the heap tier never runs);
  *   SPG_ACCUM_HEAP: every row eligible as above is merged by the heap.
  *   collision_factor: c of Eq:hash_est, >= 1 (default 1.3, the measured
  *       average probes of the warp-tier tables).
+ *   heap_cost: h, the cost of one heap step relative to one hash probe, > 0
+ *       (default 8, measured on B200: DESIGN.md §9d; 1 = the paper's
+ *       unit-cost model).
  * Unsorted output always uses the hash tiers.  Errors: SPG_ERR_INVALID_ARG. */
 #define SPG_ACCUM_AUTO 0
 #define SPG_ACCUM_HASH 1
 #define SPG_ACCUM_HEAP 2
-spg_status spg_set_accumulator(spg_ctx *ctx, int accum, double collision_factor);
+spg_status spg_set_accumulator(spg_ctx *ctx, int accum, double collision_factor,
+                               double heap_cost);
 
 /* One-phase multiply (§2, the
  * one-phase alternative: "allocate large enough memory space for output
  * matrix and compute").  No symbolic pass: every row's hash table is sized
- * by the flop upper bound (lowest 2^n > min(N_col, flop_i)), the
+ * by the flop upper bound (lowest 2^n >= 2 min(N_col, flop_i): the numeric
+ * rule of reading R6 with flop_i bounding nnz(c_i)), the
  * numeric kernels run on those bins with their row counts read on the device
  * (persistent launches) and write row i into a flop-sized ctx workspace (12
  * bytes per product, grow-only) while counting nnz(c_i); a scan gives
@@ -175,8 +180,8 @@ spg_status spg_set_accumulator(spg_ctx *ctx, int accum, double collision_factor)
  *   C_row_ptr   : device, caller-allocated int64[A.nrows + 1].
  *   nnz_C       : host out.   flop_total: host out (may be NULL).
  *   sorted      : 0/1 as for spg_numeric.
- * Errors: SPG_ERR_OVERFLOW when a row needs a table beyond 8192 slots
- * (flop_i >= 8192 and N_col >= 8192) -- use the two-phase calls for such
+ * Errors: SPG_ERR_OVERFLOW when a row needs a table beyond 16384 slots
+ * (min(flop_i, N_col) > 8192) -- use the two-phase calls for such
  * matrices; SPG_ERR_WORKSPACE when flop * 12 bytes cannot be allocated. */
 spg_status spg_onephase(spg_ctx *ctx, const spg_csr *A, const spg_csr *B, int64_t *C_row_ptr,
                         int64_t *nnz_C, int64_t *flop_total, int sorted, void *stream);
@@ -206,6 +211,19 @@ spg_status spg_plan_export(spg_ctx *ctx, int64_t *flop_out, int64_t *tsize_out,
 spg_status spg_rows_to_parts(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
                              int64_t nparts, int64_t *offsets, int64_t *flop_total,
                              void *stream);
+
+/* Bytes-balanced split for the multi-GPU numeric phase (SURVEY.md §8(e):
+ * flop balance leaves the minimal-bytes model imbalanced because nnz(C)
+ * per rank differs): the RowsToThreads rule (Fig:load_balance, P:251-270;
+ * lowbnd P:246) applied to the per-row bytes w_i = 16 + 12 (nnz(a_i) +
+ * flop_i + nnz(c_i)) instead of flop_i.
+ *   row_nnz     : device int64[A.nrows], nnz(c_i) of every row (e.g. the
+ *                 differences of C_row_ptr, gathered from the ranks).
+ *   offsets     : HOST out, int64[nparts + 1].  bytes_total: HOST out (may be
+ *                 NULL).  Blocks for the small device->host read. */
+spg_status spg_rows_to_parts_bytes(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
+                                   const int64_t *row_nnz, int64_t nparts, int64_t *offsets,
+                                   int64_t *bytes_total, void *stream);
 
 /* Masked sum for triangle counting (Sec 5.6; BASELINE config 5):
  * sum over stored C(i,j) with (i,j) in pattern(G) of C(i,j).  Every warp sums
@@ -272,12 +290,13 @@ spg_status spg_degree_relabel(spg_ctx *ctx, const spg_csr *G, int32_t *perm, int
  * MEASUREMENT (not on the product path).  For every row i of A with
  * 0 < 2 nnz(c_i) <= 1024, the row's products are inserted (keys only, in the
  * numeric phase's order) into a table of T = lowest 2^n >= 2 nnz(c_i) slots
- * three times: mode 0 linear probing on the high bits of col * H (the build,
+ * four times: mode 0 linear probing on the high bits of col * H (the build,
  * reading R5), mode 1 linear probing on the low bits (the literal remainder),
- * mode 2 4-slot chunks (HashVector-style; a probe = one chunk).
+ * mode 2 4-slot chunks (HashVector-style; a probe = one chunk),
+ * mode 3 32-slot warp buckets (a probe = one bucket read by the warp).
  *   A, B      : device CSR (values unused); C_row_ptr: device int64[A.nrows+1]
  *               from spg_symbolic on the same A, B.
- *   out       : HOST int64[9]: out[3m] = probes, out[3m+1] = products,
+ *   out       : HOST int64[12]: out[3m] = probes, out[3m+1] = products,
  *               out[3m+2] = keys inserted (= sum of nnz(c_i) over those rows).
  * Synchronizes `stream`. */
 spg_status spg_probe_stats(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,

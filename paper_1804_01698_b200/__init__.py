@@ -9,10 +9,11 @@ from .api import (Context, DeviceCSR, default_context, mask_sum, plan_export,  #
                   row_blocks_by_bytes, rows_to_parts, spg_numeric, spg_symbolic, spgemm,
                   triangle_count, triangle_count_rows, validate, masked_sum,
                   triangle_count_fused, degree_relabel, triangle_count_graph,
-                  probe_stats, masked_sum_int, spgemm_onephase)
+                  probe_stats, masked_sum_int, spgemm_onephase, rows_to_parts_bytes)
 from . import _lib  # noqa: F401
 
 __all__ = ["Context", "DeviceCSR", "default_context", "spgemm", "spg_symbolic", "spg_numeric",
            "plan_export", "rows_to_parts", "mask_sum", "validate", "triangle_count",
            "row_blocks_by_bytes", "triangle_count_rows", "masked_sum", "triangle_count_fused",
-           "degree_relabel", "triangle_count_graph", "probe_stats", "masked_sum_int", "spgemm_onephase"]
+           "degree_relabel", "triangle_count_graph", "probe_stats", "masked_sum_int", "spgemm_onephase",
+           "rows_to_parts_bytes"]

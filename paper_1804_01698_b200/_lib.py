@@ -24,7 +24,7 @@ EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_co
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
            "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel",
            "spg_probe_stats", "spg_masked_sum_int", "spg_set_accumulator", "spg_onephase",
-           "spg_onephase_emit")
+           "spg_onephase_emit", "spg_rows_to_parts_bytes")
 
 
 class spg_csr(ct.Structure):
@@ -81,9 +81,10 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_debug_counters.argtypes = [vp, i64p, vp]
     lib.spg_masked_sum.argtypes = [vp, csrp, csrp, csrp, i64, ct.POINTER(ct.c_double), vp]
     lib.spg_masked_sum_int.argtypes = [vp, csrp, csrp, csrp, i64, i64p, vp]
-    lib.spg_set_accumulator.argtypes = [vp, ct.c_int, ct.c_double]
+    lib.spg_set_accumulator.argtypes = [vp, ct.c_int, ct.c_double, ct.c_double]
     lib.spg_onephase.argtypes = [vp, csrp, csrp, vp, i64p, i64p, ct.c_int, vp]
     lib.spg_onephase_emit.argtypes = [vp, vp, vp, vp]
+    lib.spg_rows_to_parts_bytes.argtypes = [vp, csrp, csrp, vp, i64, i64p, i64p, vp]
     lib.spg_degree_relabel.argtypes = [vp, csrp] + [vp] * 11
     lib.spg_probe_stats.argtypes = [vp, csrp, csrp, vp, i64p, vp]
     for name in EXPORTS:
@@ -208,13 +209,24 @@ def spg_onephase(ctx: int, A: spg_csr, B: spg_csr, c_row_ptr: int, sorted: bool,
     return nnz.value, flop.value
 
 
+def spg_rows_to_parts_bytes(ctx: int, A: spg_csr, B: spg_csr, row_nnz: int, nparts: int,
+                            stream: int):
+    off = (ct.c_int64 * (nparts + 1))()
+    tot = ct.c_int64()
+    _check(ctx, "spg_rows_to_parts_bytes",
+           load().spg_rows_to_parts_bytes(ctx, ct.byref(A), ct.byref(B), row_nnz, nparts, off,
+                                          ct.byref(tot), stream))
+    return list(off), tot.value
+
+
 def spg_onephase_emit(ctx: int, c_col: int, c_val: int, stream: int) -> None:
     _check(ctx, "spg_onephase_emit", load().spg_onephase_emit(ctx, c_col, c_val, stream))
 
 
-def spg_set_accumulator(ctx: int, accum: str = "auto", collision_factor: float = 1.3) -> None:
+def spg_set_accumulator(ctx: int, accum: str = "auto", collision_factor: float = 1.3,
+                        heap_cost: float = 8.0) -> None:
     _check(ctx, "spg_set_accumulator",
-           load().spg_set_accumulator(ctx, ACCUM[accum], float(collision_factor)))
+           load().spg_set_accumulator(ctx, ACCUM[accum], float(collision_factor), float(heap_cost)))
 
 
 def spg_masked_sum_int(ctx: int, A: spg_csr, B: spg_csr, G: spg_csr, g_row_begin: int,
@@ -234,7 +246,7 @@ def spg_degree_relabel(ctx: int, G: spg_csr, perm: int, L: tuple, U: tuple, Gn: 
 
 
 def spg_probe_stats(ctx: int, A: spg_csr, B: spg_csr, c_row_ptr: int, stream: int) -> list[int]:
-    out = (ct.c_int64 * 9)()
+    out = (ct.c_int64 * 12)()
     _check(ctx, "spg_probe_stats",
            load().spg_probe_stats(ctx, ct.byref(A), ct.byref(B), c_row_ptr, out, stream))
     return list(out)

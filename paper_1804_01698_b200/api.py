@@ -79,10 +79,12 @@ class Context:
                 pass
             self.handle = None
 
-    def set_accumulator(self, accum: str = "auto", collision_factor: float = 1.3) -> None:
+    def set_accumulator(self, accum: str = "auto", collision_factor: float = 1.3,
+                        heap_cost: float = 8.0) -> None:
         """Sorted-output accumulator: "auto" (cost model Eq:heap_est vs
-        Eq:hash_est per row), "hash" or "heap" (§4.2.3)."""
-        _lib.spg_set_accumulator(self.handle, accum, collision_factor)
+        Eq:hash_est per row, heap steps weighted by heap_cost),
+        "hash" or "heap" (§4.2.3)."""
+        _lib.spg_set_accumulator(self.handle, accum, collision_factor, heap_cost)
 
     @property
     def launches(self) -> int:
@@ -182,6 +184,16 @@ def rows_to_parts(A: DeviceCSR, B: DeviceCSR, nparts: int, ctx: Context | None =
     return _lib.spg_rows_to_parts(ctx.handle, A.c(), B.c(), nparts, _stream())
 
 
+def rows_to_parts_bytes(A: DeviceCSR, B: DeviceCSR, row_nnz: torch.Tensor, nparts: int,
+                        ctx: Context | None = None):
+    """Bytes-balanced split: RowsToThreads on w_i = 16 + 12
+    (nnz(a_i) + flop_i + nnz(c_i)), computed on the GPU; (offsets, total)."""
+    ctx = ctx or default_context()
+    return _lib.spg_rows_to_parts_bytes(ctx.handle, A.c(), B.c(),
+                                        row_nnz.data_ptr() if row_nnz.numel() else 0, nparts,
+                                        _stream())
+
+
 def mask_sum(C: DeviceCSR, G: DeviceCSR, g_row_begin: int = 0, ctx: Context | None = None) -> int:
     ctx = ctx or default_context()
     return _lib.spg_mask_sum(ctx.handle, C.c(), G.c(), g_row_begin, _stream())
@@ -266,7 +278,7 @@ def probe_stats(A: DeviceCSR, B: DeviceCSR, ctx: Context | None = None) -> dict:
     ctx = ctx or default_context()
     rp, _, _ = spg_symbolic(A, B, ctx)
     o = _lib.spg_probe_stats(ctx.handle, A.c(), B.c(), rp.data_ptr(), _stream())
-    names = ("linear_high_bits", "linear_low_bits", "chunk4_high_bits")
+    names = ("linear_high_bits", "linear_low_bits", "chunk4_high_bits", "bucket32_warp")
     return {n: (o[3 * m], o[3 * m + 1], o[3 * m + 2], o[3 * m] / max(o[3 * m + 1], 1))
             for m, n in enumerate(names)}
 
@@ -295,9 +307,10 @@ def row_blocks_by_bytes(A: DeviceCSR, B: DeviceCSR, budget_entries: int,
 
 def triangle_count_rows(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, r0: int, r1: int,
                         sorted: bool = False, block_entries: int | None = None,
-                        ctx: Context | None = None) -> int:
+                        ctx: Context | None = None, g_shift: int = 0) -> int:
     """sum(C o G) over rows [r0, r1) of C = L*U, produced and consumed in row
-    blocks (row-range views of L) so C never has to fit whole in HBM."""
+    blocks (row-range views of L) so C never has to fit whole in HBM.  Row i
+    of L is row g_shift + i of G (a row-scattered L block)."""
     ctx = ctx or default_context()
     if r1 <= r0:
         return 0
@@ -312,7 +325,7 @@ def triangle_count_rows(L: DeviceCSR, U: DeviceCSR, G: DeviceCSR, r0: int, r1: i
     total = 0
     for b0, b1 in zip(offs[:-1], offs[1:]):
         C = spgemm(Lr.rows(b0, b1), U, sorted, ctx)
-        total += mask_sum(C, G, r0 + b0, ctx)
+        total += mask_sum(C, G, g_shift + r0 + b0, ctx)
         del C
     return total
 

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_
     const int i = rows[r];
     const int64_t rp0 = ONEP ? op.fofs[i] : c_rp[i];
     int nnz = ONEP ? 0 : (int)(c_rp[i + 1] - rp0);
-    const int logT = ONEP ? sym_log2_gpu(flop[i], B.ncols) : num_log2(nnz);
+    const int logT = ONEP ? onep_log2(flop[i], B.ncols) : num_log2(nnz);
     const int T = 1 << logT;
     for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
     __syncwarp();
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
     const int i = rows[r];
     const int64_t rp0 = ONEP ? op.fofs[i] : c_rp[i];
     int nnz = ONEP ? 0 : (int)(c_rp[i + 1] - rp0);
-    const int logT = ONEP ? sym_log2_gpu(flop[i], B.ncols) : num_log2(nnz);
+    const int logT = ONEP ? onep_log2(flop[i], B.ncols) : num_log2(nnz);
     const int T = 1 << logT;
     for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
     if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256) k_flop_stats(DevCSR A, int64_t ncols,
     sum += (unsigned long long)f;
     mx = (unsigned long long)f > mx ? (unsigned long long)f : mx;
     mxa = (unsigned long long)na > mxa ? (unsigned long long)na : mxa;
-    if (count_bins) atomicAdd(&s_bins[sym_bin(f, ncols, na)], 1u);
+    if (count_bins) atomicAdd(&s_bins[count_bins == 2 ? onep_bin(f, ncols, na) : sym_bin(f, ncols, na)], 1u);
   }
   sum = warp_sum(sum);
   for (int o = 16; o > 0; o >>= 1) {
@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
                                                      int32_t *__restrict__ rows_out,
                                                      int64_t *__restrict__ row_nnz,
                                                      const int64_t *__restrict__ flop = nullptr,
-                                                     int accum = ACC_HASH, float cfac = 1.0f) {
+                                                     int accum = ACC_HASH, float cfac = 1.0f,
+                                                     float hfac = 1.0f) {
   // mode 1: rows the heap tier takes (heap_pick) go to the BACK of their
   // bin's segment, the others to the front
   __shared__ unsigned s_cnt[kMaxBins], s_hcnt[kMaxBins];
@@ -346,24 +347,25 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const int64_t *_
   bool hp = false;
   unsigned local = 0;
   if (i < m) {
-    if (mode == 0) {
-      b = sym_bin(key[i], ncols, arp[i + 1] - arp[i]);
+    if (mode == 0 || mode == 2) {  // symbolic bins / one-phase bins (by flop)
+      b = mode == 0 ? sym_bin(key[i], ncols, arp[i + 1] - arp[i])
+                    : onep_bin(key[i], ncols, arp[i + 1] - arp[i]);
       if (b == SB_SKIP) row_nnz[i] = 0;
     } else {
       const int64_t nz = key[i + 1] - key[i], na = arp[i + 1] - arp[i];
       b = num_bin(nz, na);
-      hp = flop != nullptr && heap_pick(b, flop[i], na, nz, accum, cfac, info->b_unsorted == 0);
+      hp = flop != nullptr && heap_pick(b, flop[i], na, nz, accum, cfac, info->b_unsorted == 0, hfac);
     }
     if (b != 0) local = atomicAdd(hp ? &s_hcnt[b] : &s_cnt[b], 1u);
   }
   __syncthreads();
   const int t = threadIdx.x;
   if (t > 0 && t < kMaxBins && (s_cnt[t] || s_hcnt[t])) {
-    const unsigned long long *cnt = mode == 0 ? info->sym_count : info->num_count;
+    const unsigned long long *cnt = mode != 1 ? info->sym_count : info->num_count;
     unsigned long long off = 0;
     for (int u = 1; u < t; ++u) off += cnt[u];
     if (s_cnt[t])
-      s_base[t] = off + atomicAdd(&(mode == 0 ? info->cursor : info->num_cursor)[t],
+      s_base[t] = off + atomicAdd(&(mode != 1 ? info->cursor : info->num_cursor)[t],
                                   (unsigned long long)s_cnt[t]);
     if (s_hcnt[t])
       s_hbase[t] = off + cnt[t] - atomicAdd(&info->heap_cursor[t], (unsigned long long)s_hcnt[t]) -
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
                                                             const int64_t *__restrict__ arp,
                                                             const int64_t *__restrict__ flop = nullptr,
                                                             int accum = ACC_HASH,
-                                                            float cfac = 1.0f) {
+                                                            float cfac = 1.0f, float hfac = 1.0f) {
   __shared__ long long s_warp[33];
   __shared__ unsigned s_bins[kMaxBins], s_hbins[kMaxBins];
   __shared__ unsigned long long s_max;
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(int64_t *__restrict_
       const int64_t na = arp[base + t + 1] - arp[base + t];
       const int b = num_bin(v[t], na);
       atomicAdd(&s_bins[b], 1u);
-      if (flop && heap_pick(b, flop[base + t], na, v[t], accum, cfac, b_sorted))
+      if (flop && heap_pick(b, flop[base + t], na, v[t], accum, cfac, b_sorted, hfac))
         atomicAdd(&s_hbins[b], 1u);
     }
   long long tot;
@@ -618,6 +620,17 @@ __global__ void __launch_bounds__(256) k_parts_scatter(const int4 *__restrict__ 
     out[2 * (int64_t)d] = v;
     out[2 * (int64_t)d + 1] = v1;
   }
+}
+
+// Bytes weight of every row for the bytes-balanced split:
+// w_i = 16 + 12 (nnz(a_i) + flop_i + nnz(c_i)) -- the row's share of the
+// minimal-bytes model (A row, gathered B rows, C row).
+__global__ void __launch_bounds__(256) k_row_bytes(const int64_t *__restrict__ arp,
+                                                   const int64_t *__restrict__ flop,
+                                                   const int64_t *__restrict__ cnnz, int64_t m,
+                                                   int64_t *__restrict__ w) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+    w[i] = 16 + 12 * ((arp[i + 1] - arp[i]) + flop[i] + cnnz[i]);
 }
 
 // ---------------------------------------------------------------------------

@@ -10,6 +10,9 @@
 //   mode 1: linear probing, slot = LOW bits of col * H (the literal remainder)
 //   mode 2: 4-slot chunks (HashVector-style), chunk = high bits;
 //           a probe = one chunk read
+//   mode 3: 32-slot warp buckets (warp_bucket_insert, symbolic.cuh): the
+//           warp probes one key at a time, a probe = one bucket read (one
+//           slot per lane + ballots)
 // and the probes of every insert are counted.  out[3 m] = probes, out[3 m + 1]
 // = products, out[3 m + 2] = new keys (must equal nnz(C) of the rows).
 #pragma once
@@ -66,7 +69,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_probe_stats(DevCSR A, DevCSR B,
   __shared__ uint32_t s_tab[WARPS][kProbeTMax];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *tab = s_tab[w];
-  unsigned long long acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t i = int64_t(blockIdx.x) * WARPS + w; i < A.nrows; i += int64_t(gridDim.x) * WARPS) {
     const int64_t nnz = c_rp[i + 1] - c_rp[i];
     if (nnz == 0 || 2 * nnz > kProbeTMax) continue;
@@ -102,9 +105,26 @@ __global__ void __launch_bounds__(WARPS * 32) k_probe_stats(DevCSR A, DevCSR B,
     run(std::integral_constant<int, 0>());
     run(std::integral_constant<int, 1>());
     run(std::integral_constant<int, 2>());
+    {  // mode 3: warp buckets (every lane ends with the warp's counts)
+      for (int s = lane; s < T; s += 32) tab[s] = kEmpty;
+      __syncwarp();
+      unsigned long long pr = 0, np = 0, nk = 0;
+      auto ins = [&](bool act, uint32_t c, double) {
+        np += (unsigned long long)__popc(__ballot_sync(kFull, act));
+        nk += (unsigned long long)warp_bucket_insert(tab, logT, act, c, &pr);
+      };
+      if (seq) for_row<true, false, 2>(A, B, as, ae, 0, 1, ins);
+      else for_row<false, false, 2>(A, B, as, ae, 0, 1, ins);
+      __syncwarp();
+      if (lane == 0) {  // (warp-level counts: once per warp)
+        acc[9] += pr;
+        acc[10] += np;
+        acc[11] += nk;
+      }
+    }
   }
 #pragma unroll
-  for (int m = 0; m < 9; ++m) {
+  for (int m = 0; m < 12; ++m) {
     const unsigned long long v = warp_sum(acc[m]);
     if (lane == 0 && v) atomicAdd(out + m, v);
   }

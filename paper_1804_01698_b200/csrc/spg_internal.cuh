@@ -147,21 +147,44 @@ __device__ __forceinline__ int num_bin(int64_t nnz, int64_t na) {
 // heap merge when the paper's cost model says so (accumulator mode AUTO):
 //   T_heap = flop_i * log2 nnz(a_i)                          (Eq:heap_est)
 //   T_hash = flop_i * c + nnz(c_i) * log2 nnz(c_i)           (Eq:hash_est)
-// with c the collision factor (measured: DESIGN.md §9c).  Mode HASH never,
-// HEAP always (for the eligible rows).
+// with c the collision factor (measured: DESIGN.md §9c) and T_heap scaled by
+// h, the cost of one heap step relative to one hash probe on this GPU
+// (measured on B200; h = 1 is the paper's unit-cost model).
+// Mode HASH never, HEAP always (for the eligible rows).
 enum AccumMode { ACC_AUTO = 0, ACC_HASH = 1, ACC_HEAP = 2 };
 constexpr int kHeapMax = 16;
 constexpr int64_t kHeapMaxFlop = 2048;  // bounds one thread's serial merge
 
 __device__ __forceinline__ bool heap_pick(int bin, int64_t flop, int64_t na, int64_t nnz,
-                                          int accum, float cfac, bool b_sorted) {
+                                          int accum, float cfac, bool b_sorted, float hfac) {
   if (accum == ACC_HASH || !b_sorted || nnz <= 0 || na > kHeapMax || flop > kHeapMaxFlop ||
       (bin != NB_W256 && bin != NB_W1024))
     return false;
   if (accum == ACC_HEAP) return true;
-  const float th = (float)flop * log2f((float)na);
+  const float th = hfac * (float)flop * log2f((float)na);
   const float tc = (float)flop * cfac + (float)nnz * log2f((float)nnz);
   return th < tc;
+}
+
+// One-phase tables (spg_onephase): T = lowest 2^n >= 2 min(flop_i, ncols)
+// -- the flop bound stands in for nnz(c_i) in the numeric rule (load <= 1/2,
+// reading R6; the sorted emits use the free upper half as scratch) -- binned
+// like the symbolic tiers: W128 / W1024 / B2K..B16K; larger -> SB_G (the
+// one-phase path refuses those rows).
+__device__ __forceinline__ int onep_log2(int64_t flop, int64_t ncols) {
+  const int64_t s = flop < ncols ? flop : ncols;
+  const int n = log2_ceil64(uint64_t(2 * s));
+  return n < kMinLogT ? kMinLogT : n;
+}
+
+__device__ __forceinline__ int onep_bin(int64_t flop, int64_t ncols, int64_t na) {
+  if (flop == 0) return SB_SKIP;
+  const int n = onep_log2(flop, ncols);
+  if (na > kWarpMaxEntries && n <= 10) return SB_B2K;
+  if (n <= 7) return SB_W128;
+  if (n <= 10) return SB_W1024;
+  if (n <= 14) return SB_B2K + (n - 11);
+  return SB_G;
 }
 
 // Fibonacci hashing: HIGH bits of col*H (reading R5 of DESIGN.md; the paper's

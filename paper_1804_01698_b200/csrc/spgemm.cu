@@ -45,7 +45,7 @@ struct spg_ctx {
   Buf parts, parts2, part_hist, toff;  // column-tile parts of long rows (BM tier), sorted copy, B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
-  Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (keys, ranks, unsorted rows, CUB temp)
+  Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (histograms, ranks/buckets, unsorted rows)
   Buf mask_rows;                     // row lists of the mask-and-sum tiers
   Buf useful_bits;                   // useful-entry bitmask of k_flop_nz (pruning), grow-only
   Buf one_fofs, one_col, one_val;    // one-phase: flop prefix, flop-sized row workspace (grow-only)
@@ -65,6 +65,7 @@ struct spg_ctx {
   int tune = 0;    // SPG_TUNE=<bits>: kernel variant switches for A/B measurements (default 0)
   int accum = ACC_AUTO;   // accumulator choice for sorted output (spg_set_accumulator)
   float cfac = 1.3f;      // collision factor c of Eq:hash_est (measured)
+  float hfac = 8.0f;      // heap step cost / hash probe cost on B200 (measured)
   // optional per-launch timing (events on the stream each kernel runs on)
   int profiling = 0;
   struct Rec { const char *name; cudaEvent_t a, b; };
@@ -254,7 +255,7 @@ spg_status launch_scan(spg_ctx *c, int64_t *data, int64_t n, cudaStream_t s,
   {
     ProfScope _ps(c, s, "k_scan_down");
     k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(data, n, partial, (PlanInfo *)c->info.p, arp,
-                                                      flop, c->accum, c->cfac);
+                                                      flop, c->accum, c->cfac, c->hfac);
   }
   SPG_LAUNCHED(c, "k_scan_down");
   return SPG_OK;
@@ -344,7 +345,9 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_num_warp<1024, 4, 0, true>, s_num_w1024) == SPG_OK &&
          set_smem(c, k_num_warp<1024, 4, 1, true>, s_num_w1024) == SPG_OK &&
          set_smem(c, k_num_block<128, true>, size_t(2048) * 12) == SPG_OK &&
-         set_smem(c, k_num_block<512, true>, size_t(8192) * 12) == SPG_OK;
+         set_smem(c, k_num_block<512, true>, size_t(8192) * 12) == SPG_OK &&
+         set_smem(c, k_num_block<1024, true>, size_t(16384) * 12) == SPG_OK &&
+         set_smem(c, k_segsort_long<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK;
   }
   if (!ok) {
     cudaGetLastError();
@@ -594,15 +597,23 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       cudaStream_t ss = c->serial ? s : c->sub[sidx++ % kSubStreams];
       if (bin == SB_W128 || bin == SB_W1024) {
         const int64_t grid = std::min<int64_t>(ceil_div(n, kWarps), int64_t(c->num_sms) * 32);
+        // SPG_TUNE bit 128: HashVector-style warp-bucket probing (A/B)
+        const bool bucket = (c->tune & 128) != 0;
         if (bin == SB_W128)
           {
             ProfScope _ps(c, ss, "k_sym_warp<128>");
-            k_sym_warp<128, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 128 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
+            if (bucket)
+              k_sym_warp<128, kWarps, true><<<(unsigned)grid, kWarps * 32, kWarps * 128 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
+            else
+              k_sym_warp<128, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 128 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
           }
         else
           {
             ProfScope _ps(c, ss, "k_sym_warp<1024>");
-            k_sym_warp<1024, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 1024 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
+            if (bucket)
+              k_sym_warp<1024, kWarps, true><<<(unsigned)grid, kWarps * 32, kWarps * 1024 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
+            else
+              k_sym_warp<1024, kWarps><<<(unsigned)grid, kWarps * 32, kWarps * 1024 * 4, ss>>>(rb, n, a, b, flop, row_nnz);
           }
         SPG_LAUNCHED(c, "k_sym_warp");
       } else if (bin >= SB_B2K && bin <= SB_B32K) {
@@ -674,7 +685,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, C_row_ptr, A->row_ptr, 0, 1, info,
                                                                (int32_t *)c->rows_num.p, nullptr,
                                                                (const int64_t *)c->flop.p, c->accum,
-                                                               c->cfac);
+                                                               c->cfac, c->hfac);
     }
     SPG_LAUNCHED(c, "k_bin_scatter(num)");
   }
@@ -870,14 +881,17 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   return join(c, s);
 }
 
-spg_status spg_set_accumulator(spg_ctx *c, int accum, double collision_factor) {
+spg_status spg_set_accumulator(spg_ctx *c, int accum, double collision_factor, double heap_cost) {
   if (!c) return SPG_ERR_INVALID_ARG;
   if (accum < SPG_ACCUM_AUTO || accum > SPG_ACCUM_HEAP)
     return fail(c, SPG_ERR_INVALID_ARG, "accumulator must be SPG_ACCUM_AUTO, _HASH or _HEAP");
   if (!(collision_factor >= 1.0) || collision_factor > 1e6)
     return fail(c, SPG_ERR_INVALID_ARG, "collision factor must be >= 1");
+  if (!(heap_cost > 0.0) || heap_cost > 1e6)
+    return fail(c, SPG_ERR_INVALID_ARG, "heap cost must be > 0");
   c->accum = accum;
   c->cfac = (float)collision_factor;
+  c->hfac = (float)heap_cost;
   return SPG_OK;
 }
 
@@ -909,12 +923,12 @@ spg_status spg_onephase(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
     SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, size_t(m + 1) * 8, s));
     if (m > 0 && B->nrows > 0) {
-      // a1 + a2: flop, symbolic bins (the tables are sized by the flop bound)
-      if ((st = launch_flop(c, A, B, 1, s)) != SPG_OK) return st;
+      // a1 + a2: flop, one-phase bins (the tables are sized by the flop bound)
+      if ((st = launch_flop(c, A, B, 2, s)) != SPG_OK) return st;
       {
-        ProfScope _ps(c, s, "k_bin_scatter_sym");
+        ProfScope _ps(c, s, "k_bin_scatter_1p");
         k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, (const int64_t *)c->flop.p, A->row_ptr,
-                                                                 B->ncols, 0, info, (int32_t *)c->rows_sym.p,
+                                                                 B->ncols, 2, info, (int32_t *)c->rows_sym.p,
                                                                  row_nnz);
       }
       SPG_LAUNCHED(c, "k_bin_scatter(sym)");
@@ -948,15 +962,18 @@ spg_status spg_onephase(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
             k_num_warp<1024, 4, 0, true><<<gw, 4 * 32, 4 * 1024 * 16, s>>>(rows, 0, a, b, flop, nullptr, tc, tv, op);
         }
         SPG_LAUNCHED(c, "k_num_warp(1p)");
-        for (int bin = SB_B2K; bin <= SB_B8K; ++bin) {
+        for (int bin = SB_B2K; bin <= SB_B16K; ++bin) {
           op.bin = bin;
           const int tmax = 2048 << (bin - SB_B2K);
           ProfScope _ps(c, s, "k_num_block(1p)");
           if (tmax == 2048)
             k_num_block<128, true><<<(unsigned)(c->num_sms * 8), 128, size_t(tmax) * 12, s>>>(
                 rows, 0, a, b, flop, nullptr, tc, tv, sorted, tmax, op);
-          else
+          else if (tmax <= 8192)
             k_num_block<512, true><<<(unsigned)(c->num_sms * 4), 512, size_t(tmax) * 12, s>>>(
+                rows, 0, a, b, flop, nullptr, tc, tv, sorted, tmax, op);
+          else
+            k_num_block<1024, true><<<(unsigned)(c->num_sms), 1024, size_t(tmax) * 12, s>>>(
                 rows, 0, a, b, flop, nullptr, tc, tv, sorted, tmax, op);
           SPG_LAUNCHED(c, "k_num_block(1p)");
         }
@@ -966,9 +983,9 @@ spg_status spg_onephase(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     if ((st = launch_scan(c, row_nnz, m, s)) != SPG_OK) return st;
     if ((st = read_info(c, s)) != SPG_OK) return st;  // the one host round trip
     const PlanInfo &h = *c->host_info;
-    if (h.sym_count[SB_B16K] || h.sym_count[SB_B32K] || h.sym_count[SB_G] || h.sym_count[SB_BM])
+    if (h.sym_count[SB_G])
       return fail(c, SPG_ERR_OVERFLOW,
-                  "one-phase: rows need tables beyond 8192 slots (flop_i >= 8192); use "
+                  "one-phase: rows need tables beyond 16384 slots (min(flop_i, N_col) > 8192); use "
                   "spg_symbolic + spg_numeric");
     if ((int64_t)h.max_brow > kMaxBRow) return fail(c, SPG_ERR_OVERFLOW, "a row of B has more than 2^26 entries");
     if (h.flop_total <= cap || h.flop_total == 0) {
@@ -1068,6 +1085,53 @@ spg_status spg_rows_to_parts(spg_ctx *c, const spg_csr *A, const spg_csr *B, int
   SPG_LAUNCHED(c, "k_lowbnd");
   SPG_CUDA(c, cudaMemcpyAsync(offsets, doff, size_t(nparts + 1) * 8, cudaMemcpyDeviceToHost, s));
   if (flop_total) SPG_CUDA(c, cudaMemcpyAsync(flop_total, ps + m, 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaStreamSynchronize(s));
+  return SPG_OK;
+}
+
+spg_status spg_rows_to_parts_bytes(spg_ctx *c, const spg_csr *A, const spg_csr *B,
+                                   const int64_t *row_nnz, int64_t nparts, int64_t *offsets,
+                                   int64_t *bytes_total, void *stream) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  spg_status st;
+  if ((st = check_csr(c, A, "A", false)) != SPG_OK) return st;
+  if ((st = check_csr(c, B, "B", false)) != SPG_OK) return st;
+  if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
+  if (nparts < 1 || !offsets) return fail(c, SPG_ERR_INVALID_ARG, "nparts < 1 or offsets NULL");
+  const int64_t m = A->nrows;
+  if (m > 0 && !row_nnz) return fail(c, SPG_ERR_INVALID_ARG, "row_nnz is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  SPG_CUDA(c, cudaSetDevice(c->device));
+  c->have_plan = false;  // the flop buffer is reused
+  if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->flop, size_t(m + 1) * 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->scratch, size_t(m + 1 + nparts + 1) * 8, s)) != SPG_OK) return st;
+  PlanInfo *info = (PlanInfo *)c->info.p;
+  int64_t *ps = (int64_t *)c->scratch.p;
+  int64_t *doff = ps + (m + 1);
+  SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
+  SPG_CUDA(c, cudaMemsetAsync(ps, 0, size_t(m + 1) * 8, s));
+  if (m > 0) {
+    if (B->nrows > 0) {
+      if ((st = launch_flop(c, A, B, 0, s)) != SPG_OK) return st;
+    } else {
+      SPG_CUDA(c, cudaMemsetAsync(c->flop.p, 0, size_t(m) * 8, s));
+    }
+    {
+      ProfScope _ps(c, s, "k_row_bytes");
+      k_row_bytes<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), int64_t(c->num_sms) * 8), 256, 0, s>>>(
+          A->row_ptr, (const int64_t *)c->flop.p, row_nnz, m, ps + 1);
+    }
+    SPG_LAUNCHED(c, "k_row_bytes");
+    if ((st = launch_scan(c, ps + 1, m, s)) != SPG_OK) return st;
+  }
+  {
+    ProfScope _ps(c, s, "k_lowbnd");
+    k_lowbnd<<<(unsigned)ceil_div(nparts + 1, 256), 256, 0, s>>>(ps, m, nparts, doff);
+  }
+  SPG_LAUNCHED(c, "k_lowbnd");
+  SPG_CUDA(c, cudaMemcpyAsync(offsets, doff, size_t(nparts + 1) * 8, cudaMemcpyDeviceToHost, s));
+  if (bytes_total) SPG_CUDA(c, cudaMemcpyAsync(bytes_total, ps + m, 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
   return SPG_OK;
 }
@@ -1218,42 +1282,54 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
   SPG_CUDA(c, cudaMemsetAsync(G_rp, 0, 8, s));
   if (n == 0) return SPG_OK;
   if ((st = buf_ensure(c, c->info, sizeof(PlanInfo), s)) != SPG_OK) return st;
-  if ((st = buf_ensure(c, c->rl_key, size_t(n) * 16, s)) != SPG_OK) return st;
-  if ((st = buf_ensure(c, c->rl_rank, size_t(n) * 4, s)) != SPG_OK) return st;
+  // rl_key: degree histogram / fill counters (int64[n+1] each), bucket offsets
+  // int64[n+2] (degrees 0..n; n only with an invalid diagonal entry);
+  // rl_rank: rank int32[n] + degree buckets int32[n] + long-segment list int32[n]
+  if ((st = buf_ensure(c, c->rl_key, size_t(n + 1) * 24 + 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->rl_rank, size_t(n) * 12, s)) != SPG_OK) return st;
   if ((st = buf_ensure(c, c->rl_tmp, size_t(std::max<int64_t>(nnz, 1)) * 8, s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
   unsigned long long *bad = &info->mask_ctr[0];
-  SPG_CUDA(c, cudaMemsetAsync(bad, 0, 8, s));
-  unsigned long long *key = (unsigned long long *)c->rl_key.p, *skey = key + n;
-  int32_t *rank = (int32_t *)c->rl_rank.p;
+  unsigned long long *nlong = &info->mask_ctr[1];
+  SPG_CUDA(c, cudaMemsetAsync(info->mask_ctr, 0, 16, s));
+  unsigned long long *hist = (unsigned long long *)c->rl_key.p, *fill = hist + (n + 1);
+  int64_t *dstart = (int64_t *)(fill + (n + 1));
+  int32_t *rank = (int32_t *)c->rl_rank.p, *bucket = rank + n, *longs = bucket + n;
   int32_t *Lt = (int32_t *)c->rl_tmp.p, *Ut = Lt + nnz / 2, *Gt = Lt + nnz;
-  // CUB temporary storage: the max over the calls below
-  int end_bit = 32;
-  while (end_bit < 64 && (1ull << (end_bit - 32)) <= (unsigned long long)n) ++end_bit;  // deg <= n - 1
-  size_t t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-  SPG_CUDA(c, cub::DeviceRadixSort::SortKeys(nullptr, t0, key, skey, (int)n, 0, end_bit, s));
-  SPG_CUDA(c, cub::DeviceScan::InclusiveSum(nullptr, t1, L_rp + 1, L_rp + 1, (int)n, s));
-  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(nullptr, t2, Gt, G_col, (int)nnz, (int)n, G_rp,
-                                                 G_rp + 1, s));
-  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(nullptr, t3, Lt, L_col, (int)(nnz / 2), (int)n,
-                                                 L_rp, L_rp + 1, s));
-  const size_t tb = std::max(std::max(t0, t1), std::max(t2, t3));
-  if ((st = buf_ensure(c, c->rl_cub, tb, s)) != SPG_OK) return st;
-  size_t tbytes = c->rl_cub.bytes;
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), int64_t(c->num_sms) * 8);
   const unsigned wgrid = (unsigned)std::min<int64_t>(ceil_div(n, 8), int64_t(c->num_sms) * 16);
+  const int lwords = (int)std::min<int64_t>((n + 31) / 32, kBitmapMaxCols / 32);
+  const size_t lsmem = size_t(lwords) * 4;
+  // segmented sort of distinct ids (ascending) of [seg[i], seg[i+1]), i < nseg
+  auto segsort = [&](const int32_t *in, int32_t *out, const int64_t *seg, int64_t nseg) -> spg_status {
+    if (nseg <= 0) return SPG_OK;
+    SPG_CUDA(c, cudaMemsetAsync(nlong, 0, 8, s));
+    k_segsort_warp<8><<<(unsigned)std::min<int64_t>(ceil_div(nseg, 8), int64_t(c->num_sms) * 8), 256, 0, s>>>(
+        in, out, seg, nseg, longs, nlong);
+    SPG_LAUNCHED(c, "k_segsort_warp");
+    k_segsort_long<1024><<<(unsigned)c->num_sms, 1024, lsmem, s>>>(in, out, seg, longs, nlong, n, lwords);
+    SPG_LAUNCHED(c, "k_segsort_long");
+    return SPG_OK;
+  };
   DevCSR g = dev(G);
-  k_rl_keys<<<grid, 256, 0, s>>>(g, key);
-  SPG_LAUNCHED(c, "k_rl_keys");
-  SPG_CUDA(c, cub::DeviceRadixSort::SortKeys(c->rl_cub.p, tbytes, key, skey, (int)n, 0, end_bit, s));
-  k_rl_rank<<<grid, 256, 0, s>>>(skey, n, perm, rank);
+  // vertex order (deg(v), v): counting sort by degree, then each degree
+  // bucket sorted by id
+  SPG_CUDA(c, cudaMemsetAsync(hist, 0, size_t(n + 1) * 16, s));  // hist + fill
+  k_rl_deghist<<<grid, 256, 0, s>>>(g, hist);
+  SPG_LAUNCHED(c, "k_rl_deghist");
+  SPG_CUDA(c, cudaMemsetAsync(dstart, 0, 8, s));
+  SPG_CUDA(c, cudaMemcpyAsync(dstart + 1, hist, size_t(n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  if ((st = launch_scan(c, dstart + 1, n + 1, s)) != SPG_OK) return st;  // bucket offsets (degrees 0..n)
+  k_rl_degscatter<<<grid, 256, 0, s>>>(g, dstart, fill, bucket);
+  SPG_LAUNCHED(c, "k_rl_degscatter");
+  if ((st = segsort(bucket, rank, dstart, n + 1)) != SPG_OK) return st;  // (rank: the sorted ids, temporarily)
+  k_rl_rank<<<grid, 256, 0, s>>>(rank, n, perm, bucket);             // bucket <- rank[v]
   SPG_LAUNCHED(c, "k_rl_rank");
-  k_rl_count<<<wgrid, 256, 0, s>>>(g, perm, rank, L_rp + 1, U_rp + 1, G_rp + 1, bad);
+  int32_t *rk = bucket;
+  k_rl_count<<<wgrid, 256, 0, s>>>(g, perm, rk, L_rp + 1, U_rp + 1, G_rp + 1, bad);
   SPG_LAUNCHED(c, "k_rl_count");
-  for (int64_t *rp : {L_rp, U_rp, G_rp}) {
-    tbytes = c->rl_cub.bytes;
-    SPG_CUDA(c, cub::DeviceScan::InclusiveSum(c->rl_cub.p, tbytes, rp + 1, rp + 1, (int)n, s));
-  }
+  for (int64_t *rp : {L_rp, U_rp, G_rp})
+    if ((st = launch_scan(c, rp + 1, n, s)) != SPG_OK) return st;
   int64_t tail[3];
   SPG_CUDA(c, cudaMemcpyAsync(&tail[0], L_rp + n, 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaMemcpyAsync(&tail[1], U_rp + n, 8, cudaMemcpyDeviceToHost, s));
@@ -1264,17 +1340,11 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
                 "G is not a symmetric pattern without diagonal (lower/upper counts differ or a "
                 "diagonal entry is present)");
   if (nnz == 0) return SPG_OK;
-  k_rl_fill<<<wgrid, 256, 0, s>>>(g, perm, rank, L_rp, U_rp, G_rp, Lt, Ut, Gt);
+  k_rl_fill<<<wgrid, 256, 0, s>>>(g, perm, rk, L_rp, U_rp, G_rp, Lt, Ut, Gt);
   SPG_LAUNCHED(c, "k_rl_fill");
-  tbytes = c->rl_cub.bytes;
-  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->rl_cub.p, tbytes, Gt, G_col, (int)nnz, (int)n,
-                                                 G_rp, G_rp + 1, s));
-  tbytes = c->rl_cub.bytes;
-  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->rl_cub.p, tbytes, Lt, L_col, (int)(nnz / 2),
-                                                 (int)n, L_rp, L_rp + 1, s));
-  tbytes = c->rl_cub.bytes;
-  SPG_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->rl_cub.p, tbytes, Ut, U_col, (int)(nnz / 2),
-                                                 (int)n, U_rp, U_rp + 1, s));
+  if ((st = segsort(Gt, G_col, G_rp, n)) != SPG_OK) return st;
+  if ((st = segsort(Lt, L_col, L_rp, n)) != SPG_OK) return st;
+  if ((st = segsort(Ut, U_col, U_rp, n)) != SPG_OK) return st;
   const unsigned vgrid = (unsigned)std::min<int64_t>(ceil_div(nnz, 256), int64_t(c->num_sms) * 8);
   if (L_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(L_val, nnz / 2, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
   if (U_val) { k_fill_f64<<<vgrid, 256, 0, s>>>(U_val, nnz / 2, 1.0); SPG_LAUNCHED(c, "k_fill_f64"); }
@@ -1292,15 +1362,15 @@ spg_status spg_probe_stats(spg_ctx *c, const spg_csr *A, const spg_csr *B,
   if (!out || (A->nrows > 0 && !C_row_ptr)) return fail(c, SPG_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   SPG_CUDA(c, cudaSetDevice(c->device));
-  if ((st = buf_ensure(c, c->scratch, 9 * 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->scratch, 12 * 8, s)) != SPG_OK) return st;
   unsigned long long *d = (unsigned long long *)c->scratch.p;
-  SPG_CUDA(c, cudaMemsetAsync(d, 0, 9 * 8, s));
+  SPG_CUDA(c, cudaMemsetAsync(d, 0, 12 * 8, s));
   if (A->nrows > 0) {
     k_probe_stats<kWarps><<<(unsigned)std::min<int64_t>(ceil_div(A->nrows, kWarps), c->num_sms * 16),
                             kWarps * 32, 0, s>>>(dev(A), dev(B), C_row_ptr, d);
     SPG_LAUNCHED(c, "k_probe_stats");
   }
-  SPG_CUDA(c, cudaMemcpyAsync(out, d, 9 * 8, cudaMemcpyDeviceToHost, s));
+  SPG_CUDA(c, cudaMemcpyAsync(out, d, 12 * 8, cudaMemcpyDeviceToHost, s));
   SPG_CUDA(c, cudaStreamSynchronize(s));
   return SPG_OK;
 }

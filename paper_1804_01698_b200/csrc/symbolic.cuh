@@ -405,7 +405,43 @@ __device__ __forceinline__ bool use_seq(int64_t flop, int64_t nnz_a) {
 // ---------------------------------------------------------------------------
 // W tier: one warp per row, warp-private table of T <= TMAX slots in smem.
 // ---------------------------------------------------------------------------
-template <int TMAX, int WARPS>
+// HashVector-style warp-bucket insertion (§4.2.2; SURVEY
+// §8(f) row 2): the table is cut into 32-slot buckets; the warp takes the
+// keys of its lanes one at a time, every lane loads one slot of the key's
+// bucket (hash = high bits of key * H over T / 32 buckets), a ballot finds a
+// hit or the first empty slot ("pushed ... in order from the beginning" of
+// the chunk), a full bucket moves on to the next one (linear probing over
+// buckets).  Warp-private table: no atomics.  Returns the new keys (lane 0).
+// The A/B variant of the scalar linear probing (SPG_TUNE bit 128).
+__device__ __forceinline__ int warp_bucket_insert(uint32_t *tab, int logT, bool act, uint32_t c,
+                                                  unsigned long long *probes = nullptr) {
+  const int lane = lane_id();
+  const uint32_t nbm = (1u << (logT - 5)) - 1u;  // buckets - 1 (logT >= 5)
+  int added = 0;
+  unsigned pend = __ballot_sync(kFull, act);
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const uint32_t key = __shfl_sync(kFull, c, src);
+    uint32_t bk = logT > 5 ? (key * kHashMul) >> (32 - (logT - 5)) : 0u;
+    while (true) {
+      if (probes && lane == 0) ++*probes;
+      const uint32_t k = tab[(bk << 5) + lane];
+      if (__ballot_sync(kFull, k == key)) break;
+      const unsigned emp = __ballot_sync(kFull, k == kEmpty);
+      if (emp) {
+        if (lane == __ffs(emp) - 1) tab[(bk << 5) + lane] = key;
+        ++added;
+        break;
+      }
+      bk = (bk + 1u) & nbm;
+    }
+    __syncwarp();
+  }
+  return added;
+}
+
+template <int TMAX, int WARPS, bool BUCKET = false>
 __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restrict__ rows,
                                                          int64_t nrows, DevCSR A, DevCSR B,
                                                          const int64_t *__restrict__ flop,
@@ -423,11 +459,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) cnt += sym_insert(tab, c, logT);
+      if (BUCKET) cnt += warp_bucket_insert(tab, logT, act, c);
+      else if (act) cnt += sym_insert(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, 2>(A, B, as, ae, 0, 1, ins);
     else for_row<false, false, 2>(A, B, as, ae, 0, 1, ins);
-    cnt = warp_sum(cnt);
+    if (!BUCKET) cnt = warp_sum(cnt);  // (bucket mode: every lane holds the warp's count)
     if (lane == 0) row_nnz[i] = cnt;
     __syncwarp();
   }

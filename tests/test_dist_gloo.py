@@ -82,3 +82,135 @@ def test_spgemm_dist_gloo(tmp_path, world):
     ps = np.r_[0, np.cumsum(f)]
     work = [ps[int(p["r1"])] - ps[int(p["r0"])] for p in parts]
     assert max(work) <= -(-tot // world) + f.max()
+
+
+# ---------------------------------------------------------------- distribute + bytes balance
+def _bytes_weights(A, B):
+    """Per-row bytes of the minimal-bytes model, from the oracle."""
+    import oracle
+    f, _ = oracle.flop(A, B)
+    nnz = oracle.row_nnz(A, B)
+    return 16 + 12 * (np.diff(A.row_ptr) + f + nnz)
+
+
+def _worker_distribute(rank, world, port, result_dir, balance):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    import oracle
+    import synth
+    from paper_1804_01698_b200 import dist as sdist
+    from paper_1804_01698_b200.api import DeviceCSR
+
+    def host_dev(M):
+        return DeviceCSR(M.nrows, M.ncols, torch.from_numpy(M.row_ptr.copy()),
+                         torch.from_numpy(M.col.copy()), torch.from_numpy(M.val.copy()))
+
+    def to_synth(D):
+        return synth.CSR(D.nrows, D.ncols, D.row_ptr.numpy().astype(np.int64),
+                         D.col.numpy().astype(np.int32), D.val.numpy().astype(np.float64))
+
+    L, U, ex = synth.workload("c5_triangle", scale=10)
+    A, B, G = L, U, ex["G"]
+
+    def part(X, Y, n):
+        f, tot = oracle.flop(to_synth(X), to_synth(Y))
+        return oracle.rows_to_threads(f, n).tolist(), tot
+
+    # 1. distribute from rank 0: row blocks of A and G, all of B
+    Al, Bl, Gl, offs = sdist.distribute(host_dev(A) if rank == 0 else None,
+                                        host_dev(B) if rank == 0 else None,
+                                        host_dev(G) if rank == 0 else None,
+                                        device=torch.device("cpu"), partition=part)
+    np.savez(os.path.join(result_dir, f"d{rank}.npz"), arp=Al.row_ptr.numpy(), acol=Al.col.numpy(),
+             aval=Al.val.numpy(), brp=Bl.row_ptr.numpy(), bcol=Bl.col.numpy(), bval=Bl.val.numpy(),
+             grp=Gl.row_ptr.numpy(), gcol=Gl.col.numpy(), offs=np.array(offs))
+
+    # 2. spgemm_dist with the bytes-balanced numeric split (C3-shaped input)
+    A3, B3, _ = synth.workload("c3_rmat20", scale=12)
+    hA, hB = _HostCSR(A3), _HostCSR(B3)
+
+    def part3(X, Y, n):
+        f, tot = oracle.flop(X.M, Y.M)
+        return oracle.rows_to_threads(f, n).tolist(), tot
+
+    def rnnz(X, Y, r0, r1):
+        return torch.from_numpy(oracle.row_nnz(X.M, Y.M, r0, r1).astype(np.int64))
+
+    def pbytes(X, Y, allnnz, n):
+        f, _ = oracle.flop(X.M, Y.M)
+        w = 16 + 12 * (np.diff(X.M.row_ptr) + f + allnnz.numpy())
+        return oracle.rows_to_threads(w, n).tolist()
+
+    def local(X, Y, r0, r1, sorted_):
+        return oracle.spgemm(X.M, Y.M, r0, r1)
+
+    blk = sdist.spgemm_dist(hA, hB, True, partition=part3, local_spgemm=local, balance=balance,
+                            row_nnz=rnnz, partition_bytes=pbytes)
+    rp, col, val = blk.C
+    np.savez(os.path.join(result_dir, f"s{rank}.npz"), rp=rp, col=col, val=val, r0=blk.row_begin,
+             r1=blk.row_end, offs=np.array(blk.offsets))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,balance", [(2, "bytes"), (3, "bytes"), (3, "flop")])
+def test_distribute_and_bytes_balance_gloo(tmp_path, world, balance):
+    import oracle
+    import synth
+    port = _free_port()
+    mp.start_processes(_worker_distribute, args=(world, port, str(tmp_path), balance), nprocs=world,
+                       join=True, start_method="spawn")
+    L, U, ex = synth.workload("c5_triangle", scale=10)
+    G = ex["G"]
+    f, _ = oracle.flop(L, U)
+    offs = oracle.rows_to_threads(f, world).tolist()
+    for r in range(world):
+        d = np.load(tmp_path / f"d{r}.npz")
+        assert d["offs"].tolist() == offs
+        a, b = offs[r], offs[r + 1]
+        s0, s1 = L.row_ptr[a], L.row_ptr[b]
+        assert np.array_equal(d["arp"], L.row_ptr[a:b + 1] - s0)
+        assert np.array_equal(d["acol"], L.col[s0:s1]) and np.array_equal(d["aval"], L.val[s0:s1])
+        assert np.array_equal(d["brp"], U.row_ptr) and np.array_equal(d["bcol"], U.col)
+        g0, g1 = G.row_ptr[a], G.row_ptr[b]
+        assert np.array_equal(d["grp"], G.row_ptr[a:b + 1] - g0)
+        assert np.array_equal(d["gcol"], G.col[g0:g1])
+    # bytes-balanced split: offsets = RowsToThreads on the bytes weights, blocks
+    # concatenate to the oracle's C, and the bytes imbalance is bounded
+    A3, B3, _ = synth.workload("c3_rmat20", scale=12)
+    w = _bytes_weights(A3, B3)
+    want = oracle.rows_to_threads(w if balance == "bytes" else oracle.flop(A3, B3)[0], world).tolist()
+    parts = [np.load(tmp_path / f"s{r}.npz") for r in range(world)]
+    assert parts[0]["offs"].tolist() == want
+    rp, col, val = oracle.spgemm(A3, B3)
+    assert (np.concatenate([p["col"] for p in parts]) == col).all()
+    assert (np.concatenate([p["val"] for p in parts]) == val).all()
+    if balance == "bytes":
+        per = [w[int(p["r0"]):int(p["r1"])].sum() for p in parts]
+        mean = w.sum() / world
+        assert max(per) <= mean + w.max()  # contiguous split: within one row of perfect
+        assert max(per) / mean <= 1.01 + w.max() / mean
+
+
+def test_bytes_split_balance_c3_profile():
+    """on a C3-shaped profile (R-MAT scale 16) the flop split
+    leaves the per-rank minimal bytes uneven; the bytes split (the same
+    lowbnd rule on bytes weights) balances them to <= 1.01 at 2..8 ranks."""
+    import oracle
+    import synth
+    A, B, _ = synth.workload("c3_rmat20", scale=16)
+    w = _bytes_weights(A, B)
+    f, _ = oracle.flop(A, B)
+    worst_flop = 1.0
+    for n in (2, 4, 8):
+        ob = oracle.rows_to_threads(w, n)
+        per_b = [w[ob[t]:ob[t + 1]].sum() for t in range(n)]
+        assert max(per_b) / (w.sum() / n) <= 1.01, n
+        of = oracle.rows_to_threads(f, n)
+        per_f = [w[of[t]:of[t + 1]].sum() for t in range(n)]
+        worst_flop = max(worst_flop, max(per_f) / (w.sum() / n))
+    assert worst_flop > 1.01  # the flop split is measurably bytes-imbalanced

@@ -552,14 +552,15 @@ def test_heap_tier_bitexact_c1(spg):
 
 
 def test_heap_auto_selector_cost_model(spg):
-    """AUTO picks the heap exactly where Eq:heap_est < Eq:hash_est (P:358-366,
-    c = 1.3) among the eligible rows (warp tiers, nnz(a_i) <= 16, flop_i <=
+    """AUTO (with the paper's unit costs, h = 1) picks the heap exactly where
+    Eq:heap_est < Eq:hash_est (c = 1.3) among the eligible rows (warp tiers, nnz(a_i) <= 16, flop_i <=
     2048, sorted B); C1 (low CR, short rows) goes mostly to the heap, C2's
     stencil's interior rows (nnz(a_i) = 27) are not eligible; results exact
     vs the oracle."""
     for name, want_some in (("c1_er4096", True), ("c2_stencil64", False)):
         A, B, _ = synth.workload(name, scale=None if name == "c1_er4096" else 16)
-        ctx = _heap_ctx(spg, "auto")
+        ctx = spg.Context()
+        ctx.set_accumulator("auto", 1.3, 1.0)
         gpu_vs_oracle(A, B, True, ctx=ctx, what=f"{name} auto")
         f, _ = oracle.flop(A, B)
         nz = oracle.row_nnz(A, B)
@@ -620,7 +621,9 @@ def test_set_accumulator_errors(spg):
     from paper_1804_01698_b200 import _lib
     ctx = spg.Context()
     with pytest.raises(_lib.SpgError, match="INVALID_ARG"):
-        _lib._check(ctx.handle, "x", _lib.load().spg_set_accumulator(ctx.handle, 7, 1.3))
+        _lib._check(ctx.handle, "x", _lib.load().spg_set_accumulator(ctx.handle, 7, 1.3, 8.0))
+    with pytest.raises(_lib.SpgError, match="INVALID_ARG"):
+        ctx.set_accumulator("auto", 1.3, 0.0)
     with pytest.raises(_lib.SpgError, match="INVALID_ARG"):
         ctx.set_accumulator("auto", 0.5)
 

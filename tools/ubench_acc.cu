@@ -20,8 +20,35 @@ __device__ __forceinline__ unsigned hash32(unsigned x) {
   x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16; return x;
 }
 
+__global__ void kgen(unsigned *tab, int n, int sorted) {
+  // R-MAT-like columns in [0, 8192): each bit set with probability 0.24;
+  // sorted = 1: each group of 32 sorted (a B-row segment's round)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned x = 0, hh = hash32(i * 2654435761u + 17u);
+  for (int bit = 0; bit < 13; ++bit) {
+    hh = hash32(hh + bit);
+    if ((hh & 1023) < 246) x |= 1u << bit;
+  }
+  unsigned c = x;
+  if (sorted) {
+    const int lane = threadIdx.x & 31;
+    for (int k = 2; k <= 32; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const unsigned o = __shfl_xor_sync(0xffffffffu, c, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        c = (lower == up) ? min(c, o) : max(c, o);
+      }
+    // drop duplicates inside the round (a segment has distinct columns)
+    const unsigned prev = __shfl_up_sync(0xffffffffu, c, 1);
+    if (lane > 0 && prev == c) c = (c + 4096u * (lane & 1) + lane) & 8191u;
+  }
+  tab[i] = c;
+}
+
 template <int VAR>
-__global__ void __launch_bounds__(512, 2) kacc(int pattern, int rounds, double *gwin, double *sink) {
+__global__ void __launch_bounds__(512, 2) kacc(int pattern, int rounds, double *gwin, double *sink,
+                                               const unsigned *tab, int tabn) {
   extern __shared__ double win[];
   unsigned *bm = reinterpret_cast<unsigned *>(win + W);
   for (int s = threadIdx.x; s < W; s += 512) win[s] = 0.0;
@@ -36,24 +63,7 @@ __global__ void __launch_bounds__(512, 2) kacc(int pattern, int rounds, double *
     if (pattern == 0) c = ((hash32(w * 131 + r) & (W - 1)) & ~31u) + lane;
     else if (pattern == 1) c = rr & (W - 1);
     else if (pattern == 2) c = ((hash32(w * 131 + r) & (W - 1)) + 4 * lane + (rr & 3)) & (W - 1);
-    else {
-      // R-MAT-like: each column bit set with probability 0.24 (hot columns
-      // with few bits set), pattern 4: sorted within the round (a B segment)
-      unsigned x = 0, hh = rr;
-      for (int bit = 0; bit < 13; ++bit) {
-        hh = hash32(hh + bit);
-        if ((hh & 1023) < 246) x |= 1u << bit;
-      }
-      c = x;
-      if (pattern == 4) {  // sort the 32 lanes' columns (bitonic via shuffles)
-        for (int k = 2; k <= 32; k <<= 1)
-          for (int j = k >> 1; j > 0; j >>= 1) {
-            const unsigned o = __shfl_xor_sync(0xffffffffu, c, j);
-            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-            c = (lower == up) ? min(c, o) : max(c, o);
-          }
-      }
-    }
+    else c = __ldg(tab + ((size_t(blockIdx.x) * 16 + w) * 32 * 61 + size_t(r) * 32 + lane) % tabn);
     const double v = 1.0 + (rr & 7);
     if (VAR == 0) atomicAdd(win + c, v);
     else if (VAR == 1) {
@@ -94,6 +104,12 @@ int main() {
   cudaMemset(gwin, 0, size_t(2 * sms) * W * 8);
   cudaMalloc(&sink, 8);
   const int rounds = 4096;
+  const int tabn = 1 << 24;
+  unsigned *tab_u, *tab_s;
+  cudaMalloc(&tab_u, size_t(tabn) * 4);
+  cudaMalloc(&tab_s, size_t(tabn) * 4);
+  kgen<<<tabn / 256, 256>>>(tab_u, tabn, 0);
+  kgen<<<tabn / 256, 256>>>(tab_s, tabn, 1);
   const size_t smem = W * 8 + W / 8;
   cudaFuncSetAttribute(kacc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kacc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -103,7 +119,7 @@ int main() {
   cudaFuncSetAttribute(kacc<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const char *vn[] = {"atomicAdd(f64) smem", "CAS-guess-0 (ATOMS.CAS.64)", "plain RMW (racy bound)",
                       "warp-private window RMW", "red.global.add.f64 (L2)", "atomicAdd + atomicOr bit"};
-  const char *pn[] = {"dense run", "uniform random", "sorted gap 4", "rmat bits", "rmat sorted"};
+  const char *pn[] = {"dense run", "uniform random", "sorted gap 4", "rmat bits", "rmat sorted seg"};
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -111,12 +127,12 @@ int main() {
     for (int pat = 0; pat < 5; ++pat) {
       auto launch = [&]() {
         switch (var) {
-          case 0: kacc<0><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink); break;
-          case 1: kacc<1><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink); break;
-          case 2: kacc<2><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink); break;
-          case 3: kacc<3><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink); break;
-          case 4: kacc<4><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink); break;
-          default: kacc<5><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink); break;
+          case 0: kacc<0><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink, pat == 3 ? tab_u : tab_s, tabn); break;
+          case 1: kacc<1><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink, pat == 3 ? tab_u : tab_s, tabn); break;
+          case 2: kacc<2><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink, pat == 3 ? tab_u : tab_s, tabn); break;
+          case 3: kacc<3><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink, pat == 3 ? tab_u : tab_s, tabn); break;
+          case 4: kacc<4><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink, pat == 3 ? tab_u : tab_s, tabn); break;
+          default: kacc<5><<<2 * sms, 512, smem>>>(pat, rounds, gwin, sink, pat == 3 ? tab_u : tab_s, tabn); break;
         }
       };
       launch();
