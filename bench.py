@@ -371,6 +371,8 @@ def run_ours(args):
                                                 sorted=True, ctx=acc_ctx[mode], g_shift=deg["q0"])
                         if deg["q1"] > deg["q0"] else 0)
             return spg.spgemm(Aloc, dB, sorted=True, ctx=acc_ctx[mode])
+        if isinstance(sorted_out, str) and sorted_out.startswith("onephase_"):  # one-phase A/B
+            return spg.spgemm(Aloc, dB, sorted=sorted_out.endswith("sorted"), ctx=ctx, method="one_phase")
         if sorted_out == "deg_formed":  # the same with the default (AUTO) accumulator
             return (spg.triangle_count_rows(deg["L"], deg["U"], deg["G"], 0, deg["q1"] - deg["q0"],
                                             sorted=True, ctx=ctx, g_shift=deg["q0"])
@@ -449,6 +451,15 @@ def run_ours(args):
         step("fused_deg")
         ms_fused_deg, _, _, last_fdeg = timed("fused_deg", args.steps)
     acc_ab, acc_counts = {}, []
+    if not tri and not args.no_accum_ab:
+        # one-phase path where every row fits its tiers
+        # (min(flop_i, ncols) <= 8192) and flop x 12 B fits the workspace
+        try:
+            for kname in ("onephase_sorted", "onephase_unsorted"):
+                step(kname)
+                acc_ab[kname] = timed(kname, max(1, min(args.steps, 10)))[0]
+        except _lib.SpgError as e:
+            log(f"one-phase not applicable: {e}")
     if not args.no_accum_ab:
         kinds = (("deg_formed", "acc_hash_deg", "acc_heap_deg") if tri else ("acc_hash", "acc_heap"))
         for kname in kinds:
@@ -577,8 +588,11 @@ def run_ours(args):
                                                     "product (SURVEY 8(f) row 1); C not formed"}}
                             if ms_fused is not None else {}),
                          **({k: {"ms_per_step": v,
-                                 "note": "sorted C, accumulator A/B (SURVEY 8(f) row 4): "
-                                         + {"acc_hash": "every row hashed + sorted",
+                                 "note": "A/B variant: "
+                                         + {"onephase_sorted": "one-phase path: flop-sized tables, no "
+                                                               "symbolic pass, one host round trip (8(f) row 3)",
+                                            "onephase_unsorted": "one-phase path, unsorted C",
+                                            "acc_hash": "every row hashed + sorted",
                                             "acc_heap": "heap merge for every eligible row (P:340-352)",
                                             "deg_formed": "degree order, L'*U' formed sorted, cost model "
                                                           "(AUTO) accumulator, + mask",

@@ -1304,10 +1304,12 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
   auto segsort = [&](const int32_t *in, int32_t *out, const int64_t *seg, int64_t nseg) -> spg_status {
     if (nseg <= 0) return SPG_OK;
     SPG_CUDA(c, cudaMemsetAsync(nlong, 0, 8, s));
+    { ProfScope _ps(c, s, "k_segsort_warp");
     k_segsort_warp<8><<<(unsigned)std::min<int64_t>(ceil_div(nseg, 8), int64_t(c->num_sms) * 8), 256, 0, s>>>(
-        in, out, seg, nseg, longs, nlong);
+        in, out, seg, nseg, longs, nlong); }
     SPG_LAUNCHED(c, "k_segsort_warp");
-    k_segsort_long<1024><<<(unsigned)c->num_sms, 1024, lsmem, s>>>(in, out, seg, longs, nlong, n, lwords);
+    { ProfScope _ps(c, s, "k_segsort_long");
+      k_segsort_long<1024><<<(unsigned)c->num_sms, 1024, lsmem, s>>>(in, out, seg, longs, nlong, n, lwords); }
     SPG_LAUNCHED(c, "k_segsort_long");
     return SPG_OK;
   };
@@ -1315,18 +1317,18 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
   // vertex order (deg(v), v): counting sort by degree, then each degree
   // bucket sorted by id
   SPG_CUDA(c, cudaMemsetAsync(hist, 0, size_t(n + 1) * 16, s));  // hist + fill
-  k_rl_deghist<<<grid, 256, 0, s>>>(g, hist);
+  { ProfScope _ps(c, s, "k_rl_deghist"); k_rl_deghist<<<grid, 256, 0, s>>>(g, hist); }
   SPG_LAUNCHED(c, "k_rl_deghist");
   SPG_CUDA(c, cudaMemsetAsync(dstart, 0, 8, s));
   SPG_CUDA(c, cudaMemcpyAsync(dstart + 1, hist, size_t(n + 1) * 8, cudaMemcpyDeviceToDevice, s));
   if ((st = launch_scan(c, dstart + 1, n + 1, s)) != SPG_OK) return st;  // bucket offsets (degrees 0..n)
-  k_rl_degscatter<<<grid, 256, 0, s>>>(g, dstart, fill, bucket);
+  { ProfScope _ps(c, s, "k_rl_degscatter"); k_rl_degscatter<<<grid, 256, 0, s>>>(g, dstart, fill, bucket); }
   SPG_LAUNCHED(c, "k_rl_degscatter");
   if ((st = segsort(bucket, rank, dstart, n + 1)) != SPG_OK) return st;  // (rank: the sorted ids, temporarily)
-  k_rl_rank<<<grid, 256, 0, s>>>(rank, n, perm, bucket);             // bucket <- rank[v]
+  { ProfScope _ps(c, s, "k_rl_rank"); k_rl_rank<<<grid, 256, 0, s>>>(rank, n, perm, bucket); }  // bucket <- rank[v]
   SPG_LAUNCHED(c, "k_rl_rank");
   int32_t *rk = bucket;
-  k_rl_count<<<wgrid, 256, 0, s>>>(g, perm, rk, L_rp + 1, U_rp + 1, G_rp + 1, bad);
+  { ProfScope _ps(c, s, "k_rl_count"); k_rl_count<<<wgrid, 256, 0, s>>>(g, perm, rk, L_rp + 1, U_rp + 1, G_rp + 1, bad); }
   SPG_LAUNCHED(c, "k_rl_count");
   for (int64_t *rp : {L_rp, U_rp, G_rp})
     if ((st = launch_scan(c, rp + 1, n, s)) != SPG_OK) return st;
@@ -1340,7 +1342,7 @@ spg_status spg_degree_relabel(spg_ctx *c, const spg_csr *G, int32_t *perm, int64
                 "G is not a symmetric pattern without diagonal (lower/upper counts differ or a "
                 "diagonal entry is present)");
   if (nnz == 0) return SPG_OK;
-  k_rl_fill<<<wgrid, 256, 0, s>>>(g, perm, rk, L_rp, U_rp, G_rp, Lt, Ut, Gt);
+  { ProfScope _ps(c, s, "k_rl_fill"); k_rl_fill<<<wgrid, 256, 0, s>>>(g, perm, rk, L_rp, U_rp, G_rp, Lt, Ut, Gt); }
   SPG_LAUNCHED(c, "k_rl_fill");
   if ((st = segsort(Gt, G_col, G_rp, n)) != SPG_OK) return st;
   if ((st = segsort(Lt, L_col, L_rp, n)) != SPG_OK) return st;
