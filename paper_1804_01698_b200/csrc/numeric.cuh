@@ -1055,7 +1055,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       if (act) {
         const uint32_t off = c - (uint32_t)lo;
         atomicAdd(dv + dense_slot(off), v);  // c_ij <- c_ij + value (l.8), dense window
-        atomicOr(dbm + bm_word(off >> 5), 1u << (off & 31u));
+        atomicOr(dbm + tbm_word(off), tbm_bit(off));  // (transposed tile bitmap)
       }
     };
     auto acc_hash = [&](bool act, uint32_t c, double v) {
@@ -1174,25 +1174,35 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       // then a warp per word: lane l emits column 32 qw + l if present
       // (coalesced stores, ascending columns) and resets its slot
       static_assert(kTileCols / 32 <= THREADS, "one word per thread");
-      int32_t *wcum = reinterpret_cast<int32_t *>(eb);
-      const int nwd = kTileCols / 32;
-      const int pc = (int)threadIdx.x < nwd ? __popc(dbm[bm_word(threadIdx.x)]) : 0;
+      const int nwd = kTileCols / 32;  // 32-column groups
+      // (transposed bitmap: the 32 columns 32 qw + l are bit qw >> 3 of
+      // words 32 (qw & 7) + l -- a warp reads them with one conflict-free
+      // load and a ballot)
+      int32_t *gcnt = reinterpret_cast<int32_t *>(eb);
+      int32_t *wcum = gcnt + nwd;
+      for (int qw = w; qw < nwd; qw += NW) {
+        const unsigned bal = __ballot_sync(kFull, (dbm[(qw & 7) * 32 + lane] >> (qw >> 3)) & 1u);
+        if (lane == 0) gcnt[qw] = __popc(bal);
+      }
+      __syncthreads();
       int totw;
-      const int wx = block_excl_scan_int(pc, s_warp, &totw);
+      const int wx = block_excl_scan_int((int)threadIdx.x < nwd ? gcnt[threadIdx.x] : 0, s_warp, &totw);
       if ((int)threadIdx.x < nwd) wcum[threadIdx.x] = wx;
       __syncthreads();
       for (int qw = w; qw < nwd; qw += NW) {
-        const uint32_t word = dbm[bm_word(qw)];
-        if ((word >> lane) & 1u) {
-          const int64_t o = out + wcum[qw] + __popc(word & ((1u << lane) - 1u));
+        const uint32_t wi = (qw & 7) * 32 + lane, bt = 1u << (qw >> 3);
+        const bool present = (dbm[wi] & bt) != 0u;
+        const unsigned bal = __ballot_sync(kFull, present);
+        if (present) {
+          const int64_t o = out + wcum[qw] + __popc(bal & ((1u << lane) - 1u));
           c_col[o] = (int32_t)(lo + qw * 32 + lane);
           const uint32_t ds = dense_slot(qw * 32 + lane);
           c_val[o] = dv[ds];
           dv[ds] = 0.0;
         }
-        __syncwarp();
-        if (lane == 0) dbm[bm_word(qw)] = 0u;
       }
+      __syncthreads();  // (every group read its bits)
+      for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
     } else if (!sorted) {
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
         const int s = slot_of[p];

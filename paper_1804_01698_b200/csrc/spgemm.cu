@@ -642,7 +642,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
           }
         SPG_LAUNCHED(c, "k_sym_block");
       } else if (bin == SB_BM) {
-        const size_t nwords = (size_t((B->ncols + 31) / 32) + 31) & ~size_t(31);  // whole groups (bm_word)
+        const size_t nwords = size_t(ceil_div(B->ncols, kTileCols)) * (kTileCols / 32);  // whole tiles (tbm_word)
         const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");

@@ -1,0 +1,11 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "part or column or c3_rmat_small or bin_bound or wide or c5" > gpurun_out/r2_pytest13.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/r2_pytest13.log
+for so in 1 0; do timeout 300 python tools/profile_step.py --config c3_rmat20 --records --reps 2 --sorted $so > gpurun_out/r2_prof13_c3_s$so.log 2>&1; done
+python - <<'PY'
+import ast
+for f in ("gpurun_out/r2_prof13_c3_s1.log","gpurun_out/r2_prof13_c3_s0.log"):
+    L=[l for l in open(f) if l.startswith("[(")]
+    d=dict((n,t) for n,t in ast.literal_eval(L[-1]))
+    print(f, {k:v for k,v in d.items() if v>1})
+PY
