@@ -50,8 +50,26 @@ struct spg_ctx {
   Buf useful_bits;                   // useful-entry bitmask of k_flop_nz (pruning), grow-only
   Buf one_fofs, one_col, one_val;    // one-phase: flop prefix, flop-sized row workspace (grow-only)
   bool have_one = false;             // a one-phase result waits in the workspace
+  bool one_graph_ok = true;          // SPG_ONEPHASE_GRAPH=0: no graph capture
+  cudaGraphExec_t one_exec = nullptr;
+  int64_t one_graph_launches = 0;
   int64_t one_m = 0;
   const int64_t *one_rp = nullptr;
+  struct OneKeyT {
+    const void *arp, *acol, *aval;
+    int64_t am, an;
+    const void *brp, *bcol, *bval;
+    int64_t bm, bn;
+    const void *crp;
+    int sorted;
+    const void *ws;
+    unsigned long long cap;
+    bool operator==(const OneKeyT &o) const {
+      return arp == o.arp && acol == o.acol && aval == o.aval && am == o.am && an == o.an &&
+             brp == o.brp && bcol == o.bcol && bval == o.bval && bm == o.bm && bn == o.bn &&
+             crp == o.crp && sorted == o.sorted && ws == o.ws && cap == o.cap;
+    }
+  } one_key{};
   bool pruned = false;               // the plan runs on the pruned A' (mostly-empty B)
   int64_t prune_n = 0;
   spg_csr Ap{};
@@ -313,6 +331,8 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
     c->serial = (e && e[0] == '1') ? 1 : 0;
     const char *t = getenv("SPG_TUNE");
     c->tune = t ? atoi(t) : 0;
+    const char *og = getenv("SPG_ONEPHASE_GRAPH");
+    c->one_graph_ok = !(og && og[0] == '0');
   }
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) c->num_sms = v;
@@ -374,6 +394,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
     if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->one_exec) cudaGraphExecDestroy(c->one_exec);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
   return SPG_OK;
@@ -914,17 +935,30 @@ spg_status spg_onephase(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   if ((st = buf_ensure(c, c->flop, size_t(std::max<int64_t>(m, 1)) * 8, s)) != SPG_OK) return st;
   if ((st = buf_ensure(c, c->rows_sym, size_t(std::max<int64_t>(m, 1)) * 4, s)) != SPG_OK) return st;
   if ((st = buf_ensure(c, c->one_fofs, size_t(m + 1) * 8, s)) != SPG_OK) return st;
+  if ((st = buf_ensure(c, c->bnz, size_t((B->nrows + 31) / 32) * 4, s)) != SPG_OK) return st;
   PlanInfo *info = (PlanInfo *)c->info.p;
   int64_t *row_nnz = C_row_ptr + 1;
   int64_t *fofs = (int64_t *)c->one_fofs.p;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    // workspace: grow-only, sized by the last flop total seen (>= 1M products)
-    const unsigned long long cap = (unsigned long long)(c->one_col.bytes / 4);
+  // the launch sequence up to the host read, replayed as a CUDA graph when
+  // the inputs, outputs and workspace are the ones it was captured with
+  // (SPG_ONEPHASE_GRAPH=0 disables; the launch-bound small configs gain
+  // most), else enqueued on `s`
+  auto enqueue = [&](unsigned long long cap, cudaStream_t s) -> spg_status {
+    spg_status st;
     SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
     SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, size_t(m + 1) * 8, s));
     if (m > 0 && B->nrows > 0) {
+      // B nonempty-row bitmap: the flop pass skips the B.row_ptr gathers of
+      // empty B rows when most are empty (decided on the device; C4)
+      {
+        ProfScope _ps(c, s, "k_b_rowmask");
+        const int64_t nw = (B->nrows + 31) / 32;
+        k_b_rowmask<<<(unsigned)std::min<int64_t>(ceil_div(nw * 32, 256), int64_t(c->num_sms) * 8), 256, 0, s>>>(
+            dev(B), (uint32_t *)c->bnz.p, info);
+      }
+      SPG_LAUNCHED(c, "k_b_rowmask");
       // a1 + a2: flop, one-phase bins (the tables are sized by the flop bound)
-      if ((st = launch_flop(c, A, B, 2, s)) != SPG_OK) return st;
+      if ((st = launch_flop(c, A, B, 2, s, (const uint32_t *)c->bnz.p)) != SPG_OK) return st;
       {
         ProfScope _ps(c, s, "k_bin_scatter_1p");
         k_bin_scatter<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(m, (const int64_t *)c->flop.p, A->row_ptr,
@@ -981,6 +1015,43 @@ spg_status spg_onephase(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     }
     // a4: C_row_ptr = exclusive scan of nnz(c_i)
     if ((st = launch_scan(c, row_nnz, m, s)) != SPG_OK) return st;
+    return SPG_OK;
+  };
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    // workspace: grow-only, sized by the last flop total seen
+    const unsigned long long cap = (unsigned long long)(c->one_col.bytes / 4);
+    const spg_ctx::OneKeyT key{A->row_ptr, A->col_idx, A->val, A->nrows, A->ncols, B->row_ptr, B->col_idx, B->val,
+                     B->nrows, B->ncols, C_row_ptr, sorted, c->one_col.p, cap};
+    const bool use_graph = c->one_graph_ok && !c->profiling && m > 0;
+    if (use_graph && c->one_exec && key == c->one_key) {
+      SPG_CUDA(c, cudaGraphLaunch(c->one_exec, s));
+      c->launches += c->one_graph_launches;
+    } else if (use_graph) {
+      // everything the sequence allocates is sized before the capture
+      if ((st = buf_ensure(c, c->trow, size_t(m + 1) * 8, s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->partial, size_t(ceil_div(m, kScanTile)) * 8, s)) != SPG_OK) return st;
+      if (c->one_exec) { cudaGraphExecDestroy(c->one_exec); c->one_exec = nullptr; }
+      cudaGraph_t g = nullptr;
+      const int64_t l0 = c->launches;
+      // (captured on an internal stream: the caller's may be the legacy
+      // default stream, which cannot be captured)
+      cudaStream_t cs = c->sub[0];
+      SPG_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      const spg_status st2 = enqueue(cap, cs);
+      const cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+      if (st2 != SPG_OK) { if (g) cudaGraphDestroy(g); return st2; }
+      SPG_CUDA(c, e2);
+      cudaGraphExec_t ex = nullptr;
+      const cudaError_t e3 = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      SPG_CUDA(c, e3);
+      c->one_exec = ex;
+      c->one_key = key;
+      c->one_graph_launches = c->launches - l0;
+      SPG_CUDA(c, cudaGraphLaunch(c->one_exec, s));
+    } else {
+      if ((st = enqueue(cap, s)) != SPG_OK) return st;
+    }
     if ((st = read_info(c, s)) != SPG_OK) return st;  // the one host round trip
     const PlanInfo &h = *c->host_info;
     if (h.sym_count[SB_G])

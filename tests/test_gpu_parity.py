@@ -658,3 +658,29 @@ def test_onephase_every_bin(spg, sorted_out):
         spg.spgemm(spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B), ctx=ctx, method="one_phase")
     with pytest.raises(_lib.SpgError, match="STATE"):
         _lib.spg_onephase_emit(ctx.handle, 0, 0, 0)
+
+
+def test_onephase_graph_replay(spg, monkeypatch):
+    """The one-phase launch sequence is replayed as a CUDA graph when the
+    inputs / workspace match the captured ones: repeated calls (and a call
+    with new A values on the same structure) stay exact, and agree with a
+    context that never captures (SPG_ONEPHASE_GRAPH=0)."""
+    A, B, _ = synth.workload("c1_er4096")
+    dA = spg.DeviceCSR.from_host(A)
+    ctx = spg.Context()
+    monkeypatch.setenv("SPG_ONEPHASE_GRAPH", "0")
+    ctx0 = spg.Context()
+    o = oracle.spgemm(A, B)
+    for rep in range(3):
+        C = spg.spgemm(dA, dA, sorted=True, ctx=ctx, method="one_phase")
+        compare(*C.to_host(), *o, True, f"one-phase graph rep {rep}")
+    l0 = ctx.launches
+    C = spg.spgemm(dA, dA, sorted=True, ctx=ctx, method="one_phase")
+    assert ctx.launches > l0  # replays count their kernels
+    C0 = spg.spgemm(dA, dA, sorted=True, ctx=ctx0, method="one_phase")
+    assert torch.equal(C.row_ptr, C0.row_ptr) and torch.equal(C.col, C0.col)
+    # new values, same structure and buffers: the replayed graph reads them
+    dA.val.copy_(torch.from_numpy(synth.with_values(A, 99, 0.5, 1.5).val).to(dA.val.device))
+    A2 = synth.CSR(A.nrows, A.ncols, A.row_ptr, A.col, dA.val.cpu().numpy())
+    C = spg.spgemm(dA, dA, sorted=True, ctx=ctx, method="one_phase")
+    compare(*C.to_host(), *oracle.spgemm(A2, A2), True, "one-phase graph, new values")
