@@ -803,8 +803,14 @@ __global__ void __launch_bounds__(THREADS) k_num_global(const int32_t *__restric
 // Output position: C_row_ptr[i] + keys of the row before the part.  No global
 // atomics besides the part counter.
 // ---------------------------------------------------------------------------
-constexpr int kTEnt = 1024;                 // a_ik staged per chunk
-constexpr int kTLongSeg = 16;               // segments of >= this many products run warp-sequential
+#ifndef SPG_TENT
+#define SPG_TENT 1024
+#endif
+#ifndef SPG_TLONGSEG
+#define SPG_TLONGSEG 32
+#endif
+constexpr int kTEnt = SPG_TENT;             // a_ik staged per chunk
+constexpr int kTLongSeg = SPG_TLONGSEG;     // segments of >= this many products run warp-sequential
 constexpr int kTPartLogT = 12;
 constexpr int kTPartT = 1 << kTPartLogT;      // hash slots of a multi-tile part
 static_assert(4 * kTPartKeys <= 3 * kTPartT, "multi-tile part: load <= 3/4");
@@ -1152,7 +1158,13 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       const int RS = (PS + 31) >> 5;
       const int gs0 = (int)((int64_t)RS * w / NW), gs1 = (int)((int64_t)RS * (w + 1) / NW);
       const int gl0 = (int)((int64_t)RL * w / NW), gl1 = (int)((int64_t)RL * (w + 1) / NW);
-      if (dense) {
+      if (tune & 32) {  // (measurement only: gathers without accumulation; C left unwritten)
+        double sink = 0.0;
+        auto acc_none = [&](bool act, uint32_t c, double v) { sink += act ? v + (double)c : 0.0; };
+        for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_none);
+        for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_none);
+        if (sink == 1.2345e300) dbg[15] = 1;
+      } else if (dense) {
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_dense);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_dense);
       } else {
@@ -1169,7 +1181,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     __syncthreads();
     const long long ce = instr ? clock64() : 0;
     const int64_t out = s_rp0 + P.z;
-    if (dense) {
+    if (tune & 48) {  // (measurement only: no emit; the dense window is still reset)
+      if (dense) {
+        for (int s2 = threadIdx.x; s2 < kTileCols; s2 += THREADS) dv[s2] = 0.0;
+        for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
+      }
+    } else if (dense) {
       // keys before each 32-column word (block scan of the word popcounts),
       // then a warp per word: lane l emits column 32 qw + l if present
       // (coalesced stores, ascending columns) and resets its slot
