@@ -830,6 +830,8 @@ constexpr size_t kOffLpre = kOffEpre + size_t(kTEnt + 4) * 4;
 constexpr size_t kTEntBytes = kOffLpre + size_t(kTEnt + 4) * 4;
 static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
+static_assert(size_t(kPbitsMaxSpan) * kTileRec * 4 + size_t(kTPartKeys) * 8 <= kTUnion,
+              "tile records + rank-indexed values in the table region");
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
 static_assert(kTEnt <= 32 * 32, "32-ary owner search");
 
@@ -979,7 +981,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     DevCSR A, DevCSR B, const int64_t *__restrict__ c_rp, int32_t *__restrict__ c_col,
     double *__restrict__ c_val, int sorted, const int4 *__restrict__ parts, int64_t nparts,
     const int32_t *__restrict__ toff, int64_t nB, unsigned long long *counter, int tune,
-    unsigned long long *dbg) {
+    unsigned long long *dbg, const uint32_t *__restrict__ pbits) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_warp[33];
   __shared__ int s_red[66];
@@ -991,7 +993,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   // part pipeline (thread 0): the part after next is reserved and the next
   // part's records are loaded while this part runs; published at its end
   __shared__ long long s_q;
-  __shared__ int4 s_P, s_P1, s_Pn[2];
+  __shared__ int4 s_P, s_P1, s_P2, s_Pn[3];
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char *base = reinterpret_cast<char *>(s_dyn_f64);
@@ -1017,8 +1019,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     const long long q = (long long)atomicAdd(counter, 1ull);
     s_q = q;
     if (q < nparts) {
-      s_P = parts[2 * q];
-      s_P1 = parts[2 * q + 1];
+      s_P = parts[3 * q];
+      s_P1 = parts[3 * q + 1];
+      s_P2 = parts[3 * q + 2];
     }
     q_next = (long long)atomicAdd(counter, 1ull);
   }
@@ -1028,7 +1031,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   while (true) {
     const int64_t q = s_q;
     if (q >= nparts) break;
-    const int4 P = s_P, P1 = s_P1;
+    const int4 P = s_P, P1 = s_P1, P2 = s_P2;
     // thread 0: async copies (cp.async, no registers held) of the next
     // part's records (q_next was reserved one part ago) and of this part's
     // C row start (used at the emit); reserve the part after next
@@ -1036,8 +1039,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     if (threadIdx.x == 0) {
       cp_async8(&s_rp0, c_rp + P.x);
       if (q_next < nparts) {
-        cp_async16(&s_Pn[0], parts + 2 * q_next);
-        cp_async16(&s_Pn[1], parts + 2 * q_next + 1);
+        cp_async16(&s_Pn[0], parts + 3 * q_next);
+        cp_async16(&s_Pn[1], parts + 3 * q_next + 1);
+        cp_async16(&s_Pn[2], parts + 3 * q_next + 2);
       }
       cp_async_commit();
       q_after = q_next < nparts ? (long long)atomicAdd(counter, 1ull) : q_next;
@@ -1053,8 +1057,23 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     unsigned long long prods = 0;
     const int logT = dense ? 0 : min(num_log2(cnt), kTPartLogT);
     const int T = 1 << logT;
-    if (!dense)
+    // a narrow hash part with its tile records from the symbolic phase (the
+    // row's bitmap words + per-word ranks): products index the part's
+    // columns by rank (two loads and a popcount, no hashing, no key insert),
+    // values accumulate in vals[rank], and the emit walks the bitmap (column
+    // order: sorted for free)
+    const long long koff = (long long)(((unsigned long long)(unsigned)P2.y << 32) | (unsigned)P2.x);
+    const bool known = !dense && koff >= 0 && pbits != nullptr;
+    uint32_t *rec = reinterpret_cast<uint32_t *>(base);                       // span x kTileRec words
+    double *rv = reinterpret_cast<double *>(base + size_t(kPbitsMaxSpan) * kTileRec * 4);  // [cnt]
+    if (known) {
+      const int nrec = (t1 - t0) * kTileRec;
+      const uint4 *src = reinterpret_cast<const uint4 *>(pbits + koff * kTileRec);
+      for (int q = threadIdx.x; q < nrec / 4; q += THREADS) reinterpret_cast<uint4 *>(rec)[q] = __ldg(src + q);
+      for (int r = threadIdx.x; r < cnt; r += THREADS) rv[r] = 0.0;
+    } else if (!dense) {
       for (int s = threadIdx.x; s < T; s += THREADS) { hk[s] = kEmpty; hv[s] = 0.0; }
+    }
     if (threadIdx.x == 0) s_cnt = 0;
     const int32_t *tk0 = toff + int64_t(t0) * nB, *tk1 = toff + int64_t(t1) * nB;
     auto acc_dense = [&](bool act, uint32_t c, double v) {
@@ -1062,6 +1081,16 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         const uint32_t off = c - (uint32_t)lo;
         atomicAdd(dv + dense_slot(off), v);  // c_ij <- c_ij + value (l.8), dense window
         atomicOr(dbm + tbm_word(off), tbm_bit(off));  // (transposed tile bitmap)
+      }
+    };
+    auto acc_known = [&](bool act, uint32_t c, double v) {  // rank of the column in the part
+      if (act) {
+        const uint32_t off = c - (uint32_t)lo, q = off >> 5;
+        const uint32_t *tr = rec + (q >> 8) * kTileRec;
+        const uint32_t wd = tr[q & 255u];
+        const int rank = (int)reinterpret_cast<const uint16_t *>(tr + 256)[q & 255u] +
+                         __popc(wd & ((1u << (off & 31u)) - 1u));
+        atomicAdd(rv + rank, v);  // c_ij <- c_ij + value (l.8)
       }
     };
     auto acc_hash = [&](bool act, uint32_t c, double v) {
@@ -1163,10 +1192,13 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         auto acc_none = [&](bool act, uint32_t c, double v) { sink += act ? v + (double)c : 0.0; };
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_none);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_none);
-        if (sink == 1.2345e300) dbg[15] = 1;
+        if (sink == 1.2345e300) dbg[13] = 1;
       } else if (dense) {
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_dense);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_dense);
+      } else if (known) {
+        for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_known);
+        for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_known);
       } else {
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_hash);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_hash);
@@ -1220,6 +1252,21 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       }
       __syncthreads();  // (every group read its bits)
       for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
+    } else if (known) {  // walk the part's bitmap words: column order = rank order
+      const int nw = (t1 - t0) * 256;
+      for (int q = threadIdx.x; q < nw; q += THREADS) {
+        const uint32_t *tr = rec + (q >> 8) * kTileRec;
+        uint32_t wd = tr[q & 255];
+        if (!wd) continue;
+        int r = reinterpret_cast<const uint16_t *>(tr + 256)[q & 255];
+        while (wd) {
+          const int bit = __ffs(wd) - 1;
+          wd &= wd - 1;
+          c_col[out + r] = (int32_t)(lo + (int64_t(q) << 5) + bit);
+          c_val[out + r] = rv[r];
+          ++r;
+        }
+      }
     } else if (!sorted) {
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
         const int s = slot_of[p];
@@ -1282,6 +1329,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       s_q = q_next;
       s_P = s_Pn[0];
       s_P1 = s_Pn[1];
+      s_P2 = s_Pn[2];
       q_next = q_after;
     }
     __syncthreads();
@@ -1296,6 +1344,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       atomicAdd(dbg + (dense ? 8 : 11), (unsigned long long)(cz - ce));   // emit
       atomicAdd(dbg + 9, (unsigned long long)na);
       atomicAdd(dbg + 10, (unsigned long long)cnt);
+      if (!dense) atomicAdd(dbg + 14, (unsigned long long)(t1 - t0));  // hash part spans (tiles)
+      if (known) atomicAdd(dbg + 15, 1ull);                            // parts indexed by tile records
     }
   }
 }

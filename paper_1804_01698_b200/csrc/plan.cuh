@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(256) k_tile_offsets(DevCSR B, int ntiles, int3
   }
 }
 
-// Parts (two int4 records each) in processing order: bucket = t0 for single-tile (dense-window)
+// Parts (three int4 records each) in processing order: bucket = t0 for single-tile (dense-window)
 // parts, kMaxTiles + t0 for multi-tile (hash) parts; dense parts first, tile
 // ascending (see k_num_tpart).  Counting sort: per-block smem histograms
 // merged into hist[2 * kMaxTiles], one block scans it, then a scatter with a
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(256) k_parts_hist(const int4 *__restrict__ par
   __syncthreads();
   const int64_t n = (int64_t)info->parts_used;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&h[part_bucket(parts[2 * p])], 1u);
+    atomicAdd(&h[part_bucket(parts[3 * p])], 1u);
   __syncthreads();
   for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x)
     if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -609,16 +609,17 @@ __global__ void __launch_bounds__(256) k_parts_scatter(const int4 *__restrict__ 
   const int64_t n = (int64_t)info->parts_used;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride)
-    atomicAdd(&h[part_bucket(parts[2 * p])], 1u);
+    atomicAdd(&h[part_bucket(parts[3 * p])], 1u);
   __syncthreads();
   for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x)
     if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);  // this block's first slot in bucket b
   __syncthreads();
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride) {
-    const int4 v = parts[2 * p], v1 = parts[2 * p + 1];
+    const int4 v = parts[3 * p], v1 = parts[3 * p + 1], v2 = parts[3 * p + 2];
     const unsigned d = atomicAdd(&h[part_bucket(v)], 1u);
-    out[2 * (int64_t)d] = v;
-    out[2 * (int64_t)d + 1] = v1;
+    out[3 * (int64_t)d] = v;
+    out[3 * (int64_t)d + 1] = v1;
+    out[3 * (int64_t)d + 2] = v2;
   }
 }
 

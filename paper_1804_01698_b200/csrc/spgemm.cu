@@ -42,7 +42,8 @@ struct spg_ctx {
   void *user = nullptr;
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
-  Buf parts, parts2, part_hist, toff;  // column-tile parts of long rows (BM tier), sorted copy, B tile offsets
+  Buf parts, parts2, part_hist, toff, pkeys;  // (+ tile records of the narrow hash parts)
+  size_t pkeys_want = 0;  // column-tile parts of long rows (BM tier), sorted copy, B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
   Buf rl_key, rl_rank, rl_tmp, rl_cub;  // degree relabelling (histograms, ranks/buckets, unsorted rows)
@@ -382,7 +383,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
   if (!c) return SPG_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
   Buf *bufs[] = {&c->flop,      &c->rows_sym,  &c->rows_num,  &c->partial,   &c->slab,
-                 &c->info,      &c->scratch,   &c->parts,     &c->parts2,    &c->part_hist,
+                 &c->info,      &c->scratch,   &c->parts,     &c->parts2,    &c->part_hist, &c->pkeys,
                  &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
                  &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
                  &c->rl_tmp,    &c->rl_cub,    &c->mask_rows, &c->useful_bits, &c->one_fofs,
@@ -476,6 +477,16 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   if ((st = buf_ensure(c, c->flop, size_t(std::max<int64_t>(m, 1)) * 8, s)) != SPG_OK) return st;
   if ((st = buf_ensure(c, c->rows_sym, size_t(std::max<int64_t>(m, 1)) * 4, s)) != SPG_OK) return st;
   if ((st = buf_ensure(c, c->rows_num, size_t(std::max<int64_t>(m, 1)) * 4, s)) != SPG_OK) return st;
+  if (c->pkeys_want > c->pkeys.bytes) {  // (grown here only: see the end of spg_symbolic)
+    size_t free_b = 0, total_b = 0;
+    // (the records must leave room for C: at most a quarter of the device,
+    // and 8 GiB of what is free right now)
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && c->pkeys_want <= total_b / 4 &&
+        c->pkeys_want + (size_t(8) << 30) < free_b + c->pkeys.bytes)
+      buf_ensure(c, c->pkeys, c->pkeys_want, s);
+    cudaGetLastError();
+    c->pkeys_want = 0;
+  }
   PlanInfo *info = (PlanInfo *)c->info.p;
   SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
   SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, sizeof(int64_t), s));
@@ -602,7 +613,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       parts_cap = (int64_t)(2 * h.flop_total / kTPartKeys) + (int64_t)h.sym_count[SB_BM] + 16;
       const int64_t ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       parts_cap = std::min<int64_t>(parts_cap, (int64_t)h.sym_count[SB_BM] * ntiles + 16);
-      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * 2 * sizeof(int4), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * 3 * sizeof(int4), s)) != SPG_OK) return st;
       parts = (int4 *)c->parts.p;
       c->plan_parts = true;
     }
@@ -668,7 +679,8 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
           k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(
-              rb, n, a, b, flop, row_nnz, info, parts, parts_cap);
+              rb, n, a, b, flop, row_nnz, info, parts, parts_cap,
+              c->pkeys.p ? (uint32_t *)c->pkeys.p : nullptr, int64_t(c->pkeys.bytes / 4));
         }
         SPG_LAUNCHED(c, "k_sym_bitmap");
       } else {  // SB_G
@@ -712,6 +724,12 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   }
   if ((st = read_info(c, s)) != SPG_OK) return st;
   c->plan = *c->host_info;
+  // the hash parts' tile records did not all fit: the buffer grows at the START
+  // of the next symbolic (never between this plan and its numeric phase,
+  // whose parts point into the current buffer); these parts hash their keys
+  if (c->plan.pkeys_used * kTileRec * 4 > c->pkeys.bytes && c->plan_parts)
+    c->pkeys_want = std::max<size_t>(
+        c->pkeys_want, size_t(c->plan.pkeys_used + (c->plan.pkeys_used >> 4)) * kTileRec * 4);
   *nnz_C = (int64_t)c->plan.nnz_total;
   if (flop_total) *flop_total = (int64_t)c->plan.flop_total;
   c->have_plan = true;
@@ -767,7 +785,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       if ((st = buf_ensure(c, c->toff, size_t(B->nrows) * size_t(ntiles + 1) * 4, s)) != SPG_OK)
         return st;
-      if ((st = buf_ensure(c, c->parts2, size_t(h.parts_used) * 2 * sizeof(int4), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->parts2, size_t(h.parts_used) * 3 * sizeof(int4), s)) != SPG_OK) return st;
       if ((st = buf_ensure(c, c->part_hist, size_t(kPartBuckets) * 4, s)) != SPG_OK) return st;
       PlanInfo *dinfo = (PlanInfo *)c->info.p;
       SPG_CUDA(c, cudaMemsetAsync(&dinfo->row_counter, 0, 8, s));
@@ -885,7 +903,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
         k_num_tpart<512><<<(unsigned)(2 * c->num_sms), 512, kTPartSmem, ss>>>(
             a, b, C_row_ptr, C_col_idx, C_val, sorted, (const int4 *)c->parts2.p,
             (int64_t)h.parts_used, (const int32_t *)c->toff.p, B->nrows, &dinfo->row_counter,
-            c->tune, dinfo->dbg);
+            c->tune, dinfo->dbg, (c->tune & 256) ? nullptr : (const uint32_t *)c->pkeys.p);
       }
       SPG_LAUNCHED(c, "k_num_tpart");
     } else {  // NB_G

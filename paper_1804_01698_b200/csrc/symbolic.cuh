@@ -47,6 +47,11 @@ __device__ __forceinline__ uint32_t tbm_word(uint32_t c) {
 }
 __device__ __forceinline__ uint32_t tbm_bit(uint32_t c) { return 1u << ((c >> 8) & 31u); }
 
+// Tile records of the narrow hash parts (k_sym_bitmap -> k_num_tpart): 256
+// bitmap words + 256 u16 ranks per 8192-column tile.
+constexpr int kTileRec = 256 + 128;
+constexpr int kPbitsMaxSpan = 16;  // tiles (the record set must fit the numeric's smem region)
+
 // Bitmap variant for very long rows: column c -> bit c of an ncols-bit set.
 __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
   const uint32_t bit = 1u << (c & 31u);
@@ -513,9 +518,14 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
 // sorted it also cuts rows with nnz > kPartMinKeys into column-tile parts for
-// the numeric G tier (spg_internal.cuh): part = two int4 records {row, first
-// tile | end tile << 16, keys of the row before the part, keys in the part}
-// and {A.row_ptr[row] (lo, hi), nnz(a_row), 0}.
+// the numeric G tier (spg_internal.cuh): part = three int4 records {row,
+// first tile | end tile << 16, keys of the row before the part, keys in the
+// part}, {A.row_ptr[row] (lo, hi), nnz(a_row), 0} and {index of the part's
+// first tile record in pbits (lo, hi) or -1, 0, 0}.  For the multi-tile
+// (hash) parts spanning <= kPbitsMaxSpan tiles the row's bitmap itself is
+// kept: per tile a record of kTileRec words = the tile's 256 bitmap words and
+// 256 u16 ranks (keys of the PART before each word), so the numeric phase
+// indexes the part's columns by rank instead of hashing them.
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restrict__ rows,
@@ -523,7 +533,9 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         const int64_t *__restrict__ flop,
                                                         int64_t *__restrict__ row_nnz,
                                                         PlanInfo *info, int4 *__restrict__ parts,
-                                                        int64_t parts_cap) {
+                                                        int64_t parts_cap,
+                                                        uint32_t *__restrict__ pbits,
+                                                        int64_t pbits_cap) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
   __shared__ DeferList s_dl;  // long B rows walked by the whole block
@@ -532,9 +544,11 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
   __shared__ int s_cut[kMaxTiles];       // first | (end tile << 16) of each part
   __shared__ int s_nne[kMaxTiles + 1];   // first nonempty tile at or after each tile
+  __shared__ long long s_tkoff[kMaxTiles];  // pbits record of a hash part's tile, or -1
+  __shared__ int s_tkb[kMaxTiles];          // keys of that part before the tile
   constexpr int NW = THREADS / 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // (words rounded up to whole tiles: the transposed layout uses all 256)
+  // (words rounded up to whole tiles)
   const int nwords = (int)(((B.ncols + kTileCols - 1) >> kTileLog) << (kTileLog - 5));
   const int ntiles = (int)((B.ncols + kTileCols - 1) >> kTileLog);
   uint32_t *bm = s_dyn_u32;
@@ -548,23 +562,20 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     // set the bit of every product's column (the old value is not used: no
     // dependency on the atomic's return), then count the set bits once
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) atomicOr(bm + tbm_word(c), tbm_bit(c));
+      if (act) atomicOr(bm + (c >> 5), 1u << (c & 31u));
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     __syncthreads();
-    // keys per column tile (a warp per tile), clearing the words for the next
-    // row on the way; then the exclusive scan over the tiles = keys before
-    // each tile, and the row's count
+    // keys per column tile (a warp per tile); then the exclusive scan over
+    // the tiles = keys before each tile, and the row's count
     for (int t = w; t < ntiles; t += NW) {
       const int q0 = t << (kTileLog - 5), q1 = min(nwords, q0 + kTileCols / 32);
       int c = 0;
-      for (int q = q0 + lane; q < q1; q += 32) {
-        c += __popc(bm[q]);
-        bm[q] = 0u;
-      }
+      for (int q = q0 + lane; q < q1; q += 32) c += __popc(bm[q]);
       c = (int)__reduce_add_sync(kFull, (unsigned)c);
       if (lane == 0) s_tcnt[t] = c;
+      if (lane == 0) s_tkoff[t] = -1;
     }
     __syncthreads();
     if (w == 0) {
@@ -615,13 +626,35 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       __syncthreads();
       if (threadIdx.x == 0) {
         int np = 0;
-        for (int t = s_nne[0]; t < ntiles; t = s_nne[s_nxt[t]]) s_cut[np++] = t | (s_nxt[t] << 16);
+        long long htiles = 0;  // tiles of the row's narrow multi-tile (hash) parts
+        for (int t = s_nne[0]; t < ntiles; t = s_nne[s_nxt[t]]) {
+          s_cut[np++] = t | (s_nxt[t] << 16);
+          if (s_nxt[t] > t + 1 && s_nxt[t] - t <= kPbitsMaxSpan) htiles += s_nxt[t] - t;
+        }
         const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
         if (base + np > parts_cap) {
           atomicAdd(&info->parts_overflow, 1ull);
           s_cnt = -1;
         } else {
           s_cnt = np;
+          // tile records of the hash parts (bump allocator, in records; past
+          // the capacity the parts keep -1 and the numeric hashes their keys)
+          long long rbase = -1;
+          if (htiles > 0) {  // (counted even without a buffer: the host sizes it from the total)
+            rbase = (long long)atomicAdd(&info->pkeys_used, (unsigned long long)htiles);
+            if (pbits == nullptr || (rbase + htiles) * kTileRec > pbits_cap) rbase = -1;
+          }
+          long long ro = rbase;
+          for (int p = 0; p < np; ++p) {
+            const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
+            if (t1 > t0 + 1 && t1 - t0 <= kPbitsMaxSpan && rbase >= 0) {
+              for (int t = t0; t < t1; ++t) {
+                s_tkoff[t] = ro + (t - t0);
+                s_tkb[t] = s_tile[t] - s_tile[t0];
+              }
+              ro += t1 - t0;
+            }
+          }
           s_pbase = base;
         }
       }
@@ -629,11 +662,48 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       const int np = s_cnt;
       for (int p = threadIdx.x; p < np; p += THREADS) {
         const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
-        parts[2 * (s_pbase + p)] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
-        parts[2 * (s_pbase + p) + 1] =
+        const long long koff = (t1 > t0 + 1) ? s_tkoff[t0] : -1;
+        parts[3 * (s_pbase + p)] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
+        parts[3 * (s_pbase + p) + 1] =
             make_int4((int)(unsigned)(unsigned long long)as, (int)(unsigned)((unsigned long long)as >> 32),
                       (int)(ae - as), 0);
+        parts[3 * (s_pbase + p) + 2] =
+            make_int4((int)(unsigned)(unsigned long long)koff, (int)(unsigned)((unsigned long long)koff >> 32), 0, 0);
       }
+    }
+    __syncthreads();
+    // tile records of the hash parts (a warp per tile: lane l stores words
+    // 8 l .. 8 l + 7 and their ranks -- keys of the part before each word --
+    // as two 16-byte stores, coalesced), and the clear of every word for the
+    // next row
+    for (int t = w; t < ntiles; t += NW) {
+      const int q0 = t << (kTileLog - 5), q1 = min(nwords, q0 + kTileCols / 32);
+      const long long rec = s_tkoff[t];
+      if (rec >= 0) {
+        const int qa = q0 + 8 * lane;
+        uint32_t wv[8];
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          wv[u] = bm[qa + u];
+          c += __popc(wv[u]);
+        }
+        const int incl = warp_incl_scan(c);
+        int run = s_tkb[t] + incl - c;
+        uint32_t rk[4];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const int r0 = run;
+          run += __popc(wv[u]);
+          rk[u >> 1] = (uint32_t)r0 | ((uint32_t)run << 16);
+          run += __popc(wv[u + 1]);
+        }
+        uint32_t *rp = pbits + rec * kTileRec;
+        reinterpret_cast<uint4 *>(rp)[2 * lane] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        reinterpret_cast<uint4 *>(rp)[2 * lane + 1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+        reinterpret_cast<uint4 *>(rp + 256)[lane] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+      }
+      for (int q = q0 + lane; q < q1; q += 32) bm[q] = 0u;
     }
     __syncthreads();
   }

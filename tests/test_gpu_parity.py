@@ -684,3 +684,27 @@ def test_onephase_graph_replay(spg, monkeypatch):
     A2 = synth.CSR(A.nrows, A.ncols, A.row_ptr, A.col, dA.val.cpu().numpy())
     C = spg.spgemm(dA, dA, sorted=True, ctx=ctx, method="one_phase")
     compare(*C.to_host(), *oracle.spgemm(A2, A2), True, "one-phase graph, new values")
+
+
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_column_parts_tile_records(spg, sorted_out):
+    """Narrow hash parts index their columns by rank from the symbolic's tile
+    records (bitmap words + ranks) once the ctx's record buffer is sized: the
+    first multiply on a fresh ctx hashes (records not yet allocated), the
+    second and third use the records -- all exact vs the oracle, and the
+    records-off switch (SPG_TUNE bit 256) agrees."""
+    specs = [(150000, 50000), (30000, 9000), (9000, 8193), (70000, 4097), (20000, 12000),
+             (600000, 200000), (40000, 30000)]
+    A, B = synth.crafted_rows(specs, 1_000_000, 17)
+    dA, dB = spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B)
+    o = oracle.spgemm(A, B)
+    ctx = spg.Context()
+    for rep in range(3):
+        C = spg.spgemm(dA, dB, sorted=sorted_out, ctx=ctx)
+        compare(*C.to_host(), *o, sorted_out, f"tile records rep {rep}")
+    A3, B3, _ = synth.workload("c3_rmat20", scale=14)
+    dA3 = spg.DeviceCSR.from_host(A3)
+    o3 = oracle.spgemm(A3, B3)
+    for rep in range(2):
+        C = spg.spgemm(dA3, dA3, sorted=sorted_out, ctx=ctx)
+        compare(*C.to_host(), *o3, sorted_out, f"C3 s14 tile records rep {rep}")
