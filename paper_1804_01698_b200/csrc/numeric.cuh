@@ -817,7 +817,9 @@ static_assert(4 * kTPartKeys <= 3 * kTPartT, "multi-tile part: load <= 3/4");
 constexpr int64_t kTRankCols = int64_t(32) * kTileCols;  // sorted emit by bitmap rank up to this span
 constexpr size_t kTDenseBytes = size_t(kTileCols) * 8 + size_t(kTileCols) / 8;
 constexpr size_t kTHashBytes = size_t(kTPartT) * 12 + size_t(kTPartKeys) * 2;
-constexpr size_t kTUnion = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;
+constexpr size_t kTRecDenseBytes = size_t(kTileRec) * 4 + size_t(kTileCols) * 8;  // record + values
+constexpr size_t kTUnion0 = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;
+constexpr size_t kTUnion = kTUnion0 > kTRecDenseBytes ? kTUnion0 : kTRecDenseBytes;
 // entry stage (byte offsets): short list es i32 / ea f64 / epre i32[+1];
 // long list ls i32 / ll i32 (length) / la f64 / lpre i32[+1] (round prefix)
 constexpr size_t kOffEa = 0;
@@ -832,6 +834,8 @@ static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
 static_assert(size_t(kPbitsMaxSpan) * kTileRec * 4 + size_t(kTPartKeys) * 8 <= kTUnion,
               "tile records + rank-indexed values in the table region");
+static_assert(size_t(kTileRec) * 4 + size_t(kTileCols) * 8 <= kTUnion,
+              "one tile record + a dense part's rank-indexed values");
 constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
 static_assert(kTEnt <= 32 * 32, "32-ary owner search");
 
@@ -1014,6 +1018,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
   for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
   long long q_next = 0;  // (thread 0) reserved part after the current one
+  bool dirty = false;    // the dense window was used by a record / hash part (block-uniform)
   if (threadIdx.x == 0) {
     s_res[0][0] = s_res[0][1] = s_res[1][0] = s_res[1][1] = 0ull;
     const long long q = (long long)atomicAdd(counter, 1ull);
@@ -1063,16 +1068,22 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     // values accumulate in vals[rank], and the emit walks the bitmap (column
     // order: sorted for free)
     const long long koff = (long long)(((unsigned long long)(unsigned)P2.y << 32) | (unsigned)P2.x);
-    const bool known = !dense && koff >= 0 && pbits != nullptr;
+    const bool known = koff >= 0 && pbits != nullptr;
     uint32_t *rec = reinterpret_cast<uint32_t *>(base);                       // span x kTileRec words
-    double *rv = reinterpret_cast<double *>(base + size_t(kPbitsMaxSpan) * kTileRec * 4);  // [cnt]
+    double *rv = reinterpret_cast<double *>(base + size_t(t1 - t0) * kTileRec * 4);  // [cnt]
     if (known) {
       const int nrec = (t1 - t0) * kTileRec;
       const uint4 *src = reinterpret_cast<const uint4 *>(pbits + koff * kTileRec);
       for (int q = threadIdx.x; q < nrec / 4; q += THREADS) reinterpret_cast<uint4 *>(rec)[q] = __ldg(src + q);
       for (int r = threadIdx.x; r < cnt; r += THREADS) rv[r] = 0.0;
+      dirty = true;
     } else if (!dense) {
       for (int s = threadIdx.x; s < T; s += THREADS) { hk[s] = kEmpty; hv[s] = 0.0; }
+      dirty = true;
+    } else if (dirty) {  // a dense window after parts that used the region otherwise
+      for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
+      for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
+      dirty = false;
     }
     if (threadIdx.x == 0) s_cnt = 0;
     const int32_t *tk0 = toff + int64_t(t0) * nB, *tk1 = toff + int64_t(t1) * nB;
@@ -1193,7 +1204,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_none);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_none);
         if (sink == 1.2345e300) dbg[13] = 1;
-      } else if (dense) {
+      } else if (dense && !known) {
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_dense);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_dense);
       } else if (known) {
@@ -1214,11 +1225,11 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     const long long ce = instr ? clock64() : 0;
     const int64_t out = s_rp0 + P.z;
     if (tune & 48) {  // (measurement only: no emit; the dense window is still reset)
-      if (dense) {
+      if (dense && !known) {
         for (int s2 = threadIdx.x; s2 < kTileCols; s2 += THREADS) dv[s2] = 0.0;
         for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
       }
-    } else if (dense) {
+    } else if (dense && !known) {
       // keys before each 32-column word (block scan of the word popcounts),
       // then a warp per word: lane l emits column 32 qw + l if present
       // (coalesced stores, ascending columns) and resets its slot
@@ -1252,7 +1263,17 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       }
       __syncthreads();  // (every group read its bits)
       for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
-    } else if (known) {  // walk the part's bitmap words: column order = rank order
+    } else if (known && dense) {  // walk the tile's words, a warp per word: coalesced stores
+      for (int q = w; q < 256; q += NW) {
+        const uint32_t wd = rec[q];
+        if (!wd) continue;  // (warp-uniform)
+        if ((wd >> lane) & 1u) {
+          const int r = reinterpret_cast<const uint16_t *>(rec + 256)[q] + __popc(wd & ((1u << lane) - 1u));
+          c_col[out + r] = (int32_t)(lo + q * 32 + lane);
+          c_val[out + r] = rv[r];
+        }
+      }
+    } else if (known) {  // walk the part's bitmap words (sparse): column order = rank order
       const int nw = (t1 - t0) * 256;
       for (int q = threadIdx.x; q < nw; q += THREADS) {
         const uint32_t *tr = rec + (q >> 8) * kTileRec;

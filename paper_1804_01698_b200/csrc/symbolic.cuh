@@ -52,6 +52,16 @@ __device__ __forceinline__ uint32_t tbm_bit(uint32_t c) { return 1u << ((c >> 8)
 constexpr int kTileRec = 256 + 128;
 constexpr int kPbitsMaxSpan = 16;  // tiles (the record set must fit the numeric's smem region)
 
+// Which parts get tile records: the narrow multi-tile (hash) parts; with
+// SPG_DENSE_RECORDS also the single-tile (dense) ones (A/B, DESIGN.md §9b:
+// C3 parts kernel -10 ms sorted but bitmap symbolic +18 ms, not adopted).
+#ifndef SPG_DENSE_RECORDS
+#define SPG_DENSE_RECORDS 0
+#endif
+__device__ __forceinline__ bool rec_part(int t0, int t1) {
+  return t1 - t0 <= kPbitsMaxSpan && (SPG_DENSE_RECORDS || t1 > t0 + 1);
+}
+
 // Bitmap variant for very long rows: column c -> bit c of an ncols-bit set.
 __device__ __forceinline__ int sym_bitmap_insert(uint32_t *bm, uint32_t c) {
   const uint32_t bit = 1u << (c & 31u);
@@ -521,11 +531,11 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 // the numeric G tier (spg_internal.cuh): part = three int4 records {row,
 // first tile | end tile << 16, keys of the row before the part, keys in the
 // part}, {A.row_ptr[row] (lo, hi), nnz(a_row), 0} and {index of the part's
-// first tile record in pbits (lo, hi) or -1, 0, 0}.  For the multi-tile
-// (hash) parts spanning <= kPbitsMaxSpan tiles the row's bitmap itself is
-// kept: per tile a record of kTileRec words = the tile's 256 bitmap words and
-// 256 u16 ranks (keys of the PART before each word), so the numeric phase
-// indexes the part's columns by rank instead of hashing them.
+// first tile record in pbits (lo, hi) or -1, 0, 0}.  For the parts spanning
+// <= kPbitsMaxSpan tiles the row's bitmap itself is kept: per tile a record
+// of kTileRec words = the tile's 256 bitmap words and 256 u16 ranks (keys of
+// the PART before each word), so the numeric phase indexes the part's
+// columns by rank (no hashing, no occupancy bits).
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restrict__ rows,
@@ -626,10 +636,10 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       __syncthreads();
       if (threadIdx.x == 0) {
         int np = 0;
-        long long htiles = 0;  // tiles of the row's narrow multi-tile (hash) parts
+        long long htiles = 0;  // tiles of the row's parts spanning <= kPbitsMaxSpan tiles
         for (int t = s_nne[0]; t < ntiles; t = s_nne[s_nxt[t]]) {
           s_cut[np++] = t | (s_nxt[t] << 16);
-          if (s_nxt[t] > t + 1 && s_nxt[t] - t <= kPbitsMaxSpan) htiles += s_nxt[t] - t;
+          if (rec_part(t, s_nxt[t])) htiles += s_nxt[t] - t;
         }
         const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
         if (base + np > parts_cap) {
@@ -647,7 +657,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
           long long ro = rbase;
           for (int p = 0; p < np; ++p) {
             const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
-            if (t1 > t0 + 1 && t1 - t0 <= kPbitsMaxSpan && rbase >= 0) {
+            if (rec_part(t0, t1) && rbase >= 0) {
               for (int t = t0; t < t1; ++t) {
                 s_tkoff[t] = ro + (t - t0);
                 s_tkb[t] = s_tile[t] - s_tile[t0];
@@ -662,7 +672,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       const int np = s_cnt;
       for (int p = threadIdx.x; p < np; p += THREADS) {
         const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
-        const long long koff = (t1 > t0 + 1) ? s_tkoff[t0] : -1;
+        const long long koff = s_tkoff[t0];
         parts[3 * (s_pbase + p)] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
         parts[3 * (s_pbase + p) + 1] =
             make_int4((int)(unsigned)(unsigned long long)as, (int)(unsigned)((unsigned long long)as >> 32),
