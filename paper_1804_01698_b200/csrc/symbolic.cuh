@@ -415,7 +415,10 @@ __device__ __forceinline__ void for_row(const DevCSR &A, const DevCSR &B, int64_
 // Rows whose B rows average >= kSeqMinLen entries use the sequential
 // enumeration (no owner search, distinct keys per round); shorter ones the
 // flattened one (full 32-lane rounds).
-constexpr int kSeqMinLen = 16;
+#ifndef SPG_SEQ_MIN_LEN
+#define SPG_SEQ_MIN_LEN 16
+#endif
+constexpr int kSeqMinLen = SPG_SEQ_MIN_LEN;
 __device__ __forceinline__ bool use_seq(int64_t flop, int64_t nnz_a) {
   return flop >= int64_t(kSeqMinLen) * nnz_a;
 }
@@ -459,6 +462,11 @@ __device__ __forceinline__ int warp_bucket_insert(uint32_t *tab, int logT, bool 
   return added;
 }
 
+// rounds of one B row in flight per warp in the sequential walk (the gathers
+// of the next rounds are issued before the current one is hashed)
+#ifndef SPG_SYM_WARP_DEPTH
+#define SPG_SYM_WARP_DEPTH 2
+#endif
 template <int TMAX, int WARPS, bool BUCKET = false>
 __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restrict__ rows,
                                                          int64_t nrows, DevCSR A, DevCSR B,
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
       if (BUCKET) cnt += warp_bucket_insert(tab, logT, act, c);
       else if (act) cnt += sym_insert(tab, c, logT);
     };
-    if (use_seq(flop[i], ae - as)) for_row<true, false, 2>(A, B, as, ae, 0, 1, ins);
+    if (use_seq(flop[i], ae - as)) for_row<true, false, SPG_SYM_WARP_DEPTH>(A, B, as, ae, 0, 1, ins);
     else for_row<false, false, 2>(A, B, as, ae, 0, 1, ins);
     if (!BUCKET) cnt = warp_sum(cnt);  // (bucket mode: every lane holds the warp's count)
     if (lane == 0) row_nnz[i] = cnt;
