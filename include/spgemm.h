@@ -132,7 +132,11 @@ spg_status spg_symbolic(spg_ctx *ctx, const spg_csr *A, const spg_csr *B,
 
 /* Phase 2 -- numeric ("Numeric(C, A, B)"; "In numeric phase ... we need
  * to store the resulting value data"; optional ascending sort).
- * Must follow spg_symbolic on the same ctx with the same A, B and C_row_ptr.
+ * Must follow spg_symbolic on the same ctx with the same A, B and C_row_ptr:
+ * SPG_ERR_STATE if any of A.row_ptr, A.col_idx, B.row_ptr, B.col_idx,
+ * C_row_ptr, A.nrows or B.ncols differs from that call (pointer identity; the
+ * CONTENTS of A and B must not change in between -- not checked, since that
+ * would cost a device round trip).
  *   C_col_idx, C_val : device, caller-allocated with nnz_C entries.
  *   sorted           : 0 = columns of each C row in unspecified order;
  *                      1 = strictly increasing columns in every row.

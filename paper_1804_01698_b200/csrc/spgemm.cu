@@ -94,6 +94,7 @@ struct spg_ctx {
   // plan of the last symbolic
   bool have_plan = false;
   const int64_t *plan_a_rp = nullptr, *plan_b_rp = nullptr, *plan_c_rp = nullptr;
+  const int32_t *plan_a_col = nullptr, *plan_b_col = nullptr;
   int64_t plan_m = 0, plan_ncols = 0;
   PlanInfo plan{};
 };
@@ -736,6 +737,8 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   c->plan_a_rp = A0->row_ptr;
   c->plan_b_rp = B->row_ptr;
   c->plan_c_rp = C_row_ptr;
+  c->plan_a_col = A0->col_idx;
+  c->plan_b_col = B->col_idx;
   c->plan_m = m;
   c->plan_ncols = B->ncols;
   return SPG_OK;
@@ -750,7 +753,8 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
   if (A->ncols != B->nrows) return fail(c, SPG_ERR_DIM_MISMATCH, "A.ncols != B.nrows");
   if (sorted != 0 && sorted != 1) return fail(c, SPG_ERR_INVALID_ARG, "sorted must be 0 or 1");
   if (!c->have_plan || c->plan_a_rp != A->row_ptr || c->plan_b_rp != B->row_ptr ||
-      c->plan_c_rp != C_row_ptr || c->plan_m != A->nrows || c->plan_ncols != B->ncols)
+      c->plan_c_rp != C_row_ptr || c->plan_a_col != A->col_idx || c->plan_b_col != B->col_idx ||
+      c->plan_m != A->nrows || c->plan_ncols != B->ncols)
     return fail(c, SPG_ERR_STATE, "spg_numeric without a matching spg_symbolic");
   const PlanInfo &h = c->plan;
   if (h.nnz_total == 0) return SPG_OK;

@@ -75,6 +75,22 @@ def test_numeric_without_symbolic_is_state_error(spg):
         _lib.spg_numeric(c2.handle, A.c(), A.c(), rp.data_ptr(), 0, 0, True, 0)
 
 
+def test_numeric_with_other_arrays_is_state_error(spg):
+    """The plan is keyed on every array the symbolic phase read: a numeric call
+    whose A or B carries another col_idx array is refused."""
+    from paper_1804_01698_b200 import _lib
+    c2 = spg.Context()
+    A = spg.DeviceCSR.from_host(synth.random_sparse(40, 40, 0.2, 3))
+    rp, nnz, _ = spg.spg_symbolic(A, A, c2)
+    A2 = spg.DeviceCSR(A.nrows, A.ncols, A.row_ptr, A.col.clone(), A.val)
+    for a, b in ((A2, A), (A, A2)):
+        with pytest.raises(_lib.SpgError, match="STATE"):
+            spg.spg_numeric(a, b, rp, nnz, ctx=c2)
+    C = spg.spg_numeric(A, A, rp, nnz, ctx=c2)  # the matching call still runs
+    compare(*C.to_host(), *oracle.spgemm(synth.random_sparse(40, 40, 0.2, 3),
+                                         synth.random_sparse(40, 40, 0.2, 3)), True, "plan keyed")
+
+
 def test_identity_bitexact(spg, ctx):
     A = synth.er_poisson(2000, 8.0, 5)
     I = synth.identity(2000)
