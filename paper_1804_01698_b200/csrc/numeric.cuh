@@ -46,6 +46,21 @@ __device__ __forceinline__ uint32_t hash_vslot(uint32_t s, int logT) {
   return ((s & 3u) << (logT - 2)) + (s >> 2);
 }
 
+// Dense windows start every slot at -0.0: -0.0 + v = v for every v, and a
+// slot that received any product can never hold -0.0 again, because every
+// product is first mapped through v + (+0.0) (which turns a -0.0 product into
+// +0.0 and leaves every other value, NaN included, unchanged; the oracle's
+// accumulator starts at +0.0, so the sums are the same).  So a slot is present
+// iff its bits differ from -0.0: no occupancy bitmap, no second atomic per
+// product.
+constexpr unsigned long long kNegZeroBits = 0x8000000000000000ull;
+__device__ __forceinline__ double nz_product(double v) { return __dadd_rn(v, 0.0); }
+// fp64 add into shared memory at a 32-bit shared address (the LDS + CAS-spin
+// loop sm_100a lowers it to; no generic-address arithmetic in the loop)
+__device__ __forceinline__ void red_shared_f64(uint32_t saddr, double v) {
+  asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(saddr), "d"(v) : "memory");
+}
+
 // Lanes of a round holding the same key c combine their values into the
 // lowest such lane; returns true for the lanes that then hold a key to apply
 // (active, first of their key).  Summation order inside a round is free
@@ -910,8 +925,10 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int32_t 
 
 // Rounds [g0, g1) of the staged LONG entries: entry j covers rounds
 // [lpre[j], lpre[j+1]) = ceil(ll[j] / 32) rounds; round r of entry j is the
-// products ls[j] + 32 r + lane of ONE B row segment (distinct columns).  Two
-// rounds per step (both gathers issued before either update).
+// products ls[j] + 32 r + lane of ONE B row segment (distinct columns).  The
+// warp walks its entries one at a time (segment start, length and a_ik in
+// registers for the whole entry), two rounds per step with both gathers
+// issued before either update.
 template <typename F>
 __device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *ls,
                                                 const int32_t *ll, const double *la,
@@ -919,35 +936,33 @@ __device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *
                                                 int g1, F &&f) {
   if (g0 >= g1) return;
   const int lane = lane_id();
-  int cur = tpart_find(lpre, n, g0);
-  int rbeg = lpre[cur], rend = cur + 1 < n ? lpre[cur + 1] : R, s0 = ls[cur], L = ll[cur];
-  double a = la[cur];
-  auto at = [&](int g, bool &act, int64_t &q, double &av) {
-    while (g >= rend) {  // warp-uniform: next entry
-      ++cur;
-      rbeg = rend;
-      rend = cur + 1 < n ? lpre[cur + 1] : R;
-      s0 = ls[cur];
-      L = ll[cur];
-      a = la[cur];
+  int j = tpart_find(lpre, n, g0);
+  int g = g0;
+  while (g < g1) {
+    const int rb = lpre[j];
+    const int re = min(g1, j + 1 < n ? lpre[j + 1] : R);
+    const int L = ll[j];
+    const double a = la[j];
+    const int32_t *pc = B.col + ls[j];
+    const double *pv = B.val + ls[j];
+    int t = (g - rb) * 32 + lane;
+    for (; g + 1 < re; g += 2, t += 64) {
+      const bool act0 = t < L, act1 = t + 32 < L;
+      const uint32_t c0 = act0 ? (uint32_t)__ldg(pc + t) : 0u;
+      const double v0 = act0 ? __ldg(pv + t) : 0.0;
+      const uint32_t c1 = act1 ? (uint32_t)__ldg(pc + t + 32) : 0u;
+      const double v1 = act1 ? __ldg(pv + t + 32) : 0.0;
+      f(act0, c0, a * v0);  // a_ik * b_kj (Fig:code_spgemm l.5)
+      f(act1, c1, a * v1);
     }
-    const int t = (g - rbeg) * 32 + lane;
-    act = t < L;
-    q = int64_t(s0) + t;
-    av = a;
-  };
-  for (int g = g0; g < g1; g += 2) {
-    bool act0, act1 = false;
-    int64_t q0, q1 = 0;
-    double a0, a1 = 0.0;
-    at(g, act0, q0, a0);
-    if (g + 1 < g1) at(g + 1, act1, q1, a1);
-    const uint32_t c0 = act0 ? (uint32_t)__ldg(B.col + q0) : 0u;
-    const double v0 = act0 ? __ldg(B.val + q0) : 0.0;
-    const uint32_t c1 = act1 ? (uint32_t)__ldg(B.col + q1) : 0u;
-    const double v1 = act1 ? __ldg(B.val + q1) : 0.0;
-    f(act0, c0, a0 * v0);  // a_ik * b_kj (Fig:code_spgemm l.5)
-    f(act1, c1, a1 * v1);
+    if (g < re) {
+      const bool act0 = t < L;
+      const uint32_t c0 = act0 ? (uint32_t)__ldg(pc + t) : 0u;
+      const double v0 = act0 ? __ldg(pv + t) : 0.0;
+      f(act0, c0, a * v0);
+      ++g;
+    }
+    ++j;
   }
 }
 
@@ -1002,7 +1017,6 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char *base = reinterpret_cast<char *>(s_dyn_f64);
   double *dv = reinterpret_cast<double *>(base);                          // dense window
-  uint32_t *dbm = reinterpret_cast<uint32_t *>(base + size_t(kTileCols) * 8);
   double *hv = reinterpret_cast<double *>(base);                          // hash table
   uint32_t *hk = reinterpret_cast<uint32_t *>(base + size_t(kTPartT) * 8);
   uint16_t *slot_of = reinterpret_cast<uint16_t *>(base + size_t(kTPartT) * 12);
@@ -1014,9 +1028,11 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   int32_t *ll = reinterpret_cast<int32_t *>(eb + kOffLl);
   int32_t *epre = reinterpret_cast<int32_t *>(eb + kOffEpre);
   int32_t *lpre = reinterpret_cast<int32_t *>(eb + kOffLpre);
-  // the dense window starts clean; every dense part resets what it used
-  for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
-  for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
+  // the dense window starts clean (every slot -0.0: absent); every dense part
+  // resets what it used
+  unsigned long long *dvb = reinterpret_cast<unsigned long long *>(dv);
+  const uint32_t dv_sa = (uint32_t)__cvta_generic_to_shared(dv);
+  for (int s = threadIdx.x; s < kTileCols; s += THREADS) dvb[s] = kNegZeroBits;
   long long q_next = 0;  // (thread 0) reserved part after the current one
   bool dirty = false;    // the dense window was used by a record / hash part (block-uniform)
   if (threadIdx.x == 0) {
@@ -1081,18 +1097,15 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       for (int s = threadIdx.x; s < T; s += THREADS) { hk[s] = kEmpty; hv[s] = 0.0; }
       dirty = true;
     } else if (dirty) {  // a dense window after parts that used the region otherwise
-      for (int s = threadIdx.x; s < kTileCols; s += THREADS) dv[s] = 0.0;
-      for (int s = threadIdx.x; s < kTileCols / 32; s += THREADS) dbm[s] = 0u;
+      for (int s = threadIdx.x; s < kTileCols; s += THREADS) dvb[s] = kNegZeroBits;
       dirty = false;
     }
     if (threadIdx.x == 0) s_cnt = 0;
     const int32_t *tk0 = toff + int64_t(t0) * nB, *tk1 = toff + int64_t(t1) * nB;
+    const uint32_t lo32 = (uint32_t)lo;
     auto acc_dense = [&](bool act, uint32_t c, double v) {
-      if (act) {
-        const uint32_t off = c - (uint32_t)lo;
-        atomicAdd(dv + dense_slot(off), v);  // c_ij <- c_ij + value (l.8), dense window
-        atomicOr(dbm + tbm_word(off), tbm_bit(off));  // (transposed tile bitmap)
-      }
+      // c_ij <- c_ij + value (l.8), dense window (presence: the slot left -0.0)
+      if (act) red_shared_f64(dv_sa + 8u * dense_slot(c - lo32), nz_product(v));
     };
     auto acc_known = [&](bool act, uint32_t c, double v) {  // rank of the column in the part
       if (act) {
@@ -1225,44 +1238,40 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     const long long ce = instr ? clock64() : 0;
     const int64_t out = s_rp0 + P.z;
     if (tune & 48) {  // (measurement only: no emit; the dense window is still reset)
-      if (dense && !known) {
-        for (int s2 = threadIdx.x; s2 < kTileCols; s2 += THREADS) dv[s2] = 0.0;
-        for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
-      }
+      if (dense && !known)
+        for (int s2 = threadIdx.x; s2 < kTileCols; s2 += THREADS) dvb[s2] = kNegZeroBits;
     } else if (dense && !known) {
-      // keys before each 32-column word (block scan of the word popcounts),
-      // then a warp per word: lane l emits column 32 qw + l if present
-      // (coalesced stores, ascending columns) and resets its slot
-      static_assert(kTileCols / 32 <= THREADS, "one word per thread");
-      const int nwd = kTileCols / 32;  // 32-column groups
-      // (transposed bitmap: the 32 columns 32 qw + l are bit qw >> 3 of
-      // words 32 (qw & 7) + l -- a warp reads them with one conflict-free
-      // load and a ballot)
-      int32_t *gcnt = reinterpret_cast<int32_t *>(eb);
-      int32_t *wcum = gcnt + nwd;
-      for (int qw = w; qw < nwd; qw += NW) {
-        const unsigned bal = __ballot_sync(kFull, (dbm[(qw & 7) * 32 + lane] >> (qw >> 3)) & 1u);
-        if (lane == 0) gcnt[qw] = __popc(bal);
+      // warp w owns the 32-column groups [GPW w, GPW (w + 1)) (ascending
+      // columns): one pass of ballots over the present slots (bits != -0.0)
+      // counts them, a scan of the NW warp totals gives each warp's output
+      // start, a second pass stores the present entries (coalesced, ascending
+      // columns) and resets their slots to -0.0
+      constexpr int GPW = (kTileCols / 32) / NW;
+      static_assert(GPW * NW * 32 == kTileCols, "groups per warp");
+      unsigned msk[GPW];
+      int tot = 0;
+#pragma unroll
+      for (int j = 0; j < GPW; ++j) {
+        const uint32_t off = uint32_t(w * GPW + j) * 32u + lane;
+        msk[j] = __ballot_sync(kFull, dvb[dense_slot(off)] != kNegZeroBits);
+        tot += __popc(msk[j]);
       }
+      if (lane == 0) s_red[w] = tot;
       __syncthreads();
-      int totw;
-      const int wx = block_excl_scan_int((int)threadIdx.x < nwd ? gcnt[threadIdx.x] : 0, s_warp, &totw);
-      if ((int)threadIdx.x < nwd) wcum[threadIdx.x] = wx;
-      __syncthreads();
-      for (int qw = w; qw < nwd; qw += NW) {
-        const uint32_t wi = (qw & 7) * 32 + lane, bt = 1u << (qw >> 3);
-        const bool present = (dbm[wi] & bt) != 0u;
-        const unsigned bal = __ballot_sync(kFull, present);
-        if (present) {
-          const int64_t o = out + wcum[qw] + __popc(bal & ((1u << lane) - 1u));
-          c_col[o] = (int32_t)(lo + qw * 32 + lane);
-          const uint32_t ds = dense_slot(qw * 32 + lane);
-          c_val[o] = dv[ds];
-          dv[ds] = 0.0;
+      int64_t o = out + (int)__reduce_add_sync(kFull, lane < w ? (unsigned)s_red[lane] : 0u);
+      const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+      for (int j = 0; j < GPW; ++j) {
+        if ((msk[j] >> lane) & 1u) {
+          const uint32_t off = uint32_t(w * GPW + j) * 32u + lane;
+          const uint32_t ds = dense_slot(off);
+          const int64_t p = o + __popc(msk[j] & below);
+          c_col[p] = (int32_t)(lo + off);
+          c_val[p] = dv[ds];
+          dvb[ds] = kNegZeroBits;
         }
+        o += __popc(msk[j]);
       }
-      __syncthreads();  // (every group read its bits)
-      for (int s2 = threadIdx.x; s2 < kTileCols / 32; s2 += THREADS) dbm[s2] = 0u;
     } else if (known && dense) {  // walk the tile's words, a warp per word: coalesced stores
       for (int q = w; q < 256; q += NW) {
         const uint32_t wd = rec[q];
@@ -1273,19 +1282,22 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
           c_val[out + r] = rv[r];
         }
       }
-    } else if (known) {  // walk the part's bitmap words (sparse): column order = rank order
+    } else if (known) {
+      // values in rank order = column order (coalesced copy); columns by a
+      // walk of the part's bitmap words (sparse: mostly one bit per word)
+      for (int r = threadIdx.x; r < cnt; r += THREADS) c_val[out + r] = rv[r];
       const int nw = (t1 - t0) * 256;
+      int32_t *ccol = c_col + out;
+      const int32_t lo_i = (int32_t)lo;
       for (int q = threadIdx.x; q < nw; q += THREADS) {
         const uint32_t *tr = rec + (q >> 8) * kTileRec;
         uint32_t wd = tr[q & 255];
         if (!wd) continue;
         int r = reinterpret_cast<const uint16_t *>(tr + 256)[q & 255];
+        const int32_t cb = lo_i + (q << 5);
         while (wd) {
-          const int bit = __ffs(wd) - 1;
+          ccol[r++] = cb + __ffs(wd) - 1;
           wd &= wd - 1;
-          c_col[out + r] = (int32_t)(lo + (int64_t(q) << 5) + bit);
-          c_val[out + r] = rv[r];
-          ++r;
         }
       }
     } else if (!sorted) {

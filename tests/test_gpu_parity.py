@@ -724,3 +724,26 @@ def test_column_parts_tile_records(spg, sorted_out):
     for rep in range(2):
         C = spg.spgemm(dA3, dA3, sorted=sorted_out, ctx=ctx)
         compare(*C.to_host(), *o3, sorted_out, f"C3 s14 tile records rep {rep}")
+
+
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_dense_window_negative_zero_products(spg, ctx, sorted_out):
+    """Dense column windows mark absent slots with -0.0 (DESIGN.md reading
+    R17): every product is mapped through v + (+0.0) first, so an entry whose
+    only terms are -0.0 products (a_ik < 0 times b_kj = 0.0) is still present
+    (structure is value-blind, reading R1) with value 0.0.  One long row with
+    two heavy tiles (dense parts) and a multi-tile light run (hash part)."""
+    A, B = _tile_rows([6000, 3000, 700, 0, 900], 8, 41)
+    bval = B.val.copy()
+    bval[B.row_ptr[2]:B.row_ptr[3]] = 0.0      # B row 2: every value +0.0
+    bval[B.row_ptr[1]:B.row_ptr[2]] *= -1.0    # B row 1: negative values
+    B = synth.CSR(B.nrows, B.ncols, B.row_ptr, B.col, bval)
+    aval = A.val.copy()
+    aval[2] = -1.25                            # a_02 < 0: -0.0 products
+    A = synth.CSR(A.nrows, A.ncols, A.row_ptr, A.col, aval)
+    o_rp, o_col, o_val = oracle.spgemm(A, B)
+    assert (o_val == 0.0).sum() > 1000         # keys reached only through B row 2
+    dA, dB = spg.DeviceCSR.from_host(A), spg.DeviceCSR.from_host(B)
+    for rep in range(2):                       # (the second with tile records)
+        C = spg.spgemm(dA, dB, sorted=sorted_out, ctx=ctx)
+        compare(*C.to_host(), o_rp, o_col, o_val, sorted_out, f"-0.0 products rep {rep}")
