@@ -29,17 +29,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Build the library (``out``: another path, for A/B variants built with
+    SPG_NVCC_EXTRA defines; the in-tree library is the product)."""
+    if out is None and not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     extra = os.environ.get("SPG_NVCC_EXTRA", "").split()  # (A/B builds only)
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", os.path.join(CSRC, "spgemm.cu")]
+    dst = out or LIB
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", dst + ".tmp", os.path.join(CSRC, "spgemm.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(dst + ".tmp", dst)
+    return dst
 
 
 if __name__ == "__main__":

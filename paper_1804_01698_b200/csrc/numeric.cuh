@@ -53,6 +53,28 @@ __device__ __forceinline__ uint32_t hash_vslot(uint32_t s, int logT) {
 // accumulator starts at +0.0, so the sums are the same).  So a slot is present
 // iff its bits differ from -0.0: no occupancy bitmap, no second atomic per
 // product.
+// C (written once, never re-read by the multiply) goes out with evict-first
+// stores so its 116 GB stream (config 3) does not push B's rows out of L2;
+// the tile records (read once) come in with evict-first loads.
+#ifndef SPG_STCS
+#define SPG_STCS 1
+#endif
+template <typename T>
+__device__ __forceinline__ void st_c(T *p, T v) {
+#if SPG_STCS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+template <typename T>
+__device__ __forceinline__ T ld_once(const T *p) {
+#if SPG_STCS
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
 constexpr unsigned long long kNegZeroBits = 0x8000000000000000ull;
 __device__ __forceinline__ double nz_product(double v) { return __dadd_rn(v, 0.0); }
 // fp64 add into shared memory at a 32-bit shared address (the LDS + CAS-spin
@@ -925,16 +947,21 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int32_t 
 
 // Rounds [g0, g1) of the staged LONG entries: entry j covers rounds
 // [lpre[j], lpre[j+1]) = ceil(ll[j] / 32) rounds; round r of entry j is the
-// products ls[j] + 32 r + lane of ONE B row segment (distinct columns).  The
-// warp walks its entries one at a time (segment start, length and a_ik in
-// registers for the whole entry), two rounds per step with both gathers
-// issued before either update.
+// products ls[j] + 32 r + lane of ONE B row segment (distinct columns).  A
+// rolling software pipeline of kLD register slots: right after the round in
+// slot d is applied, the slot is refilled with the round kLD ahead (the load
+// cursor walks the entries), so kLD independent gathers stay in flight
+// across entry boundaries.  Inactive lanes hold the column kEmpty.
+#ifndef SPG_LONG_DEPTH
+#define SPG_LONG_DEPTH 0
+#endif
+constexpr int kLD = SPG_LONG_DEPTH;
 template <typename F>
-__device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *ls,
-                                                const int32_t *ll, const double *la,
-                                                const int32_t *lpre, int n, int R, int g0,
-                                                int g1, F &&f) {
-  if (g0 >= g1) return;
+__device__ __forceinline__ void for_long_rounds_entry(const DevCSR &B, const int32_t *ls,
+                                                      const int32_t *ll, const double *la,
+                                                      const int32_t *lpre, int n, int R,
+                                                      int g0, int g1, F &&f) {
+  // (SPG_LONG_DEPTH=0: entry by entry, two rounds per step inside an entry)
   const int lane = lane_id();
   int j = tpart_find(lpre, n, g0);
   int g = g0;
@@ -952,7 +979,7 @@ __device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *
       const double v0 = act0 ? __ldg(pv + t) : 0.0;
       const uint32_t c1 = act1 ? (uint32_t)__ldg(pc + t + 32) : 0u;
       const double v1 = act1 ? __ldg(pv + t + 32) : 0.0;
-      f(act0, c0, a * v0);  // a_ik * b_kj (Fig:code_spgemm l.5)
+      f(act0, c0, a * v0);
       f(act1, c1, a * v1);
     }
     if (g < re) {
@@ -963,6 +990,62 @@ __device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *
       ++g;
     }
     ++j;
+  }
+}
+
+template <typename F>
+__device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *ls,
+                                                const int32_t *ll, const double *la,
+                                                const int32_t *lpre, int n, int R, int g0,
+                                                int g1, F &&f) {
+  if (g0 >= g1) return;
+  if constexpr (kLD == 0) {
+    for_long_rounds_entry(B, ls, ll, la, lpre, n, R, g0, g1, f);
+    return;
+  }
+  constexpr int D = kLD > 0 ? kLD : 1;
+  const int lane = lane_id();
+  int j = tpart_find(lpre, n, g0);  // load cursor: entry j, its rounds [rb, re)
+  int rb = lpre[j], re = j + 1 < n ? lpre[j + 1] : R, L = ll[j];
+  const int32_t *pc = B.col + ls[j];
+  const double *pv = B.val + ls[j];
+  int gl = g0;  // next round to load
+  uint32_t c[D];
+  double v[D];
+  int jd[D];  // entry of the slot's round (its a_ik is read from smem when applied)
+  auto load = [&](int d) {  // round gl into slot d (gl < g1, warp-uniform)
+    while (gl >= re) {
+      ++j;
+      rb = re;
+      re = j + 1 < n ? lpre[j + 1] : R;
+      L = ll[j];
+      pc = B.col + ls[j];
+      pv = B.val + ls[j];
+    }
+    const int t = (gl - rb) * 32 + lane;
+    c[d] = kEmpty;
+    v[d] = 0.0;
+    if (t < L) {
+      c[d] = (uint32_t)__ldg(pc + t);
+      v[d] = __ldg(pv + t);
+    }
+    jd[d] = j;
+    ++gl;
+  };
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    c[d] = kEmpty;
+    jd[d] = 0;
+    if (gl < g1) load(d);
+  }
+  for (int g = g0; g < g1; g += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (g + d < g1) {
+        f(c[d] != kEmpty, c[d], la[jd[d]] * v[d]);  // a_ik * b_kj (Fig:code_spgemm l.5)
+        if (gl < g1) load(d);
+      }
+    }
   }
 }
 
@@ -995,12 +1078,17 @@ __device__ __forceinline__ void block_excl_scan3(const int (&v)[3], int (&ex)[3]
   }
 }
 
+#ifndef SPG_TPART_INSTR
+#define SPG_TPART_INSTR 0
+#endif
+constexpr bool kTpartInstr = SPG_TPART_INSTR != 0;  // per-phase clock counters into dbg[]
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     DevCSR A, DevCSR B, const int64_t *__restrict__ c_rp, int32_t *__restrict__ c_col,
     double *__restrict__ c_val, int sorted, const int4 *__restrict__ parts, int64_t nparts,
     const int32_t *__restrict__ toff, int64_t nB, unsigned long long *counter, int tune,
-    unsigned long long *dbg, const uint32_t *__restrict__ pbits) {
+    unsigned long long *dbg, const uint32_t *__restrict__ pbits,
+    const uint16_t *__restrict__ dpfx) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_warp[33];
   __shared__ int s_red[66];
@@ -1009,6 +1097,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   // (entries << 32) | (products or rounds)
   __shared__ unsigned long long s_res[2][2];
   __shared__ long long s_rp0;
+  __shared__ __align__(16) uint16_t s_dp[kDenseStripes];  // dense part: keys before each warp's stripe
   // part pipeline (thread 0): the part after next is reserved and the next
   // part's records are loaded while this part runs; published at its end
   __shared__ long long s_q;
@@ -1047,7 +1136,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     q_next = (long long)atomicAdd(counter, 1ull);
   }
   __syncthreads();
-  const bool instr = (tune & 8) && threadIdx.x == 0;
+  const bool instr = kTpartInstr && threadIdx.x == 0;  // (phase clocks: SPG_TPART_INSTR builds)
   int par = 0;  // staging buffer parity (alternates per chunk)
   while (true) {
     const int64_t q = s_q;
@@ -1059,6 +1148,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     long long q_after = 0;
     if (threadIdx.x == 0) {
       cp_async8(&s_rp0, c_rp + P.x);
+      if (dpfx != nullptr && P2.z >= 0 && (P.y >> 16) == (P.y & 0xFFFF) + 1) {  // dense part's stripe prefixes
+        cp_async16(&s_dp[0], dpfx + int64_t(P2.z) * kDenseStripes);
+        cp_async16(&s_dp[8], dpfx + int64_t(P2.z) * kDenseStripes + 8);
+      }
       if (q_next < nparts) {
         cp_async16(&s_Pn[0], parts + 3 * q_next);
         cp_async16(&s_Pn[1], parts + 3 * q_next + 1);
@@ -1090,7 +1183,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     if (known) {
       const int nrec = (t1 - t0) * kTileRec;
       const uint4 *src = reinterpret_cast<const uint4 *>(pbits + koff * kTileRec);
-      for (int q = threadIdx.x; q < nrec / 4; q += THREADS) reinterpret_cast<uint4 *>(rec)[q] = __ldg(src + q);
+      for (int q = threadIdx.x; q < nrec / 4; q += THREADS) reinterpret_cast<uint4 *>(rec)[q] = ld_once(src + q);
       for (int r = threadIdx.x; r < cnt; r += THREADS) rv[r] = 0.0;
       dirty = true;
     } else if (!dense) {
@@ -1196,7 +1289,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
           ++xs;
         }
       }
-      if (tune & 8) {  // (measurement: products of the long segments)
+      if (kTpartInstr) {  // (measurement: products of the long segments)
         unsigned long long lp = 0;
 #pragma unroll
         for (int u = 0; u < kPer; ++u) lp += Ls[u] >= kTLongSeg ? (unsigned long long)Ls[u] : 0ull;
@@ -1240,6 +1333,33 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     if (tune & 48) {  // (measurement only: no emit; the dense window is still reset)
       if (dense && !known)
         for (int s2 = threadIdx.x; s2 < kTileCols; s2 += THREADS) dvb[s2] = kNegZeroBits;
+    } else if (dense && !known && dpfx != nullptr && P2.z >= 0) {
+      // one pass: warp w owns the 512-column stripe w (32-column groups
+      // [GPW w, GPW (w + 1))) and starts at the symbolic's count of the
+      // tile's keys before it; present slots (bits != -0.0) are stored in
+      // column order (coalesced) and reset to -0.0
+      constexpr int GPW = (kTileCols / 32) / NW;
+      static_assert(GPW * NW * 32 == kTileCols && NW == kDenseStripes, "one stripe per warp");
+      const int64_t ob = out + s_dp[w];
+      int32_t *cc = c_col + ob;
+      double *cvp = c_val + ob;
+      const unsigned below = (1u << lane) - 1u;
+      const int32_t cbase = (int32_t)lo + w * GPW * 32 + lane;
+      int o = 0;
+#pragma unroll 4
+      for (int j = 0; j < GPW; ++j) {
+        const uint32_t ds = dense_slot(uint32_t(w * GPW + j) * 32u + lane);
+        const unsigned long long bits = dvb[ds];
+        const bool pres = bits != kNegZeroBits;
+        const unsigned m = __ballot_sync(kFull, pres);
+        if (pres) {
+          const int p = o + __popc(m & below);
+          st_c(cc + p, cbase + j * 32);
+          st_c(cvp + p, __longlong_as_double(bits));
+          dvb[ds] = kNegZeroBits;
+        }
+        o += __popc(m);
+      }
     } else if (dense && !known) {
       // warp w owns the 32-column groups [GPW w, GPW (w + 1)) (ascending
       // columns): one pass of ballots over the present slots (bits != -0.0)
@@ -1266,8 +1386,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
           const uint32_t off = uint32_t(w * GPW + j) * 32u + lane;
           const uint32_t ds = dense_slot(off);
           const int64_t p = o + __popc(msk[j] & below);
-          c_col[p] = (int32_t)(lo + off);
-          c_val[p] = dv[ds];
+          st_c(c_col + p, (int32_t)(lo + off));
+          st_c(c_val + p, dv[ds]);
           dvb[ds] = kNegZeroBits;
         }
         o += __popc(msk[j]);
@@ -1278,14 +1398,14 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         if (!wd) continue;  // (warp-uniform)
         if ((wd >> lane) & 1u) {
           const int r = reinterpret_cast<const uint16_t *>(rec + 256)[q] + __popc(wd & ((1u << lane) - 1u));
-          c_col[out + r] = (int32_t)(lo + q * 32 + lane);
-          c_val[out + r] = rv[r];
+          st_c(c_col + out + r, (int32_t)(lo + q * 32 + lane));
+          st_c(c_val + out + r, rv[r]);
         }
       }
     } else if (known) {
       // values in rank order = column order (coalesced copy); columns by a
       // walk of the part's bitmap words (sparse: mostly one bit per word)
-      for (int r = threadIdx.x; r < cnt; r += THREADS) c_val[out + r] = rv[r];
+      for (int r = threadIdx.x; r < cnt; r += THREADS) st_c(c_val + out + r, rv[r]);
       const int nw = (t1 - t0) * 256;
       int32_t *ccol = c_col + out;
       const int32_t lo_i = (int32_t)lo;
@@ -1296,15 +1416,15 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         int r = reinterpret_cast<const uint16_t *>(tr + 256)[q & 255];
         const int32_t cb = lo_i + (q << 5);
         while (wd) {
-          ccol[r++] = cb + __ffs(wd) - 1;
+          st_c(ccol + r++, (int32_t)(cb + __ffs(wd) - 1));
           wd &= wd - 1;
         }
       }
     } else if (!sorted) {
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
         const int s = slot_of[p];
-        c_col[out + p] = (int32_t)hk[s];
-        c_val[out + p] = hv[hash_vslot(s, logT)];
+        st_c(c_col + out + p, (int32_t)hk[s]);
+        st_c(c_val + out + p, hv[hash_vslot(s, logT)]);
       }
     } else {
       // gather the pairs into the entry stage, sort them with the table
@@ -1347,8 +1467,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
           const uint32_t off = gk[p] - (uint32_t)lo;
           const uint32_t wd = off >> 5;
           const int64_t o = out + rpre[wd] + __popc(rbm[wd] & ((1u << (off & 31u)) - 1u));
-          c_col[o] = (int32_t)gk[p];
-          c_val[o] = gv[p];
+          st_c(c_col + o, (int32_t)gk[p]);
+          st_c(c_val + o, gv[p]);
         }
       } else {
         int NB = 32;

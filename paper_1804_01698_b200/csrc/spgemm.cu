@@ -42,7 +42,7 @@ struct spg_ctx {
   void *user = nullptr;
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
-  Buf parts, parts2, part_hist, toff, pkeys;  // (+ tile records of the narrow hash parts)
+  Buf parts, parts2, part_hist, toff, pkeys, dpfx;  // (+ tile records of the narrow hash parts)
   size_t pkeys_want = 0;  // column-tile parts of long rows (BM tier), sorted copy, B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
@@ -358,7 +358,7 @@ spg_status spg_ctx_create(spg_ctx **out, spg_alloc_fn alloc, spg_free_fn free_fn
          set_smem(c, k_sym_block<128>, size_t(4096) * 4) == SPG_OK &&
          set_smem(c, k_sym_block<256>, size_t(8192) * 4) == SPG_OK &&
          set_smem(c, k_sym_block<1024>, size_t(32768) * 4) == SPG_OK &&
-         set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
+         set_smem(c, k_sym_bitmap<1024>, size_t(kBitmapMaxCols / 8) + kBmStageBytes) == SPG_OK &&
          set_smem(c, k_num_tpart<512>, kTPartSmem) == SPG_OK &&
          set_smem(c, k_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
          set_smem(c, k_csr_mask_sum_block<1024>, size_t(kBitmapMaxCols / 8)) == SPG_OK &&
@@ -615,6 +615,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       const int64_t ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       parts_cap = std::min<int64_t>(parts_cap, (int64_t)h.sym_count[SB_BM] * ntiles + 16);
       if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * 3 * sizeof(int4), s)) != SPG_OK) return st;
+      if ((st = buf_ensure(c, c->dpfx, size_t(parts_cap) * kDenseStripes * 2, s)) != SPG_OK) return st;
       parts = (int4 *)c->parts.p;
       c->plan_parts = true;
     }
@@ -679,9 +680,10 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
         const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
-          k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4, ss>>>(
+          k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4 + kBmStageBytes, ss>>>(
               rb, n, a, b, flop, row_nnz, info, parts, parts_cap,
-              c->pkeys.p ? (uint32_t *)c->pkeys.p : nullptr, int64_t(c->pkeys.bytes / 4));
+              c->pkeys.p ? (uint32_t *)c->pkeys.p : nullptr, int64_t(c->pkeys.bytes / 4),
+              parts ? (uint16_t *)c->dpfx.p : nullptr);
         }
         SPG_LAUNCHED(c, "k_sym_bitmap");
       } else {  // SB_G
@@ -907,7 +909,8 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
         k_num_tpart<512><<<(unsigned)(2 * c->num_sms), 512, kTPartSmem, ss>>>(
             a, b, C_row_ptr, C_col_idx, C_val, sorted, (const int4 *)c->parts2.p,
             (int64_t)h.parts_used, (const int32_t *)c->toff.p, B->nrows, &dinfo->row_counter,
-            c->tune, dinfo->dbg, (c->tune & 256) ? nullptr : (const uint32_t *)c->pkeys.p);
+            c->tune, dinfo->dbg, (c->tune & 256) ? nullptr : (const uint32_t *)c->pkeys.p,
+            (c->tune & 1024) ? nullptr : (const uint16_t *)c->dpfx.p);
       }
       SPG_LAUNCHED(c, "k_num_tpart");
     } else {  // NB_G

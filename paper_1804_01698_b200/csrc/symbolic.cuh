@@ -50,7 +50,8 @@ __device__ __forceinline__ uint32_t tbm_bit(uint32_t c) { return 1u << ((c >> 8)
 // Tile records of the narrow hash parts (k_sym_bitmap -> k_num_tpart): 256
 // bitmap words + 256 u16 ranks per 8192-column tile.
 constexpr int kTileRec = 256 + 128;
-constexpr int kPbitsMaxSpan = 16;  // tiles (the record set must fit the numeric's smem region)
+constexpr int kPbitsMaxSpan = 16;
+constexpr int kDenseStripes = 16;  // 512-column stripes of a dense tile (one per numeric warp)  // tiles (the record set must fit the numeric's smem region)
 
 // Which parts get tile records: the narrow multi-tile (hash) parts; with
 // SPG_DENSE_RECORDS also the single-tile (dense) ones (A/B, DESIGN.md §9b:
@@ -532,6 +533,105 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
   }
 }
 
+// Bitmap-tier product walk: the row's a_ik are staged kBmEnt at a time
+// (entries with an empty B row dropped; es = B row start, epre = products
+// before the entry, < 2^31: the chunk's B rows are distinct), and the chunk's products are cut into FLATTENED rounds of
+// 32 consecutive products (setting a bit twice is harmless, so B-row
+// boundaries do not matter and every lane is busy).  Warp w takes a
+// contiguous range of rounds; the owner entry of each lane's product comes
+// from a window of the next 32 entry starts; kBmD rounds are resolved, then
+// their kBmD column gathers issued together, then their bits set.
+constexpr int kBmEnt = 1024;  // entries staged per chunk (= block size)
+constexpr int kBmD = 4;       // rounds in flight per warp
+constexpr size_t kBmStageBytes = size_t(kBmEnt) * 12 + 16;
+
+template <int THREADS>
+__device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, int64_t as,
+                                            int64_t ae, uint32_t *bm, int64_t *es,
+                                            int32_t *epre, int *s_w) {
+  static_assert(THREADS == kBmEnt, "one staged entry per thread");
+  constexpr int NW = THREADS / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned le = lane == 31 ? kFull : ((2u << lane) - 1u);  // lanes <= this one
+  for (int64_t cb = as; cb < ae; cb += kBmEnt) {
+    // stage: thread t holds entry cb + t
+    const int64_t e = cb + threadIdx.x;
+    int len = 0;
+    int64_t bs = 0;
+    if (e < ae) {
+      const int k = __ldg(A.col + e);
+      const int64_t b0 = __ldg(B.rp + k);
+      len = (int)(__ldg(B.rp + k + 1) - b0);
+      bs = b0;
+    }
+    // block exclusive scans of (nonempty, len), sharing their barriers
+    const unsigned bal = __ballot_sync(kFull, len > 0);
+    const int ipre = warp_incl_scan(len);
+    if (lane == 31) {
+      s_w[w] = __popc(bal);
+      s_w[33 + w] = ipre;
+    }
+    __syncthreads();  // (also: the previous chunk's rounds are done with es / epre)
+    if (w == 0) {
+      const int xc = lane < NW ? s_w[lane] : 0, xp = lane < NW ? s_w[33 + lane] : 0;
+      const int ic = warp_incl_scan(xc), ip = warp_incl_scan(xp);
+      if (lane < NW) {
+        s_w[lane] = ic - xc;
+        s_w[33 + lane] = ip - xp;
+      }
+      if (lane == 31) {
+        s_w[32] = ic;
+        s_w[65] = ip;
+      }
+    }
+    __syncthreads();
+    if (len > 0) {
+      const int x = s_w[w] + __popc(bal & ((1u << lane) - 1u));
+      es[x] = bs;
+      epre[x] = s_w[33 + w] + ipre - len;
+    }
+    const int n = s_w[32], P = s_w[65];
+    __syncthreads();
+    const int R = (P + 31) >> 5;
+    const int g0 = (int)((int64_t)R * w / NW), g1 = (int)((int64_t)R * (w + 1) / NW);
+    if (g0 < g1) {
+      // owner of round g0's first product: last j with epre[j] <= 32 g0
+      int cur;
+      {
+        const int x = g0 * 32;
+        const int c1 = lane * 32;
+        const unsigned b1 = __ballot_sync(kFull, c1 < n && epre[c1] <= x);
+        const int blk = 31 - __clz(b1);
+        const int c2 = blk * 32 + lane;
+        const unsigned b2 = __ballot_sync(kFull, c2 < n && epre[c2] <= x);
+        cur = blk * 32 + 31 - __clz(b2);
+      }
+      for (int g = g0; g < g1; g += kBmD) {
+        int64_t q[kBmD];
+        bool act[kBmD];
+#pragma unroll
+        for (int d = 0; d < kBmD; ++d) {
+          const int x0 = (g + d) * 32, x = x0 + lane;
+          act[d] = (g + d < g1) && x < P;
+          const int ej = cur + 1 + lane;
+          const int st = ej < n ? epre[ej] : INT32_MAX;  // start of entry cur + 1 + lane (> x0)
+          const unsigned pos = __reduce_or_sync(kFull, st < x0 + 32 ? (1u << (st - x0)) : 0u);
+          const int j = cur + __popc(pos & le);
+          cur += __popc(__ballot_sync(kFull, st <= x0 + 32));  // owner of the next round's first product
+          q[d] = act[d] ? es[j] + (x - epre[j]) : 0;
+        }
+        uint32_t c[kBmD];
+#pragma unroll
+        for (int d = 0; d < kBmD; ++d) c[d] = act[d] ? (uint32_t)__ldg(B.col + q[d]) : 0u;
+#pragma unroll
+        for (int d = 0; d < kBmD; ++d)
+          if (act[d]) atomicOr(bm + (c[d] >> 5), 1u << (c[d] & 31u));  // insert key
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // BM tier (bitmap, ncols <= kBitmapMaxCols): the set of distinct columns of
 // c_i* is exactly the set bits of an ncols-bit smem bitmap.  When B rows are
@@ -553,10 +653,12 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         PlanInfo *info, int4 *__restrict__ parts,
                                                         int64_t parts_cap,
                                                         uint32_t *__restrict__ pbits,
-                                                        int64_t pbits_cap) {
+                                                        int64_t pbits_cap,
+                                                        uint16_t *__restrict__ dpfx) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
-  __shared__ DeferList s_dl;  // long B rows walked by the whole block
+  __shared__ int s_w[66];
+  __shared__ int s_dpart[kMaxTiles];  // part index of a dense (single-tile, no record) part at the tile, or -1
   __shared__ long long s_pbase;
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
@@ -570,6 +672,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   const int nwords = (int)(((B.ncols + kTileCols - 1) >> kTileLog) << (kTileLog - 5));
   const int ntiles = (int)((B.ncols + kTileCols - 1) >> kTileLog);
   uint32_t *bm = s_dyn_u32;
+  int64_t *bm_es = reinterpret_cast<int64_t *>(s_dyn_u32 + nwords);  // staged entries (bm_walk_row)
+  int32_t *bm_epre = reinterpret_cast<int32_t *>(bm_es + kBmEnt);
   const bool want_parts = parts != nullptr && info->b_unsorted == 0;
   for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;  // (the count pass re-clears)
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
@@ -577,14 +681,9 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
-    // set the bit of every product's column (the old value is not used: no
-    // dependency on the atomic's return), then count the set bits once
-    auto ins = [&](bool act, uint32_t c, double) {
-      if (act) atomicOr(bm + (c >> 5), 1u << (c & 31u));
-    };
-    if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
-    else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
-    __syncthreads();
+    // set the bit of every product's column (flattened rounds), then count
+    // the set bits once
+    bm_walk_row<THREADS>(A, B, as, ae, bm, bm_es, bm_epre, s_w);
     // keys per column tile (a warp per tile); then the exclusive scan over
     // the tiles = keys before each tile, and the row's count
     for (int t = w; t < ntiles; t += NW) {
@@ -593,7 +692,10 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       for (int q = q0 + lane; q < q1; q += 32) c += __popc(bm[q]);
       c = (int)__reduce_add_sync(kFull, (unsigned)c);
       if (lane == 0) s_tcnt[t] = c;
-      if (lane == 0) s_tkoff[t] = -1;
+      if (lane == 0) {
+        s_tkoff[t] = -1;
+        s_dpart[t] = -1;
+      }
     }
     __syncthreads();
     if (w == 0) {
@@ -665,6 +767,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
           long long ro = rbase;
           for (int p = 0; p < np; ++p) {
             const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
+            if (t1 == t0 + 1 && !rec_part(t0, t1) && dpfx != nullptr) s_dpart[t0] = (int)(base + p);
             if (rec_part(t0, t1) && rbase >= 0) {
               for (int t = t0; t < t1; ++t) {
                 s_tkoff[t] = ro + (t - t0);
@@ -686,7 +789,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
             make_int4((int)(unsigned)(unsigned long long)as, (int)(unsigned)((unsigned long long)as >> 32),
                       (int)(ae - as), 0);
         parts[3 * (s_pbase + p) + 2] =
-            make_int4((int)(unsigned)(unsigned long long)koff, (int)(unsigned)((unsigned long long)koff >> 32), 0, 0);
+            make_int4((int)(unsigned)(unsigned long long)koff, (int)(unsigned)((unsigned long long)koff >> 32),
+                      t1 == t0 + 1 ? s_dpart[t0] : -1, 0);
       }
     }
     __syncthreads();
@@ -717,9 +821,21 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
           run += __popc(wv[u + 1]);
         }
         uint32_t *rp = pbits + rec * kTileRec;
-        reinterpret_cast<uint4 *>(rp)[2 * lane] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        reinterpret_cast<uint4 *>(rp)[2 * lane + 1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-        reinterpret_cast<uint4 *>(rp + 256)[lane] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+        // (evict-first: read once, by the numeric phase)
+        __stcs(reinterpret_cast<uint4 *>(rp) + 2 * lane, make_uint4(wv[0], wv[1], wv[2], wv[3]));
+        __stcs(reinterpret_cast<uint4 *>(rp) + 2 * lane + 1, make_uint4(wv[4], wv[5], wv[6], wv[7]));
+        __stcs(reinterpret_cast<uint4 *>(rp + 256) + lane, make_uint4(rk[0], rk[1], rk[2], rk[3]));
+      }
+      // dense single-tile part: keys of the tile before each 512-column
+      // stripe (the numeric's warp w emits stripe w: no count pass there)
+      const int dp = s_dpart[t];
+      if (dp >= 0) {
+        const int qa = q0 + 8 * lane;  // lane: half a stripe (8 words)
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c += __popc(bm[qa + u]);
+        const int ex = warp_incl_scan(c) - c;
+        if ((lane & 1) == 0) dpfx[int64_t(dp) * kDenseStripes + (lane >> 1)] = (uint16_t)ex;
       }
       for (int q = q0 + lane; q < q1; q += 32) bm[q] = 0u;
     }
