@@ -1228,8 +1228,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     };
     for (int cb = 0; cb < na; cb += kTEnt) {
       const int n = min(kTEnt, na - cb);
-      __syncthreads();  // table init / the previous chunk's rounds are done
-      // (the other parity's reservations were last read before this barrier)
+      // the previous chunk's rounds are done with the staged lists (the
+      // first chunk follows the publish barrier of the previous part: its
+      // emit is done, and the table init is ordered before the rounds by
+      // the staging barrier below); the other parity's reservations were
+      // last read before the barrier ending the previous chunk's staging
+      if (cb > 0) __syncthreads();
       if (threadIdx.x == 0) s_res[par ^ 1][0] = s_res[par ^ 1][1] = 0ull;
       const long long ca = instr ? clock64() : 0;
       // stage: thread owns entries [t*per, t*per + per), per <= 2; entries

@@ -542,6 +542,14 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 // from a window of the next 32 entry starts; kBmD rounds are resolved, then
 // their kBmD column gathers issued together, then their bits set.
 constexpr int kBmEnt = 1024;  // entries staged per chunk (= block size)
+// Bank spreading of the bitmap words: word q is stored at q with its low 5
+// bits (the bank) XOR-ed with a multiplicative hash of q >> 5 (a bijection
+// inside every 32-word group, so a tile's words stay in the tile's 256).
+// R-MAT columns with bits 5-9 clear (a quarter of them) all map to bank 0 of
+// their group otherwise.
+__device__ __forceinline__ uint32_t bm_phys(uint32_t q) {
+  return q ^ (((q >> 5) * 0x9E3779B1u) >> 27);
+}
 constexpr int kBmD = 4;       // rounds in flight per warp
 constexpr size_t kBmStageBytes = size_t(kBmEnt) * 12 + 16;
 
@@ -625,7 +633,7 @@ __device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, in
         for (int d = 0; d < kBmD; ++d) c[d] = act[d] ? (uint32_t)__ldg(B.col + q[d]) : 0u;
 #pragma unroll
         for (int d = 0; d < kBmD; ++d)
-          if (act[d]) atomicOr(bm + (c[d] >> 5), 1u << (c[d] & 31u));  // insert key
+          if (act[d]) atomicOr(bm + bm_phys(c[d] >> 5), 1u << (c[d] & 31u));  // insert key
       }
     }
   }
@@ -807,7 +815,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
         int c = 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          wv[u] = bm[qa + u];
+          wv[u] = bm[bm_phys(qa + u)];
           c += __popc(wv[u]);
         }
         const int incl = warp_incl_scan(c);
@@ -833,7 +841,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
         const int qa = q0 + 8 * lane;  // lane: half a stripe (8 words)
         int c = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c += __popc(bm[qa + u]);
+        for (int u = 0; u < 8; ++u) c += __popc(bm[bm_phys(qa + u)]);
         const int ex = warp_incl_scan(c) - c;
         if ((lane & 1) == 0) dpfx[int64_t(dp) * kDenseStripes + (lane >> 1)] = (uint16_t)ex;
       }
