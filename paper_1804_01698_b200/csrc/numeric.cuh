@@ -587,20 +587,38 @@ __device__ __forceinline__ void block_bucket_sort_to(const uint32_t *keys, const
     ex += v;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
-    const uint32_t k = keys[e];
-    grp[cnt[(k - mn) >> sh] + loc[e]] = k;
+  // scatter into bucket order: grp[pos] = key, loc[pos] = its entry (the
+  // positions are computed before loc is overwritten: <= kSortPer entries
+  // per thread)
+  constexpr int kSortPer = 16;
+  int pos[kSortPer];
+#pragma unroll
+  for (int u = 0; u < kSortPer; ++u) {
+    const int e = (int)threadIdx.x + u * (int)blockDim.x;
+    pos[u] = e < nnz ? (int)cnt[(keys[e] - mn) >> sh] + (int)loc[e] : -1;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
-    const uint32_t k = keys[e];
+#pragma unroll
+  for (int u = 0; u < kSortPer; ++u) {
+    const int e = (int)threadIdx.x + u * (int)blockDim.x;
+    if (pos[u] >= 0) {
+      grp[pos[u]] = keys[e];
+      loc[pos[u]] = (uint32_t)e;
+    }
+  }
+  __syncthreads();
+  // rank inside the bucket, walking the keys in bucket order (the lanes of a
+  // warp sit in the same or neighbouring buckets: no lane waits on a lane of
+  // a far larger bucket)
+  for (int p = threadIdx.x; p < nnz; p += blockDim.x) {
+    const uint32_t k = grp[p];
     const uint32_t b = (k - mn) >> sh;
     const int lo = (int)cnt[b];
     const int hi = (int)b + 1 < NB ? (int)cnt[b + 1] : nnz;
     int rnk = 0;
     for (int q = lo; q < hi; ++q) rnk += grp[q] < k;
     c_col[out + lo + rnk] = (int32_t)k;
-    c_val[out + lo + rnk] = vals[e];
+    c_val[out + lo + rnk] = vals[loc[p]];
   }
 }
 
@@ -852,11 +870,12 @@ constexpr int kTPartLogT = 12;
 constexpr int kTPartT = 1 << kTPartLogT;      // hash slots of a multi-tile part
 static_assert(4 * kTPartKeys <= 3 * kTPartT, "multi-tile part: load <= 3/4");
 constexpr int64_t kTRankCols = int64_t(32) * kTileCols;  // sorted emit by bitmap rank up to this span
-constexpr size_t kTDenseBytes = size_t(kTileCols) * 8 + size_t(kTileCols) / 8;
+constexpr size_t kTDenseBytes = size_t(kTileCols) * 8;  // (presence: -0.0 slots)
 constexpr size_t kTHashBytes = size_t(kTPartT) * 12 + size_t(kTPartKeys) * 2;
 constexpr size_t kTRecDenseBytes = size_t(kTileRec) * 4 + size_t(kTileCols) * 8;  // record + values
 constexpr size_t kTUnion0 = kTDenseBytes > kTHashBytes ? kTDenseBytes : kTHashBytes;
-constexpr size_t kTUnion = kTUnion0 > kTRecDenseBytes ? kTUnion0 : kTRecDenseBytes;
+constexpr size_t kTUnion =
+    (SPG_DENSE_RECORDS && kTRecDenseBytes > kTUnion0) ? kTRecDenseBytes : kTUnion0;
 // entry stage (byte offsets): short list es i32 / ea f64 / epre i32[+1];
 // long list ls i32 / ll i32 (length) / la f64 / lpre i32[+1] (round prefix)
 constexpr size_t kOffEa = 0;
@@ -871,9 +890,16 @@ static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
 static_assert(size_t(kPbitsMaxSpan) * kTileRec * 4 + size_t(kTPartKeys) * 8 <= kTUnion,
               "tile records + rank-indexed values in the table region");
-static_assert(size_t(kTileRec) * 4 + size_t(kTileCols) * 8 <= kTUnion,
+static_assert(!SPG_DENSE_RECORDS || size_t(kTileRec) * 4 + size_t(kTileCols) * 8 <= kTUnion,
               "one tile record + a dense part's rank-indexed values");
-constexpr size_t kTPartSmem = kTUnion + kTEntBytes;
+// Next-part prefetch (cp.async, issued while this part runs): the first
+// kTPf entries of the next part -- A.col, A.val, then the two tile offsets of
+// every such entry -- so a part's first staging chunk waits on no global load.
+constexpr int kTPf = 512;
+constexpr size_t kOffPfCol = 0, kOffPfVal = size_t(kTPf) * 4, kOffPfS0 = kOffPfVal + size_t(kTPf) * 8,
+                 kOffPfE0 = kOffPfS0 + size_t(kTPf) * 4;
+constexpr size_t kTPfBytes = kOffPfE0 + size_t(kTPf) * 4;
+constexpr size_t kTPartSmem = kTUnion + kTEntBytes + kTPfBytes;
 static_assert(kTEnt <= 32 * 32, "32-ary owner search");
 
 // Asynchronous global -> shared copies (cp.async; Ampere+ LDGSTS, no
@@ -884,6 +910,10 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
                "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -1102,6 +1132,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   // part's records are loaded while this part runs; published at its end
   __shared__ long long s_q;
   __shared__ int4 s_P, s_P1, s_P2, s_Pn[3];
+  __shared__ int s_pn_ok;  // the next part exists (its records are in s_Pn once thread 0 waited)
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char *base = reinterpret_cast<char *>(s_dyn_f64);
@@ -1117,6 +1148,13 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   int32_t *ll = reinterpret_cast<int32_t *>(eb + kOffLl);
   int32_t *epre = reinterpret_cast<int32_t *>(eb + kOffEpre);
   int32_t *lpre = reinterpret_cast<int32_t *>(eb + kOffLpre);
+  char *pfb = eb + kTEntBytes;  // next-part prefetch
+  int32_t *pf_col = reinterpret_cast<int32_t *>(pfb + kOffPfCol);
+  double *pf_val = reinterpret_cast<double *>(pfb + kOffPfVal);
+  int32_t *pf_s0 = reinterpret_cast<int32_t *>(pfb + kOffPfS0);
+  int32_t *pf_e0 = reinterpret_cast<int32_t *>(pfb + kOffPfE0);
+  static_assert(kTPf <= THREADS, "one prefetched entry per thread");
+  int pf_n = 0;  // entries of the current part prefetched (block-uniform)
   // the dense window starts clean (every slot -0.0: absent); every dense part
   // resets what it used
   unsigned long long *dvb = reinterpret_cast<unsigned long long *>(dv);
@@ -1152,6 +1190,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         cp_async16(&s_dp[0], dpfx + int64_t(P2.z) * kDenseStripes);
         cp_async16(&s_dp[8], dpfx + int64_t(P2.z) * kDenseStripes + 8);
       }
+      s_pn_ok = q_next < nparts;
       if (q_next < nparts) {
         cp_async16(&s_Pn[0], parts + 3 * q_next);
         cp_async16(&s_Pn[1], parts + 3 * q_next + 1);
@@ -1242,21 +1281,28 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       // products/rounds) atomic per list, so within a list the products /
       // rounds prefix increases with the slot (round owner searches)
       constexpr int kPer = (kTEnt + THREADS - 1) / THREADS;
-      const int per = (n + THREADS - 1) / THREADS;
-      const int jlo = min(n, (int)threadIdx.x * per), jhi = min(n, jlo + per);
       int Ls[kPer], s0s[kPer];
       double avs[kPer];
       unsigned long long vS = 0, vL = 0;  // (entries << 32) | products (short) / rounds (long)
+      if (cb == 0 && pf_n > 0) cp_async_wait_all();  // (this thread's own prefetch)
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int j = jlo + u;
+        const int j = (int)threadIdx.x + u * THREADS;  // (entries strided over the threads)
         Ls[u] = 0;
-        if (j < jhi) {
-          const int k = __ldg(A.col + as + cb + j);
-          const int s0 = __ldg(tk0 + k), e0 = __ldg(tk1 + k);
+        if (j < n) {
+          int s0, e0;
+          if (cb == 0 && j < pf_n) {  // prefetched while the previous part ran
+            s0 = pf_s0[j];
+            e0 = pf_e0[j];
+            avs[u] = pf_val[j];
+          } else {
+            const int k = __ldg(A.col + as + cb + j);
+            s0 = __ldg(tk0 + k);
+            e0 = __ldg(tk1 + k);
+            avs[u] = __ldg(A.val + as + cb + j);
+          }
           s0s[u] = s0;
           Ls[u] = e0 - s0;
-          avs[u] = __ldg(A.val + as + cb + j);
           if (Ls[u] >= kTLongSeg) vL += (1ull << 32) | (unsigned long long)((Ls[u] + 31) >> 5);
           else if (Ls[u] > 0) vS += (1ull << 32) | (unsigned long long)Ls[u];
         }
@@ -1299,7 +1345,22 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         for (int u = 0; u < kPer; ++u) lp += Ls[u] >= kTLongSeg ? (unsigned long long)Ls[u] : 0ull;
         if (lp) atomicAdd(dbg + (dense ? 12 : 13), lp);
       }
+      if (cb == 0 && threadIdx.x == 0) cp_async_wait_all();  // (the next part's records: s_Pn)
       __syncthreads();
+      if (cb == 0) {
+        // prefetch, stage 1: the next part's first kTPf entries (A.col, A.val)
+        pf_n = 0;
+        if (s_pn_ok) {
+          const int4 Qn1 = s_Pn[1];
+          const int64_t asn = (int64_t)(((unsigned long long)(unsigned)Qn1.y << 32) | (unsigned)Qn1.x);
+          pf_n = min(Qn1.z, kTPf);
+          if ((int)threadIdx.x < pf_n) {
+            cp_async4(pf_col + threadIdx.x, A.col + asn + threadIdx.x);
+            cp_async8(pf_val + threadIdx.x, A.val + asn + threadIdx.x);
+            cp_async_commit();
+          }
+        }
+      }
       const unsigned long long tS = s_res[par][0], tL = s_res[par][1];
       par ^= 1;
       const int nS = (int)(tS >> 32), PS = (int)(tS & 0xFFFFFFFFu);
@@ -1330,10 +1391,18 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         prods += (unsigned long long)PS;
       }
     }
-    if (threadIdx.x == 0) cp_async_wait_all();
+    cp_async_wait_all();  // (thread 0: C row start, stripe prefixes; all: prefetch stage 1)
     __syncthreads();
     const long long ce = instr ? clock64() : 0;
     const int64_t out = s_rp0 + P.z;
+    if ((int)threadIdx.x < pf_n) {
+      // prefetch, stage 2: the two tile offsets of each prefetched entry
+      const int4 Qn = s_Pn[0];
+      const int k = pf_col[threadIdx.x];
+      cp_async4(pf_s0 + threadIdx.x, toff + int64_t(Qn.y & 0xFFFF) * nB + k);
+      cp_async4(pf_e0 + threadIdx.x, toff + int64_t(Qn.y >> 16) * nB + k);
+      cp_async_commit();
+    }
     if (tune & 48) {  // (measurement only: no emit; the dense window is still reset)
       if (dense && !known)
         for (int s2 = threadIdx.x; s2 < kTileCols; s2 += THREADS) dvb[s2] = kNegZeroBits;

@@ -575,9 +575,11 @@ __global__ void __launch_bounds__(256) k_parts_hist(const int4 *__restrict__ par
   __shared__ unsigned h[kPartBuckets];
   for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x) h[b] = 0u;
   __syncthreads();
-  const int64_t n = (int64_t)info->parts_used;
-  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&h[part_bucket(parts[3 * p])], 1u);
+  const int64_t n = (int64_t)info->parts_pool;  // (slots handed out; holes have row -1)
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
+    const int4 v = parts[3 * p];
+    if (v.x >= 0) atomicAdd(&h[part_bucket(v)], 1u);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x)
     if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -606,16 +608,20 @@ __global__ void __launch_bounds__(256) k_parts_scatter(const int4 *__restrict__ 
   __shared__ unsigned h[kPartBuckets];
   for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x) h[b] = 0u;
   __syncthreads();
-  const int64_t n = (int64_t)info->parts_used;
+  const int64_t n = (int64_t)info->parts_pool;  // (slots handed out; holes have row -1)
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride)
-    atomicAdd(&h[part_bucket(parts[3 * p])], 1u);
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride) {
+    const int4 v = parts[3 * p];
+    if (v.x >= 0) atomicAdd(&h[part_bucket(v)], 1u);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < kPartBuckets; b += blockDim.x)
     if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);  // this block's first slot in bucket b
   __syncthreads();
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += stride) {
-    const int4 v = parts[3 * p], v1 = parts[3 * p + 1], v2 = parts[3 * p + 2];
+    const int4 v = parts[3 * p];
+    if (v.x < 0) continue;
+    const int4 v1 = parts[3 * p + 1], v2 = parts[3 * p + 2];
     const unsigned d = atomicAdd(&h[part_bucket(v)], 1u);
     out[3 * (int64_t)d] = v;
     out[3 * (int64_t)d + 1] = v1;

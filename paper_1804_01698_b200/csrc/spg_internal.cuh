@@ -57,7 +57,9 @@ struct PlanInfo {
   unsigned long long mask_n[2];     // lengths of their row lists (warp tier, block tier)
   unsigned long long mask_isum;     // exact int64 sum of the warp partials (two's complement)
   unsigned long long mask_inexact;  // nonzero: some warp partial was not an integer below 2^53
-  unsigned long long pkeys_used;    // sorted key lists of the multi-tile parts (bump allocator)
+  unsigned long long pkeys_used;    // tile records wanted by the narrow hash parts (exact count)
+  unsigned long long parts_pool;    // parts slots handed out in per-block chunks (>= parts_used; holes have row -1)
+  unsigned long long pkeys_pool;    // tile records handed out in per-block chunks
   unsigned long long heap_count[kMaxBins];   // rows of each numeric bin taken by the heap tier
   unsigned long long heap_cursor[kMaxBins];  // (scatter cursors, from the back of the bin)
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)

@@ -614,6 +614,7 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       parts_cap = (int64_t)(2 * h.flop_total / kTPartKeys) + (int64_t)h.sym_count[SB_BM] + 16;
       const int64_t ntiles = (B->ncols + kTileCols - 1) / kTileCols;
       parts_cap = std::min<int64_t>(parts_cap, (int64_t)h.sym_count[SB_BM] * ntiles + 16);
+      parts_cap += int64_t(c->num_sms) * 2 * kPoolParts;  // (per-block pools: at most one partial chunk per block)
       if ((st = buf_ensure(c, c->parts, size_t(parts_cap) * 3 * sizeof(int4), s)) != SPG_OK) return st;
       if ((st = buf_ensure(c, c->dpfx, size_t(parts_cap) * kDenseStripes * 2, s)) != SPG_OK) return st;
       parts = (int4 *)c->parts.p;
@@ -732,7 +733,8 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   // whose parts point into the current buffer); these parts hash their keys
   if (c->plan.pkeys_used * kTileRec * 4 > c->pkeys.bytes && c->plan_parts)
     c->pkeys_want = std::max<size_t>(
-        c->pkeys_want, size_t(c->plan.pkeys_used + (c->plan.pkeys_used >> 4)) * kTileRec * 4);
+        c->pkeys_want, size_t(c->plan.pkeys_used + (c->plan.pkeys_used >> 4) +
+                              size_t(c->num_sms) * 2 * kPoolRecs) * kTileRec * 4);
   *nnz_C = (int64_t)c->plan.nnz_total;
   if (flop_total) *flop_total = (int64_t)c->plan.flop_total;
   c->have_plan = true;
@@ -805,7 +807,7 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       SPG_LAUNCHED(c, "k_tile_offsets");
       // parts in processing order (dense first, tile ascending)
       const unsigned pgrid = (unsigned)std::max<int64_t>(
-          1, std::min<int64_t>(ceil_div((int64_t)h.parts_used, 256), int64_t(c->num_sms) * 4));
+          1, std::min<int64_t>(ceil_div((int64_t)h.parts_pool, 256), int64_t(c->num_sms) * 4));
       {
         ProfScope _ps(c, s, "k_parts_hist");
         k_parts_hist<<<pgrid, 256, 0, s>>>((const int4 *)c->parts.p, dinfo, (unsigned *)c->part_hist.p);

@@ -51,7 +51,13 @@ __device__ __forceinline__ uint32_t tbm_bit(uint32_t c) { return 1u << ((c >> 8)
 // bitmap words + 256 u16 ranks per 8192-column tile.
 constexpr int kTileRec = 256 + 128;
 constexpr int kPbitsMaxSpan = 16;
-constexpr int kDenseStripes = 16;  // 512-column stripes of a dense tile (one per numeric warp)  // tiles (the record set must fit the numeric's smem region)
+constexpr int kDenseStripes = 16;
+// The bitmap symbolic hands out parts slots and tile records from per-block
+// pools refilled kPoolParts / kPoolRecs at a time (one global atomic per
+// refill instead of two round trips per row); unused part slots are marked
+// with row -1 and skipped by the parts bucket sort.
+constexpr int kPoolParts = 512;
+constexpr int kPoolRecs = 2048;  // 512-column stripes of a dense tile (one per numeric warp)  // tiles (the record set must fit the numeric's smem region)
 
 // Which parts get tile records: the narrow multi-tile (hash) parts; with
 // SPG_DENSE_RECORDS also the single-tile (dense) ones (A/B, DESIGN.md §9b:
@@ -533,14 +539,16 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
   }
 }
 
-// Bitmap-tier product walk: the row's a_ik are staged kBmEnt at a time
-// (entries with an empty B row dropped; es = B row start, epre = products
-// before the entry, < 2^31: the chunk's B rows are distinct), and the chunk's products are cut into FLATTENED rounds of
-// 32 consecutive products (setting a bit twice is harmless, so B-row
-// boundaries do not matter and every lane is busy).  Warp w takes a
-// contiguous range of rounds; the owner entry of each lane's product comes
-// from a window of the next 32 entry starts; kBmD rounds are resolved, then
-// their kBmD column gathers issued together, then their bits set.
+// Bitmap-tier product walk: the row's a_ik are staged kBmEnt at a time into
+// two lists (entries with an empty B row dropped): LONG entries (B row of
+// >= 32 entries) at the front of the stage, walked entry by entry in rounds
+// of 32 consecutive columns of one B row (two rounds per step, no owner
+// search); SHORT ones at the back, cut into FLATTENED rounds of 32
+// consecutive products whatever the B-row boundaries (setting a bit twice is
+// harmless), the owner entry of each lane's product found from a window of
+// the next 32 entry starts.  Each list's rounds are split evenly over the
+// warps.  Stage entry: {B row start (int64), length, rounds / products
+// before it}.
 constexpr int kBmEnt = 1024;  // entries staged per chunk (= block size)
 // Bank spreading of the bitmap words: word q is stored at q with its low 5
 // bits (the bank) XOR-ed with a multiplicative hash of q >> 5 (a bijection
@@ -550,17 +558,34 @@ constexpr int kBmEnt = 1024;  // entries staged per chunk (= block size)
 __device__ __forceinline__ uint32_t bm_phys(uint32_t q) {
   return q ^ (((q >> 5) * 0x9E3779B1u) >> 27);
 }
-constexpr int kBmD = 4;       // rounds in flight per warp
-constexpr size_t kBmStageBytes = size_t(kBmEnt) * 12 + 16;
+constexpr int kBmD = 4;        // short rounds resolved per batch
+constexpr int kBmLong = 32;    // B rows of >= kBmLong entries walk sequentially
+constexpr size_t kBmStageBytes = size_t(kBmEnt) * 16 + 16;
+
+__device__ __forceinline__ void bm_set(uint32_t *bm, uint32_t c) {
+  atomicOr(bm + bm_phys(c >> 5), 1u << (c & 31u));  // insert key
+}
+
+// last j < n with pre[j] <= x (pre[0] = 0 <= x, nondecreasing, n <= 1024)
+__device__ __forceinline__ int bm_find(const int32_t *pre, int n, int x) {
+  const int lane = lane_id();
+  const int c1 = lane * 32;
+  const unsigned b1 = __ballot_sync(kFull, c1 < n && pre[c1] <= x);
+  const int blk = 31 - __clz(b1);
+  const int c2 = blk * 32 + lane;
+  const unsigned b2 = __ballot_sync(kFull, c2 < n && pre[c2] <= x);
+  return blk * 32 + 31 - __clz(b2);
+}
 
 template <int THREADS>
 __device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, int64_t as,
-                                            int64_t ae, uint32_t *bm, int64_t *es,
-                                            int32_t *epre, int *s_w) {
+                                            int64_t ae, uint32_t *bm, int64_t *st_bs,
+                                            int32_t *st_len, int32_t *st_pre, int *s_w) {
   static_assert(THREADS == kBmEnt, "one staged entry per thread");
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned le = lane == 31 ? kFull : ((2u << lane) - 1u);  // lanes <= this one
+  const unsigned lt = (1u << lane) - 1u;
   for (int64_t cb = as; cb < ae; cb += kBmEnt) {
     // stage: thread t holds entry cb + t
     const int64_t e = cb + threadIdx.x;
@@ -572,57 +597,79 @@ __device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, in
       len = (int)(__ldg(B.rp + k + 1) - b0);
       bs = b0;
     }
-    // block exclusive scans of (nonempty, len), sharing their barriers
-    const unsigned bal = __ballot_sync(kFull, len > 0);
-    const int ipre = warp_incl_scan(len);
+    const bool lg = len >= kBmLong, sh = len > 0 && !lg;
+    const int rl = lg ? (len + 31) >> 5 : 0, ps = sh ? len : 0;
+    const unsigned bl = __ballot_sync(kFull, lg), bsh = __ballot_sync(kFull, sh);
+    const int irl = warp_incl_scan(rl), ips = warp_incl_scan(ps);
     if (lane == 31) {
-      s_w[w] = __popc(bal);
-      s_w[33 + w] = ipre;
+      s_w[w] = __popc(bl);
+      s_w[32 + w] = irl;
+      s_w[64 + w] = __popc(bsh);
+      s_w[96 + w] = ips;
     }
-    __syncthreads();  // (also: the previous chunk's rounds are done with es / epre)
-    if (w == 0) {
-      const int xc = lane < NW ? s_w[lane] : 0, xp = lane < NW ? s_w[33 + lane] : 0;
-      const int ic = warp_incl_scan(xc), ip = warp_incl_scan(xp);
-      if (lane < NW) {
-        s_w[lane] = ic - xc;
-        s_w[33 + lane] = ip - xp;
-      }
-      if (lane == 31) {
-        s_w[32] = ic;
-        s_w[65] = ip;
-      }
+    __syncthreads();  // (also: the previous chunk's rounds are done with the stage)
+    if (w < 4) {  // four block scans, one per warp
+      const int x = lane < NW ? s_w[32 * w + lane] : 0;
+      const int xi = warp_incl_scan(x);
+      if (lane < NW) s_w[32 * w + lane] = xi - x;
+      if (lane == 31) s_w[128 + w] = xi;
     }
     __syncthreads();
-    if (len > 0) {
-      const int x = s_w[w] + __popc(bal & ((1u << lane) - 1u));
-      es[x] = bs;
-      epre[x] = s_w[33 + w] + ipre - len;
+    const int nL = s_w[128], RL = s_w[129], nS = s_w[130], PS = s_w[131];
+    if (lg) {
+      const int x = s_w[w] + __popc(bl & lt);
+      st_bs[x] = bs;
+      st_len[x] = len;
+      st_pre[x] = s_w[32 + w] + irl - rl;
+    } else if (sh) {
+      const int x = kBmEnt - nS + s_w[64 + w] + __popc(bsh & lt);
+      st_bs[x] = bs;
+      st_pre[x] = s_w[96 + w] + ips - ps;
     }
-    const int n = s_w[32], P = s_w[65];
     __syncthreads();
-    const int R = (P + 31) >> 5;
+    // long entries: rounds [RL w / NW, RL (w + 1) / NW), entry by entry
+    {
+      const int g0 = (int)((int64_t)RL * w / NW), g1 = (int)((int64_t)RL * (w + 1) / NW);
+      if (g0 < g1) {
+        int j = bm_find(st_pre, nL, g0);
+        int g = g0;
+        while (g < g1) {
+          const int rb = st_pre[j];
+          const int re = min(g1, j + 1 < nL ? st_pre[j + 1] : RL);
+          const int L = st_len[j];
+          const int32_t *pc = B.col + st_bs[j];
+          int t = (g - rb) * 32 + lane;
+          for (; g + 1 < re; g += 2, t += 64) {
+            const bool a0 = t < L, a1 = t + 32 < L;
+            const uint32_t c0 = a0 ? (uint32_t)__ldg(pc + t) : 0u;
+            const uint32_t c1 = a1 ? (uint32_t)__ldg(pc + t + 32) : 0u;
+            if (a0) bm_set(bm, c0);
+            if (a1) bm_set(bm, c1);
+          }
+          if (g < re) {
+            if (t < L) bm_set(bm, (uint32_t)__ldg(pc + t));
+            ++g;
+          }
+          ++j;
+        }
+      }
+    }
+    // short entries: flattened rounds [R w / NW, R (w + 1) / NW)
+    const int64_t *es = st_bs + (kBmEnt - nS);
+    const int32_t *epre = st_pre + (kBmEnt - nS);
+    const int R = (PS + 31) >> 5;
     const int g0 = (int)((int64_t)R * w / NW), g1 = (int)((int64_t)R * (w + 1) / NW);
     if (g0 < g1) {
-      // owner of round g0's first product: last j with epre[j] <= 32 g0
-      int cur;
-      {
-        const int x = g0 * 32;
-        const int c1 = lane * 32;
-        const unsigned b1 = __ballot_sync(kFull, c1 < n && epre[c1] <= x);
-        const int blk = 31 - __clz(b1);
-        const int c2 = blk * 32 + lane;
-        const unsigned b2 = __ballot_sync(kFull, c2 < n && epre[c2] <= x);
-        cur = blk * 32 + 31 - __clz(b2);
-      }
+      int cur = bm_find(epre, nS, g0 * 32);  // owner of round g0's first product
       for (int g = g0; g < g1; g += kBmD) {
         int64_t q[kBmD];
         bool act[kBmD];
 #pragma unroll
         for (int d = 0; d < kBmD; ++d) {
           const int x0 = (g + d) * 32, x = x0 + lane;
-          act[d] = (g + d < g1) && x < P;
+          act[d] = (g + d < g1) && x < PS;
           const int ej = cur + 1 + lane;
-          const int st = ej < n ? epre[ej] : INT32_MAX;  // start of entry cur + 1 + lane (> x0)
+          const int st = ej < nS ? epre[ej] : INT32_MAX;  // start of entry cur + 1 + lane (> x0)
           const unsigned pos = __reduce_or_sync(kFull, st < x0 + 32 ? (1u << (st - x0)) : 0u);
           const int j = cur + __popc(pos & le);
           cur += __popc(__ballot_sync(kFull, st <= x0 + 32));  // owner of the next round's first product
@@ -633,7 +680,7 @@ __device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, in
         for (int d = 0; d < kBmD; ++d) c[d] = act[d] ? (uint32_t)__ldg(B.col + q[d]) : 0u;
 #pragma unroll
         for (int d = 0; d < kBmD; ++d)
-          if (act[d]) atomicOr(bm + bm_phys(c[d] >> 5), 1u << (c[d] & 31u));  // insert key
+          if (act[d]) bm_set(bm, c[d]);
       }
     }
   }
@@ -665,9 +712,10 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         uint16_t *__restrict__ dpfx) {
   extern __shared__ uint32_t s_dyn_u32[];
   __shared__ int s_cnt, s_next;
-  __shared__ int s_w[66];
+  __shared__ int s_w[132];
   __shared__ int s_dpart[kMaxTiles];  // part index of a dense (single-tile, no record) part at the tile, or -1
   __shared__ long long s_pbase;
+  __shared__ long long s_pp_cur, s_pp_end, s_rp_cur, s_rp_end, s_hole_lo, s_hole_hi;
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
   __shared__ int s_cut[kMaxTiles];       // first | (end tile << 16) of each part
@@ -680,10 +728,12 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   const int nwords = (int)(((B.ncols + kTileCols - 1) >> kTileLog) << (kTileLog - 5));
   const int ntiles = (int)((B.ncols + kTileCols - 1) >> kTileLog);
   uint32_t *bm = s_dyn_u32;
-  int64_t *bm_es = reinterpret_cast<int64_t *>(s_dyn_u32 + nwords);  // staged entries (bm_walk_row)
-  int32_t *bm_epre = reinterpret_cast<int32_t *>(bm_es + kBmEnt);
+  int64_t *bm_bs = reinterpret_cast<int64_t *>(s_dyn_u32 + nwords);  // staged entries (bm_walk_row)
+  int32_t *bm_len = reinterpret_cast<int32_t *>(bm_bs + kBmEnt);
+  int32_t *bm_pre = bm_len + kBmEnt;
   const bool want_parts = parts != nullptr && info->b_unsorted == 0;
   for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;  // (the count pass re-clears)
+  if (threadIdx.x == 0) s_pp_cur = s_pp_end = s_rp_cur = s_rp_end = 0;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int i = rows[r];
     if (threadIdx.x == 0) s_next = 0;
@@ -691,7 +741,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     // set the bit of every product's column (flattened rounds), then count
     // the set bits once
-    bm_walk_row<THREADS>(A, B, as, ae, bm, bm_es, bm_epre, s_w);
+    bm_walk_row<THREADS>(A, B, as, ae, bm, bm_bs, bm_len, bm_pre, s_w);
     // keys per column tile (a warp per tile); then the exclusive scan over
     // the tiles = keys before each tile, and the row's count
     for (int t = w; t < ntiles; t += NW) {
@@ -759,18 +809,45 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
           s_cut[np++] = t | (s_nxt[t] << 16);
           if (rec_part(t, s_nxt[t])) htiles += s_nxt[t] - t;
         }
-        const long long base = (long long)atomicAdd(&info->parts_used, (unsigned long long)np);
+        // part slots from the block's pool (a refill leaves the rest of the
+        // old chunk as holes, marked below by the whole block)
+        s_hole_lo = s_hole_hi = 0;
+        long long base = s_pp_cur;
+        if (base + np > s_pp_end) {
+          s_hole_lo = s_pp_cur;
+          s_hole_hi = s_pp_end;
+          const long long chunk = np > kPoolParts ? np : kPoolParts;
+          base = (long long)atomicAdd(&info->parts_pool, (unsigned long long)chunk);
+          s_pp_end = base + chunk;
+          if (s_pp_end > parts_cap) s_pp_end = parts_cap;
+        }
         if (base + np > parts_cap) {
           atomicAdd(&info->parts_overflow, 1ull);
           s_cnt = -1;
+          s_pp_cur = s_pp_end;
         } else {
+          s_pp_cur = base + np;
           s_cnt = np;
-          // tile records of the hash parts (bump allocator, in records; past
-          // the capacity the parts keep -1 and the numeric hashes their keys)
+          atomicAdd(&info->parts_used, (unsigned long long)np);  // (exact count; result unused)
+          // tile records of the hash parts (block pool, in records; without
+          // room the parts keep -1 and the numeric hashes their keys)
           long long rbase = -1;
-          if (htiles > 0) {  // (counted even without a buffer: the host sizes it from the total)
-            rbase = (long long)atomicAdd(&info->pkeys_used, (unsigned long long)htiles);
-            if (pbits == nullptr || (rbase + htiles) * kTileRec > pbits_cap) rbase = -1;
+          if (htiles > 0) {
+            atomicAdd(&info->pkeys_used, (unsigned long long)htiles);  // (the host sizes the buffer from it)
+            if (pbits != nullptr) {
+              rbase = s_rp_cur;
+              if (rbase + htiles > s_rp_end) {
+                const long long chunk = htiles > kPoolRecs ? htiles : kPoolRecs;
+                rbase = (long long)atomicAdd(&info->pkeys_pool, (unsigned long long)chunk);
+                s_rp_end = rbase + chunk;
+              }
+              if ((rbase + htiles) * kTileRec > pbits_cap) {
+                rbase = -1;
+                s_rp_cur = s_rp_end;
+              } else {
+                s_rp_cur = rbase + htiles;
+              }
+            }
           }
           long long ro = rbase;
           for (int p = 0; p < np; ++p) {
@@ -789,6 +866,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       }
       __syncthreads();
       const int np = s_cnt;
+      for (long long h = s_hole_lo + threadIdx.x; h < s_hole_hi; h += THREADS)
+        parts[3 * h] = make_int4(-1, 0, 0, 0);  // (hole: skipped by the parts bucket sort)
       for (int p = threadIdx.x; p < np; p += THREADS) {
         const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
         const long long koff = s_tkoff[t0];
@@ -849,6 +928,9 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     }
     __syncthreads();
   }
+  // the rest of the block's last parts chunk: holes
+  if (parts != nullptr)
+    for (long long h = s_pp_cur + threadIdx.x; h < s_pp_end; h += THREADS) parts[3 * h] = make_int4(-1, 0, 0, 0);
 }
 
 // ---------------------------------------------------------------------------
