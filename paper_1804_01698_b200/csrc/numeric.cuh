@@ -1427,8 +1427,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         const unsigned m = __ballot_sync(kFull, pres);
         if (pres) {
           const int p = o + __popc(m & below);
-          st_c(cc + p, cbase + j * 32);
-          st_c(cvp + p, __longlong_as_double(bits));
+          if (!(tune & 8192)) {  // (measurement switch: 8192 skips the stores)
+            st_c(cc + p, cbase + j * 32);
+            st_c(cvp + p, __longlong_as_double(bits));
+          }
           dvb[ds] = kNegZeroBits;
         }
         o += __popc(m);
@@ -1478,7 +1480,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     } else if (known) {
       // values in rank order = column order (coalesced copy); columns by a
       // walk of the part's bitmap words (sparse: mostly one bit per word)
-      for (int r = threadIdx.x; r < cnt; r += THREADS) st_c(c_val + out + r, rv[r]);
+      if (!(tune & 4096))  // (measurement switch: 4096 skips the value stores)
+        for (int r = threadIdx.x; r < cnt; r += THREADS) st_c(c_val + out + r, rv[r]);
       const int nw = (t1 - t0) * 256;
       int32_t *ccol = c_col + out;
       const int32_t lo_i = (int32_t)lo;
@@ -1488,6 +1491,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         if (!wd) continue;
         int r = reinterpret_cast<const uint16_t *>(tr + 256)[q & 255];
         const int32_t cb = lo_i + (q << 5);
+        if (tune & 2048) continue;  // (measurement switch: 2048 skips the column stores)
         while (wd) {
           st_c(ccol + r++, (int32_t)(cb + __ffs(wd) - 1));
           wd &= wd - 1;
@@ -1568,7 +1572,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       atomicAdd(dbg + 6, (unsigned long long)c_stage);
       atomicAdd(dbg + 7, (unsigned long long)c_rounds);
       atomicAdd(dbg + (dense ? 8 : 11), (unsigned long long)(cz - ce));   // emit
-      atomicAdd(dbg + 9, (unsigned long long)na);
+      if (!dense && !known) atomicAdd(dbg + 9, (unsigned long long)(cz - ce));  // emit of the hashing parts
       atomicAdd(dbg + 10, (unsigned long long)cnt);
       if (!dense) atomicAdd(dbg + 14, (unsigned long long)(t1 - t0));  // hash part spans (tiles)
       if (known) atomicAdd(dbg + 15, 1ull);                            // parts indexed by tile records
