@@ -888,7 +888,7 @@ constexpr size_t kOffLpre = kOffEpre + size_t(kTEnt + 4) * 4;
 constexpr size_t kTEntBytes = kOffLpre + size_t(kTEnt + 4) * 4;
 static_assert(size_t(kTPartKeys) * 12 <= kTEntBytes, "sorted gather");
 static_assert(size_t(kTRankCols / 32) * 8 <= kTUnion, "rank bitmap + prefix in the table region");
-static_assert(size_t(kPbitsMaxSpan) * kTileRec * 4 + size_t(kTPartKeys) * 8 <= kTUnion,
+static_assert(size_t(kPbitsMaxSpan) * kTileRec * 4 + size_t(kTPartKeys) * 12 <= kTUnion,
               "tile records + rank-indexed values in the table region");
 static_assert(!SPG_DENSE_RECORDS || size_t(kTileRec) * 4 + size_t(kTileCols) * 8 <= kTUnion,
               "one tile record + a dense part's rank-indexed values");
@@ -1219,6 +1219,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
     const bool known = koff >= 0 && pbits != nullptr;
     uint32_t *rec = reinterpret_cast<uint32_t *>(base);                       // span x kTileRec words
     double *rv = reinterpret_cast<double *>(base + size_t(t1 - t0) * kTileRec * 4);  // [cnt]
+    int32_t *rcol = reinterpret_cast<int32_t *>(rv + kTPartKeys);  // [cnt]: column of each rank
     if (known) {
       const int nrec = (t1 - t0) * kTileRec;
       const uint4 *src = reinterpret_cast<const uint4 *>(pbits + koff * kTileRec);
@@ -1247,6 +1248,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         const int rank = (int)reinterpret_cast<const uint16_t *>(tr + 256)[q & 255u] +
                          __popc(wd & ((1u << (off & 31u)) - 1u));
         atomicAdd(rv + rank, v);  // c_ij <- c_ij + value (l.8)
+        rcol[rank] = (int32_t)c;  // (every product of the key stores the same column)
       }
     };
     auto acc_hash = [&](bool act, uint32_t c, double v) {
@@ -1427,7 +1429,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         const unsigned m = __ballot_sync(kFull, pres);
         if (pres) {
           const int p = o + __popc(m & below);
-          if (!(tune & 8192)) {  // (measurement switch: 8192 skips the stores)
+          if (tune & 16384) {  // (A/B: plain write-back stores)
+            cc[p] = cbase + j * 32;
+            cvp[p] = __longlong_as_double(bits);
+          } else if (!(tune & 8192)) {  // (measurement switch: 8192 skips the stores)
             st_c(cc + p, cbase + j * 32);
             st_c(cvp + p, __longlong_as_double(bits));
           }
@@ -1478,24 +1483,12 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         }
       }
     } else if (known) {
-      // values in rank order = column order (coalesced copy); columns by a
-      // walk of the part's bitmap words (sparse: mostly one bit per word)
-      if (!(tune & 4096))  // (measurement switch: 4096 skips the value stores)
-        for (int r = threadIdx.x; r < cnt; r += THREADS) st_c(c_val + out + r, rv[r]);
-      const int nw = (t1 - t0) * 256;
-      int32_t *ccol = c_col + out;
-      const int32_t lo_i = (int32_t)lo;
-      for (int q = threadIdx.x; q < nw; q += THREADS) {
-        const uint32_t *tr = rec + (q >> 8) * kTileRec;
-        uint32_t wd = tr[q & 255];
-        if (!wd) continue;
-        int r = reinterpret_cast<const uint16_t *>(tr + 256)[q & 255];
-        const int32_t cb = lo_i + (q << 5);
-        if (tune & 2048) continue;  // (measurement switch: 2048 skips the column stores)
-        while (wd) {
-          st_c(ccol + r++, (int32_t)(cb + __ffs(wd) - 1));
-          wd &= wd - 1;
-        }
+      // every key of the part received at least one product, which stored
+      // its column at the key's rank: columns and values (rank order = column
+      // order) go out as two coalesced copies, no bitmap walk
+      for (int r = threadIdx.x; r < cnt; r += THREADS) {
+        st_c(c_col + out + r, rcol[r]);
+        st_c(c_val + out + r, rv[r]);
       }
     } else if (!sorted) {
       for (int p = threadIdx.x; p < cnt; p += THREADS) {
@@ -1540,12 +1533,27 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
           exr += __popc(rbm[q2]);
         }
         __syncthreads();
+        // ranks first (u16 after the gathered pairs), then the pairs placed at
+        // their ranks in the table region (rbm / rpre are done), then two
+        // coalesced copies out
+        uint16_t *rk = reinterpret_cast<uint16_t *>(eb + size_t(kTPartKeys) * 12);
+        static_assert(size_t(kTPartKeys) * 14 <= kTEntBytes, "ranks after the gathered pairs");
         for (int p = threadIdx.x; p < cnt; p += THREADS) {
           const uint32_t off = gk[p] - (uint32_t)lo;
           const uint32_t wd = off >> 5;
-          const int64_t o = out + rpre[wd] + __popc(rbm[wd] & ((1u << (off & 31u)) - 1u));
-          st_c(c_col + o, (int32_t)gk[p]);
-          st_c(c_val + o, gv[p]);
+          rk[p] = (uint16_t)(rpre[wd] + __popc(rbm[wd] & ((1u << (off & 31u)) - 1u)));
+        }
+        __syncthreads();
+        int32_t *scol = reinterpret_cast<int32_t *>(base);
+        double *sval = reinterpret_cast<double *>(base + size_t(kTPartKeys) * 4);
+        for (int p = threadIdx.x; p < cnt; p += THREADS) {
+          scol[rk[p]] = (int32_t)gk[p];
+          sval[rk[p]] = gv[p];
+        }
+        __syncthreads();
+        for (int r = threadIdx.x; r < cnt; r += THREADS) {
+          st_c(c_col + out + r, scol[r]);
+          st_c(c_val + out + r, sval[r]);
         }
       } else {
         int NB = 32;

@@ -550,6 +550,10 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
 // warps.  Stage entry: {B row start (int64), length, rounds / products
 // before it}.
 constexpr int kBmEnt = 1024;  // entries staged per chunk (= block size)
+#ifndef SPG_SYM_INSTR
+#define SPG_SYM_INSTR 0
+#endif
+constexpr bool kSymInstr = SPG_SYM_INSTR != 0;
 // Bank spreading of the bitmap words: word q is stored at q with its low 5
 // bits (the bank) XOR-ed with a multiplicative hash of q >> 5 (a bijection
 // inside every 32-word group, so a tile's words stay in the tile's 256).
@@ -715,7 +719,8 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   __shared__ int s_w[132];
   __shared__ int s_dpart[kMaxTiles];  // part index of a dense (single-tile, no record) part at the tile, or -1
   __shared__ long long s_pbase;
-  __shared__ long long s_pp_cur, s_pp_end, s_rp_cur, s_rp_end, s_hole_lo, s_hole_hi;
+  __shared__ long long s_pp_cur, s_pp_end, s_rp_cur, s_rp_end, s_hole_lo, s_hole_hi, s_rbase;
+  __shared__ int s_prec[kMaxTiles];  // record tiles of the row's parts before each part
   __shared__ int s_tile[kMaxTiles + 1];  // keys of the row before each column tile
   __shared__ int s_tcnt[kMaxTiles];      // keys of the row in each column tile
   __shared__ int s_cut[kMaxTiles];       // first | (end tile << 16) of each part
@@ -739,9 +744,11 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
-    // set the bit of every product's column (flattened rounds), then count
+    const long long k0 = kSymInstr ? clock64() : 0;
+    // set the bit of every product's column (long / short lists), then count
     // the set bits once
     bm_walk_row<THREADS>(A, B, as, ae, bm, bm_bs, bm_len, bm_pre, s_w);
+    const long long k1 = kSymInstr ? clock64() : 0;
     // keys per column tile (a warp per tile); then the exclusive scan over
     // the tiles = keys before each tile, and the row's count
     for (int t = w; t < ntiles; t += NW) {
@@ -772,6 +779,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
     __syncthreads();
     const int nnz = s_cnt;
     if (threadIdx.x == 0) row_nnz[i] = nnz;
+    const long long k2 = kSymInstr ? clock64() : 0;
     if (want_parts && nnz > kPartMinKeys) {
       // parts: greedy runs of consecutive tiles holding <= kTPartKeys keys; a
       // tile holding more stands alone (dense window in the numeric phase).
@@ -806,6 +814,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
         int np = 0;
         long long htiles = 0;  // tiles of the row's parts spanning <= kPbitsMaxSpan tiles
         for (int t = s_nne[0]; t < ntiles; t = s_nne[s_nxt[t]]) {
+          s_prec[np] = (int)htiles;  // record tiles of the parts before this one
           s_cut[np++] = t | (s_nxt[t] << 16);
           if (rec_part(t, s_nxt[t])) htiles += s_nxt[t] - t;
         }
@@ -849,18 +858,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
               }
             }
           }
-          long long ro = rbase;
-          for (int p = 0; p < np; ++p) {
-            const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
-            if (t1 == t0 + 1 && !rec_part(t0, t1) && dpfx != nullptr) s_dpart[t0] = (int)(base + p);
-            if (rec_part(t0, t1) && rbase >= 0) {
-              for (int t = t0; t < t1; ++t) {
-                s_tkoff[t] = ro + (t - t0);
-                s_tkb[t] = s_tile[t] - s_tile[t0];
-              }
-              ro += t1 - t0;
-            }
-          }
+          s_rbase = rbase;
           s_pbase = base;
         }
       }
@@ -868,19 +866,30 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       const int np = s_cnt;
       for (long long h = s_hole_lo + threadIdx.x; h < s_hole_hi; h += THREADS)
         parts[3 * h] = make_int4(-1, 0, 0, 0);  // (hole: skipped by the parts bucket sort)
-      for (int p = threadIdx.x; p < np; p += THREADS) {
+      const long long rbase = s_rbase;
+      for (int p = threadIdx.x; p < np; p += THREADS) {  // (a thread per part)
         const int t0 = s_cut[p] & 0xFFFF, t1 = s_cut[p] >> 16;
-        const long long koff = s_tkoff[t0];
+        const bool dpt = t1 == t0 + 1 && !rec_part(t0, t1) && dpfx != nullptr;
+        if (dpt) s_dpart[t0] = (int)(s_pbase + p);
+        long long koff = -1;
+        if (rec_part(t0, t1) && rbase >= 0) {
+          koff = rbase + s_prec[p];
+          for (int t = t0; t < t1; ++t) {  // (<= kPbitsMaxSpan tiles)
+            s_tkoff[t] = koff + (t - t0);
+            s_tkb[t] = s_tile[t] - s_tile[t0];
+          }
+        }
         parts[3 * (s_pbase + p)] = make_int4(i, s_cut[p], s_tile[t0], s_tile[t1] - s_tile[t0]);
         parts[3 * (s_pbase + p) + 1] =
             make_int4((int)(unsigned)(unsigned long long)as, (int)(unsigned)((unsigned long long)as >> 32),
                       (int)(ae - as), 0);
         parts[3 * (s_pbase + p) + 2] =
             make_int4((int)(unsigned)(unsigned long long)koff, (int)(unsigned)((unsigned long long)koff >> 32),
-                      t1 == t0 + 1 ? s_dpart[t0] : -1, 0);
+                      dpt ? (int)(s_pbase + p) : -1, 0);
       }
     }
     __syncthreads();
+    const long long k3 = kSymInstr ? clock64() : 0;
     // tile records of the hash parts (a warp per tile: lane l stores words
     // 8 l .. 8 l + 7 and their ranks -- keys of the part before each word --
     // as two 16-byte stores, coalesced), and the clear of every word for the
@@ -927,6 +936,15 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       for (int q = q0 + lane; q < q1; q += 32) bm[q] = 0u;
     }
     __syncthreads();
+    if (kSymInstr && threadIdx.x == 0) {  // (phase clocks: SPG_SYM_INSTR builds)
+      const long long k4 = clock64();
+      atomicAdd(&info->dbg[0], 1ull);
+      atomicAdd(&info->dbg[1], (unsigned long long)(k1 - k0));  // walk (staging + rounds)
+      atomicAdd(&info->dbg[2], (unsigned long long)(k2 - k1));  // tile counts + scan
+      atomicAdd(&info->dbg[3], (unsigned long long)(k3 - k2));  // parts
+      atomicAdd(&info->dbg[4], (unsigned long long)(k4 - k3));  // records, stripes, clear
+      atomicAdd(&info->dbg[5], (unsigned long long)(ae - as));
+    }
   }
   // the rest of the block's last parts chunk: holes
   if (parts != nullptr)
