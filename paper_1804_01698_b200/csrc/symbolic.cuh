@@ -50,7 +50,10 @@ __device__ __forceinline__ uint32_t tbm_bit(uint32_t c) { return 1u << ((c >> 8)
 // Tile records of the narrow hash parts (k_sym_bitmap -> k_num_tpart): 256
 // bitmap words + 256 u16 ranks per 8192-column tile.
 constexpr int kTileRec = 256 + 128;
-constexpr int kPbitsMaxSpan = 16;
+#ifndef SPG_PBITS_SPAN
+#define SPG_PBITS_SPAN 16
+#endif
+constexpr int kPbitsMaxSpan = SPG_PBITS_SPAN;
 constexpr int kDenseStripes = 16;
 // The bitmap symbolic hands out parts slots and tile records from per-block
 // pools refilled kPoolParts / kPoolRecs at a time (one global atomic per
