@@ -640,13 +640,15 @@ __device__ __forceinline__ void block_bucket_sort_store(const uint32_t *keys, co
 // emit unordered into C, reload the row into smem, bucket-sort it into C (a7).
 // ---------------------------------------------------------------------------
 template <int THREADS, bool ONEP = false>
-__global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict__ rows,
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_num_block(const int32_t *__restrict__ rows,
                                                        int64_t nrows, DevCSR A, DevCSR B,
                                                        const int64_t *__restrict__ flop,
                                                        const int64_t *__restrict__ c_rp,
                                                        int32_t *__restrict__ c_col,
                                                        double *__restrict__ c_val, int sorted,
-                                                       int tmax, OnePhase op = OnePhase{}) {
+                                                       int tmax, OnePhase op = OnePhase{},
+                                                       const int64_t *__restrict__ list_off = nullptr,
+                                                       const int32_t *__restrict__ lists = nullptr) {
   extern __shared__ double s_dyn_f64[];
   __shared__ int s_cnt, s_next;
   __shared__ DeferList s_dl;  // long B rows walked by the whole block
@@ -666,21 +668,51 @@ __global__ void __launch_bounds__(THREADS) k_num_block(const int32_t *__restrict
     int nnz = ONEP ? 0 : (int)(c_rp[i + 1] - rp0);
     const int logT = ONEP ? onep_log2(flop[i], B.ncols) : num_log2(nnz);
     const int T = 1 << logT;
-    for (int s = threadIdx.x; s < T; s += THREADS) { keys[s] = kEmpty; vals[s] = 0.0; }
+    // rows with a sorted column list from the bitmap symbolic: a key -> rank
+    // table is built first (every key distinct: inserts do not collide on a
+    // key), each product adds into vals2[rank] after a read-only probe, and
+    // the emit copies the list and vals2 out (sorted, coalesced; no key CAS
+    // per product, no sort).  One walk serves both kinds of rows (a uniform
+    // branch in the accumulate: one instantiation of the walk, registers).
+    const long long lo_ = (!ONEP && list_off != nullptr) ? list_off[i] : -1;
+    const bool lrow = lo_ >= 0;
+    const int32_t *L = lists + (lrow ? lo_ : 0);
+    uint16_t *rank = reinterpret_cast<uint16_t *>(vals + (T >> 1));  // [T] (list rows)
+    for (int s = threadIdx.x; s < T; s += THREADS) keys[s] = kEmpty;
+    for (int s = threadIdx.x; s < (lrow ? nnz : T); s += THREADS) vals[s] = 0.0;
     if (threadIdx.x == 0) { s_cnt = 0; s_next = 0; }
+    if (lrow) {
+      __syncthreads();
+      for (int r = threadIdx.x; r < nnz; r += THREADS) {
+        bool isnew = false;
+        rank[probe_chunk(keys, (uint32_t)__ldg(L + r), logT, &isnew)] = (uint16_t)r;
+      }
+    }
     __syncthreads();
     {
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
+      auto slot_of = [&](uint32_t c) -> double * {
+        return lrow ? vals + rank[probe_find(keys, c, logT)]
+                    : vals + hash_vslot(num_probe_smem(keys, c, logT), logT);
+      };
       auto acc = [&](bool act, uint32_t c, double v) {  // c_ij <- c_ij + value (l.8)
-        if (act) atomicAdd(vals + hash_vslot(num_probe_smem(keys, c, logT), logT), v);
+        if (act) atomicAdd(slot_of(c), v);
       };
       auto acc_comb = [&](bool act, uint32_t c, double v) {  // keys may repeat in a round
-        if (warp_combine(act, c, v)) atomicAdd(vals + hash_vslot(num_probe_smem(keys, c, logT), logT), v);
+        if (warp_combine(act, c, v)) atomicAdd(slot_of(c), v);
       };
       if (use_seq(flop[i], ae - as)) for_row<true, true>(A, B, as, ae, w, NW, acc, &s_next, &s_dl);
       else for_row<false, true>(A, B, as, ae, w, NW, acc_comb, &s_next, &s_dl);
     }
     __syncthreads();
+    if (lrow) {
+      for (int r = threadIdx.x; r < nnz; r += THREADS) {
+        c_col[rp0 + r] = __ldg(L + r);
+        c_val[rp0 + r] = vals[r];
+      }
+      __syncthreads();
+      continue;
+    }
     block_emit_unsorted(keys, vals, T, rp0, c_col, c_val, &s_cnt, logT);
     if (ONEP) {  // nnz(c_i) = the emitted count
       __syncthreads();

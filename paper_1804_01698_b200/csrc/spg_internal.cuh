@@ -60,6 +60,8 @@ struct PlanInfo {
   unsigned long long pkeys_used;    // tile records wanted by the narrow hash parts (exact count)
   unsigned long long parts_pool;    // parts slots handed out in per-block chunks (>= parts_used; holes have row -1)
   unsigned long long pkeys_pool;    // tile records handed out in per-block chunks
+  unsigned long long lists_need;    // keys of the rows that want a sorted column list (exact count)
+  unsigned long long lists_pool;    // list entries handed out in per-block chunks
   unsigned long long heap_count[kMaxBins];   // rows of each numeric bin taken by the heap tier
   unsigned long long heap_cursor[kMaxBins];  // (scatter cursors, from the back of the bin)
   unsigned long long dbg[16];       // measurement counters (SPG_TUNE bit 8 instrumentation)
@@ -97,6 +99,9 @@ __device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {
 // column space fits one (it also cuts the row into column-range parts for the
 // numeric phase); otherwise the larger smem hash tables / global hash.
 constexpr int64_t kBitmapMaxCols = int64_t(200 * 1024) * 8;  // 200 KB of bits
+#ifndef SPG_MED_BM
+#define SPG_MED_BM 0
+#endif
 
 // Rows with more than kWarpMaxEntries a_ik go to a block tier even when their
 // table is small: one warp would walk all their a_ik alone.
@@ -108,7 +113,9 @@ __device__ __forceinline__ int sym_bin(int64_t flop, int64_t ncols, int64_t na) 
   if (na > kWarpMaxEntries && n <= 10) return SB_B2K;
   if (n <= 7) return SB_W128;
   if (n <= 10) return SB_W1024;
-  if (n <= 13) return SB_B2K + (n - 11);
+  // rows of 1024..8191 products: the bitmap tier when the column space fits
+  // (it hands the numeric block tier the row's sorted column list)
+  if (n <= 13 && (!SPG_MED_BM || ncols > kBitmapMaxCols)) return SB_B2K + (n - 11);
   if (ncols <= kBitmapMaxCols) return SB_BM;
   if (n <= 15) return SB_B2K + (n - 11);
   return SB_G;
@@ -239,6 +246,22 @@ __device__ __forceinline__ uint32_t probe_chunk(uint32_t *keys, uint32_t c, int 
       continue;  // lost the slot to another key: re-read this chunk
     }
     ch = (ch + 1u) & cmask;  // chunk full: next chunk (linear probing)
+  }
+}
+
+// Slot of key c, known to be in the (complete) table: chunked probing
+// without inserts.
+__device__ __forceinline__ uint32_t probe_find(const uint32_t *keys, uint32_t c, int logT) {
+  const uint32_t cmask = (1u << (logT - kChunkLog)) - 1u;
+  uint32_t ch = (c * kHashMul) >> (32 - (logT - kChunkLog));
+  while (true) {
+    const uint32_t b = ch << kChunkLog;
+    const uint4 k = *reinterpret_cast<const uint4 *>(keys + b);
+    if (k.x == c) return b;
+    if (k.y == c) return b + 1;
+    if (k.z == c) return b + 2;
+    if (k.w == c) return b + 3;
+    ch = (ch + 1u) & cmask;
   }
 }
 

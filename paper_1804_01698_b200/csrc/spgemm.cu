@@ -42,7 +42,10 @@ struct spg_ctx {
   void *user = nullptr;
   std::string err;
   Buf flop, rows_sym, rows_num, partial, slab, info, scratch;
-  Buf parts, parts2, part_hist, toff, pkeys, dpfx;  // (+ tile records of the narrow hash parts)
+  Buf parts, parts2, part_hist, toff, pkeys, dpfx;
+  Buf lists, list_off;    // sorted column lists of the block-tier rows (from the bitmap symbolic)
+  size_t lists_want = 0;  // (grown at the start of the next symbolic)
+  bool plan_lists = false;  // (+ tile records of the narrow hash parts)
   size_t pkeys_want = 0;  // column-tile parts of long rows (BM tier), sorted copy, B tile offsets
   Buf bnz, prune_cnt, prune_rp, prune_col, prune_val, prune_idx;  // B nonempty-row bitmap; pruned A
   Buf trow;                          // row of the first a_ik of every kFlopTile tile of A
@@ -488,6 +491,15 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
     cudaGetLastError();
     c->pkeys_want = 0;
   }
+  if (c->lists_want > c->lists.bytes) {  // (grown here only, like the tile records)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && c->lists_want <= total_b / 8 &&
+        c->lists_want + (size_t(8) << 30) < free_b + c->lists.bytes)
+      buf_ensure(c, c->lists, c->lists_want, s);
+    cudaGetLastError();
+    c->lists_want = 0;
+  }
+  c->plan_lists = false;
   PlanInfo *info = (PlanInfo *)c->info.p;
   SPG_CUDA(c, cudaMemsetAsync(info, 0, sizeof(PlanInfo), s));
   SPG_CUDA(c, cudaMemsetAsync(C_row_ptr, 0, sizeof(int64_t), s));
@@ -679,12 +691,30 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
       } else if (bin == SB_BM) {
         const size_t nwords = size_t(ceil_div(B->ncols, kTileCols)) * (kTileCols / 32);  // whole tiles (tbm_word)
         const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 2);
+        // sorted column lists for the rows the numeric block tier will take
+        // (first call: a guess from the bin's row count; then the need).
+        // Off by default (SPG_TUNE bit 65536 turns them on): measured on C3
+        // the block tier gains what the bitmap symbolic loses
+        if ((c->tune & 65536) && c->lists.bytes == 0) {
+          size_t free_b = 0, total_b = 0;
+          const size_t guess = size_t(n) * 2048 * 4;
+          if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && guess <= total_b / 8 &&
+              guess + (size_t(8) << 30) < free_b)
+            buf_ensure(c, c->lists, guess, ss);
+          cudaGetLastError();
+        }
+        if ((c->tune & 65536) && c->lists.bytes && buf_ensure(c, c->list_off, size_t(m) * 8, ss) == SPG_OK) {
+          SPG_CUDA(c, cudaMemsetAsync(c->list_off.p, 0xFF, size_t(m) * 8, ss));
+          c->plan_lists = true;
+        }
         {
           ProfScope _ps(c, ss, "k_sym_bitmap<1024>");
           k_sym_bitmap<1024><<<(unsigned)grid, 1024, nwords * 4 + kBmStageBytes, ss>>>(
               rb, n, a, b, flop, row_nnz, info, parts, parts_cap,
               c->pkeys.p ? (uint32_t *)c->pkeys.p : nullptr, int64_t(c->pkeys.bytes / 4),
-              parts ? (uint16_t *)c->dpfx.p : nullptr);
+              parts ? (uint16_t *)c->dpfx.p : nullptr,
+              c->plan_lists ? (int64_t *)c->list_off.p : nullptr,
+              c->plan_lists ? (int32_t *)c->lists.p : nullptr, int64_t(c->lists.bytes / 4));
         }
         SPG_LAUNCHED(c, "k_sym_bitmap");
       } else {  // SB_G
@@ -731,6 +761,9 @@ spg_status spg_symbolic(spg_ctx *c, const spg_csr *A, const spg_csr *B, int64_t 
   // the hash parts' tile records did not all fit: the buffer grows at the START
   // of the next symbolic (never between this plan and its numeric phase,
   // whose parts point into the current buffer); these parts hash their keys
+  if (c->plan_lists && size_t(c->plan.lists_need + size_t(c->num_sms) * 2 * kPoolList) * 4 > c->lists.bytes)
+    c->lists_want = size_t(c->plan.lists_need + (c->plan.lists_need >> 4) +
+                           size_t(c->num_sms) * 2 * kPoolList) * 4;
   if (c->plan.pkeys_used * kTileRec * 4 > c->pkeys.bytes && c->plan_parts)
     c->pkeys_want = std::max<size_t>(
         c->pkeys_want, size_t(c->plan.pkeys_used + (c->plan.pkeys_used >> 4) +
@@ -887,21 +920,26 @@ spg_status spg_numeric(spg_ctx *c, const spg_csr *A, const spg_csr *B, const int
       const int tmax = 1 << logT;
       const size_t smem = size_t(tmax) * 12;
       const int64_t grid = std::min<int64_t>(n, int64_t(c->num_sms) * 8);
+      // rows with a sorted column list from the bitmap symbolic (SPG_TUNE
+      // bit 32768 ignores the lists: A/B)
+      const bool use_lists = c->plan_lists && !(c->tune & 32768);
+      const int64_t *lo_p = use_lists ? (const int64_t *)c->list_off.p : nullptr;
+      const int32_t *li_p = use_lists ? (const int32_t *)c->lists.p : nullptr;
       // block size per table size (measured on C3: 2K slots 128 threads,
       // 4K / 8K 512, 16K 1024 -- smaller blocks idle less at the row
       // barrier, larger ones keep the occupancy of the big tables)
       if (logT <= 11) {
         ProfScope _ps(c, ss, "k_num_block<128>");
         k_num_block<128><<<(unsigned)std::min<int64_t>(n, int64_t(c->num_sms) * 32), 128, smem, ss>>>(
-            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax);
+            rb, n, a, b, flop, C_row_ptr, C_col_idx, C_val, sorted, tmax, OnePhase{}, lo_p, li_p);
       } else if (logT <= 13) {
         ProfScope _ps(c, ss, "k_num_block<512>");
         k_num_block<512><<<(unsigned)grid, 512, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx,
-                                                           C_val, sorted, tmax);
+                                                           C_val, sorted, tmax, OnePhase{}, lo_p, li_p);
       } else {
         ProfScope _ps(c, ss, "k_num_block<1024>");
         k_num_block<1024><<<(unsigned)grid, 1024, smem, ss>>>(rb, n, a, b, flop, C_row_ptr, C_col_idx,
-                                                             C_val, sorted, tmax);
+                                                             C_val, sorted, tmax, OnePhase{}, lo_p, li_p);
       }
       SPG_LAUNCHED(c, "k_num_block");
     } else if (use_parts) {  // NB_G: column-tile parts, independent work items

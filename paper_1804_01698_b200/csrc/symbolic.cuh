@@ -51,7 +51,7 @@ __device__ __forceinline__ uint32_t tbm_bit(uint32_t c) { return 1u << ((c >> 8)
 // bitmap words + 256 u16 ranks per 8192-column tile.
 constexpr int kTileRec = 256 + 128;
 #ifndef SPG_PBITS_SPAN
-#define SPG_PBITS_SPAN 16
+#define SPG_PBITS_SPAN 24
 #endif
 constexpr int kPbitsMaxSpan = SPG_PBITS_SPAN;
 constexpr int kDenseStripes = 16;
@@ -60,7 +60,8 @@ constexpr int kDenseStripes = 16;
 // refill instead of two round trips per row); unused part slots are marked
 // with row -1 and skipped by the parts bucket sort.
 constexpr int kPoolParts = 512;
-constexpr int kPoolRecs = 2048;  // 512-column stripes of a dense tile (one per numeric warp)  // tiles (the record set must fit the numeric's smem region)
+constexpr int kPoolRecs = 2048;
+constexpr int kPoolList = 65536;  // sorted column lists of the block-tier rows (entries per pool chunk)  // 512-column stripes of a dense tile (one per numeric warp)  // tiles (the record set must fit the numeric's smem region)
 
 // Which parts get tile records: the narrow multi-tile (hash) parts; with
 // SPG_DENSE_RECORDS also the single-tile (dense) ones (A/B, DESIGN.md §9b:
@@ -716,8 +717,12 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
                                                         int64_t parts_cap,
                                                         uint32_t *__restrict__ pbits,
                                                         int64_t pbits_cap,
-                                                        uint16_t *__restrict__ dpfx) {
+                                                        uint16_t *__restrict__ dpfx,
+                                                        int64_t *__restrict__ list_off,
+                                                        int32_t *__restrict__ lists,
+                                                        int64_t lists_cap) {
   extern __shared__ uint32_t s_dyn_u32[];
+  __shared__ long long s_lbase, s_lp_cur, s_lp_end;  // this row's sorted column list; the block's list pool
   __shared__ int s_cnt, s_next;
   __shared__ int s_w[132];
   __shared__ int s_dpart[kMaxTiles];  // part index of a dense (single-tile, no record) part at the tile, or -1
@@ -741,7 +746,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
   int32_t *bm_pre = bm_len + kBmEnt;
   const bool want_parts = parts != nullptr && info->b_unsorted == 0;
   for (int s = threadIdx.x; s < nwords; s += THREADS) bm[s] = 0u;  // (the count pass re-clears)
-  if (threadIdx.x == 0) s_pp_cur = s_pp_end = s_rp_cur = s_rp_end = 0;
+  if (threadIdx.x == 0) s_pp_cur = s_pp_end = s_rp_cur = s_rp_end = s_lp_cur = s_lp_end = 0;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int i = rows[r];
     if (threadIdx.x == 0) s_next = 0;
@@ -777,6 +782,25 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
       if (lane == 0) {
         s_tile[ntiles] = carry;
         s_cnt = carry;
+        // a row the numeric BLOCK tier will take (512 < nnz <= 8192: no
+        // parts) gets its sorted column list, from the block's list pool
+        long long lb = -1;
+        if (lists != nullptr && carry > 512 && carry <= kPartMinKeys) {
+          atomicAdd(&info->lists_need, (unsigned long long)carry);  // (the host sizes the buffer from it)
+          lb = s_lp_cur;
+          if (lb + carry > s_lp_end) {
+            lb = (long long)atomicAdd(&info->lists_pool, (unsigned long long)kPoolList);
+            s_lp_end = lb + kPoolList;
+          }
+          if (lb + carry > lists_cap) {
+            lb = -1;
+            s_lp_cur = s_lp_end;
+          } else {
+            s_lp_cur = lb + carry;
+          }
+        }
+        s_lbase = lb;
+        if (list_off != nullptr) list_off[i] = lb;
       }
     }
     __syncthreads();
@@ -935,6 +959,28 @@ __global__ void __launch_bounds__(THREADS) k_sym_bitmap(const int32_t *__restric
         for (int u = 0; u < 8; ++u) c += __popc(bm[bm_phys(qa + u)]);
         const int ex = warp_incl_scan(c) - c;
         if ((lane & 1) == 0) dpfx[int64_t(dp) * kDenseStripes + (lane >> 1)] = (uint16_t)ex;
+      }
+      // the row's sorted column list: lane l writes the columns of the
+      // tile's words 8 l .. 8 l + 7 in order
+      if (s_lbase >= 0 && s_tile[t + 1] > s_tile[t]) {
+        const int qa = q0 + 8 * lane;
+        uint32_t wv[8];
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          wv[u] = bm[bm_phys(qa + u)];
+          c += __popc(wv[u]);
+        }
+        int32_t *dst = lists + s_lbase + s_tile[t] + warp_incl_scan(c) - c;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint32_t wd = wv[u];
+          const int32_t cb = (int32_t)(qa + u) << 5;
+          while (wd) {
+            *dst++ = cb + __ffs(wd) - 1;
+            wd &= wd - 1;
+          }
+        }
       }
       for (int q = q0 + lane; q < q1; q += 32) bm[q] = 0u;
     }

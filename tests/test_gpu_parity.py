@@ -747,3 +747,20 @@ def test_dense_window_negative_zero_products(spg, ctx, sorted_out):
     for rep in range(2):                       # (the second with tile records)
         C = spg.spgemm(dA, dB, sorted=sorted_out, ctx=ctx)
         compare(*C.to_host(), o_rp, o_col, o_val, sorted_out, f"-0.0 products rep {rep}")
+
+
+@pytest.mark.parametrize("sorted_out", [True, False])
+def test_block_tier_sorted_lists(spg, monkeypatch, sorted_out):
+    """Sorted column lists (SPG_TUNE bit 65536, off by default): the bitmap
+    symbolic writes each block-tier row's sorted columns and the numeric
+    block tier accumulates by rank and emits by copying -- exact vs the
+    oracle on R-MAT rows with 512 < nnz(c_i) <= 8192 (and the rows around
+    them), twice on one ctx (the first call sizes the list buffer)."""
+    monkeypatch.setenv("SPG_TUNE", "65536")
+    ctx = spg.Context()
+    A, B, _ = synth.workload("c3_rmat20", scale=15)
+    dA = spg.DeviceCSR.from_host(A)
+    o = oracle.spgemm(A, B)
+    for rep in range(2):
+        C = spg.spgemm(dA, dA, sorted=sorted_out, ctx=ctx)
+        compare(*C.to_host(), *o, sorted_out, f"sorted lists rep {rep}")

@@ -1,0 +1,10 @@
+set -x
+python -c "from paper_1804_01698_b200 import build; build.build()" || exit 1
+SPG_NVCC_EXTRA="-DSPG_MED_BM=0" python -c "from paper_1804_01698_b200 import build; build.build(out='tools/ab_so/medbm0.so')" || exit 1
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/s4b_pytest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/s4b_pytest.log
+for r in 1 2; do
+timeout 900 python tools/ab_tune.py --rounds 1 --tunes 0,32768 --kernels k_num_tpart,k_sym_bitmap,k_num_block,k_sym_block > gpurun_out/s4b_ab_new$r.log 2>&1
+timeout 900 python tools/ab_tune.py --rounds 1 --so tools/ab_so/medbm0.so --kernels k_num_tpart,k_sym_bitmap,k_num_block,k_sym_block > gpurun_out/s4b_ab_m0$r.log 2>&1
+done
+grep -h tune= gpurun_out/s4b_ab_*.log
