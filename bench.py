@@ -357,11 +357,10 @@ def run_ours(args):
                "relabel_s": time.perf_counter() - t_rl}
 
     # accumulator A/B: sorted output with every eligible row
-    # hashed, or merged by the heap (the default ctx runs the cost model, AUTO)
-    acc_ctx = {}
-    for mode in ("hash", "heap"):
-        acc_ctx[mode] = spg.Context(local)
-        acc_ctx[mode].set_accumulator(mode)
+    # hashed, or merged by the heap (the default runs the cost model, AUTO).
+    # The variants switch the accumulator of the bench's own ctx (a second ctx
+    # could not hold C3's tile records next to the first one's)
+    acc_ctx = {mode: ctx for mode in ("hash", "heap")}
 
     def step(sorted_out):
         if isinstance(sorted_out, str) and sorted_out.startswith("acc_"):  # acc_<mode>[_deg]
@@ -463,8 +462,14 @@ def run_ours(args):
     if not args.no_accum_ab:
         kinds = (("deg_formed", "acc_hash_deg", "acc_heap_deg") if tri else ("acc_hash", "acc_heap"))
         for kname in kinds:
-            step(kname)
-            ms_k, _, _, last_k = timed(kname, max(1, min(args.steps, 5)))
+            mode = kname.split("_")[1]
+            if mode in ("hash", "heap"):
+                ctx.set_accumulator(mode)
+            try:
+                step(kname)
+                ms_k, _, _, last_k = timed(kname, max(1, min(args.steps, 5)))
+            finally:
+                ctx.set_accumulator("auto")
             acc_ab[kname] = ms_k
             if tri:
                 acc_counts.append(float(last_k))
@@ -478,19 +483,17 @@ def run_ours(args):
             parity["ok"] = parity["ok"] and all(
                 int(round(x / 2)) == parity["oracle_triangles"] for x in counts.tolist())
     clk = clocks.stop()
-    # (the A/B contexts' workspaces -- e.g. C3's tile records -- are released
-    # before the profiled pass builds its own)
     acc_ctx.clear()
     torch.cuda.empty_cache()
 
     # ---- per-kernel attribution: a separate profiled pass (outside the timed
-    # steps) on a ctx whose bins run on one stream, so each kernel's events
-    # bracket only that kernel
+    # steps) on the bench's ctx (its grow-only workspaces -- C3's tile records
+    # among them -- are the timed steps' ones) with its bins on one stream, so
+    # each kernel's events bracket only that kernel
     recs = []
     if rank == 0:
-        os.environ["SPG_SERIAL_BINS"] = "1"
-        pctx = spg.Context(local)
-        os.environ.pop("SPG_SERIAL_BINS")
+        pctx = ctx
+        _lib.spg_set_serial_bins(pctx.handle, True)
 
         def prof_step():
             if tri:  # the headline C5 step: row blocks of C = L*U, each masked by G
@@ -512,6 +515,7 @@ def run_ours(args):
         _lib.spg_profile_enable(pctx.handle, False)
         recs = _lib.spg_profile_records(pctx.handle)
         _lib.spg_profile_reset(pctx.handle)
+        _lib.spg_set_serial_bins(pctx.handle, False)
         ctx_attr, prof_steps = pctx, nprof
 
     gflops = lambda ms: 2.0 * flop_total / (ms * 1e-3) / 1e9  # noqa: E731

@@ -97,6 +97,13 @@ int64_t spg_launch_count(const spg_ctx *ctx);
  * events and returns their number; spg_profile_record returns the kernel
  * name (static string owned by the library) and duration in ms. */
 spg_status spg_profile_enable(spg_ctx *ctx, int enable);
+/* Bins on one stream (measurement aid; off by default, also set by the
+ * environment variable SPG_SERIAL_BINS=1 at ctx creation).  With on != 0 the
+ * per-bin kernels of the symbolic and numeric phases run one after another
+ * on the caller's stream instead of on concurrent internal streams, so the
+ * per-launch records of spg_profile_enable bracket one kernel each.  The
+ * results are identical.  Returns SPG_ERR_INVALID_ARG for a NULL ctx. */
+spg_status spg_set_serial_bins(spg_ctx *ctx, int on);
 spg_status spg_profile_reset(spg_ctx *ctx);
 int64_t spg_profile_count(spg_ctx *ctx);
 spg_status spg_profile_record(spg_ctx *ctx, int64_t idx, const char **name, float *ms);

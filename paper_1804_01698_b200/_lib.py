@@ -20,7 +20,7 @@ STATUS = {0: "SPG_OK", 1: "SPG_ERR_INVALID_ARG", 2: "SPG_ERR_DIM_MISMATCH",
 # every symbol include/spgemm.h declares
 EXPORTS = ("spg_ctx_create", "spg_ctx_destroy", "spg_last_error", "spg_launch_count",
            "spg_symbolic", "spg_numeric", "spg_get_info", "spg_plan_export",
-           "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable",
+           "spg_rows_to_parts", "spg_mask_sum", "spg_validate", "spg_profile_enable", "spg_set_serial_bins",
            "spg_profile_reset", "spg_profile_count", "spg_profile_record",
            "spg_debug_counters", "spg_masked_sum", "spg_degree_relabel",
            "spg_probe_stats", "spg_masked_sum_int", "spg_set_accumulator", "spg_onephase",
@@ -74,6 +74,7 @@ def load(path: str | None = None) -> ct.CDLL:
     lib.spg_mask_sum.argtypes = [vp, csrp, csrp, i64, i64p, vp]
     lib.spg_validate.argtypes = [vp, csrp, ct.c_int, vp]
     lib.spg_profile_enable.argtypes = [vp, ct.c_int]
+    lib.spg_set_serial_bins.argtypes = [vp, ct.c_int]
     lib.spg_profile_reset.argtypes = [vp]
     lib.spg_profile_count.argtypes = [vp]
     lib.spg_profile_count.restype = i64
@@ -166,6 +167,10 @@ def spg_validate(ctx: int, M: spg_csr, check_sorted: bool, stream: int) -> None:
 
 def spg_profile_enable(ctx: int, enable: bool) -> None:
     _check(ctx, "spg_profile_enable", load().spg_profile_enable(ctx, 1 if enable else 0))
+
+
+def spg_set_serial_bins(ctx: int, on: bool) -> None:
+    _check(ctx, "spg_set_serial_bins", load().spg_set_serial_bins(ctx, 1 if on else 0))
 
 
 def spg_profile_reset(ctx: int) -> None:

@@ -415,6 +415,12 @@ spg_status spg_profile_enable(spg_ctx *c, int enable) {
   return SPG_OK;
 }
 
+spg_status spg_set_serial_bins(spg_ctx *c, int on) {
+  if (!c) return SPG_ERR_INVALID_ARG;
+  c->serial = on ? 1 : 0;
+  return SPG_OK;
+}
+
 spg_status spg_profile_reset(spg_ctx *c) {
   if (!c) return SPG_ERR_INVALID_ARG;
   for (auto &r : c->recs) cudaEventSynchronize(r.b);
