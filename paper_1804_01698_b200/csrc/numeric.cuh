@@ -114,8 +114,10 @@ __device__ __forceinline__ bool warp_combine(bool act, uint32_t c, double &v) {
 __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t *cnt, int T,
                                           int logT, int nnz, int64_t rp0,
                                           int32_t *__restrict__ c_col,
-                                          double *__restrict__ c_val, int sorted) {
+                                          double *__restrict__ c_val, int sorted, int vlog = 0) {
+  // (vlog > 0: the value of slot s is at hash_vslot(s, vlog))
   const int lane = lane_id();
+  auto vs = [&](uint32_t s) -> uint32_t { return vlog ? hash_vslot(s, vlog) : s; };
   const unsigned lt_mask = (1u << lane) - 1u;
   if (!sorted) {
     int base = 0;
@@ -126,7 +128,7 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
       if (occ) {
         const int64_t o = rp0 + base + __popc(bal & lt_mask);
         c_col[o] = (int32_t)k;
-        c_val[o] = vals[s0 + lane];
+        c_val[o] = vals[vs(s0 + lane)];
       }
       base += __popc(bal);
     }
@@ -189,7 +191,7 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
           const int e = 4 * lane + r;
           if (e < nnz) {
             c_col[rp0 + e] = (int32_t)(mn + (pk[r] >> logT));
-            c_val[rp0 + e] = vals[pk[r] & uint32_t(T - 1)];
+            c_val[rp0 + e] = vals[vs(pk[r] & uint32_t(T - 1))];
           }
         }
         return;
@@ -199,11 +201,25 @@ __device__ __forceinline__ void warp_emit(uint32_t *keys, double *vals, uint32_t
     // are monotone in the column: b(c) = (c - min) >> sh, T buckets for
     // nnz <= T/2 keys; each key's position = bucket offset + its rank
     // among the (few) keys of its bucket.
-    // 1. compact occupied slots to the front (destination <= source)
+    // 1. compact occupied slots to the front (destination <= source; with
+    //    permuted values (vlog > 0, T <= 256) a lane first holds its slots'
+    //    values in registers, so no write lands on an unread value)
+    double vreg[8];
+    if (vlog) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vreg[j] = 32 * j < T ? vals[vs(32 * j + lane)] : 0.0;
+      __syncwarp();
+    }
     int base = 0;
     for (int s0 = 0; s0 < T; s0 += 32) {
       const uint32_t k = keys[s0 + lane];
-      const double v = vals[s0 + lane];
+      double v = 0.0;
+      if (vlog) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) if (32 * j == s0) v = vreg[j];
+      } else {
+        v = vals[s0 + lane];
+      }
       const bool occ = k != kEmpty;
       const unsigned bal = __ballot_sync(kFull, occ);
       __syncwarp();
@@ -322,16 +338,24 @@ __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_
     for (int s = lane; s < T; s += 32) { keys[s] = kEmpty; vals[s] = 0.0; }
     __syncwarp();
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
+    // value slot of key c (chunked probing: the values of chunk position e
+    // live at e T/4 + chunk, as in the block tiers, so a round's first-slot
+    // values fall in distinct banks)
+    // (tables of <= 256 slots: the emit can hold a lane's values in registers)
+    const bool chunked = SPG_WARP_CHUNK && T <= 256;
+    auto wslot = [&](uint32_t c) -> uint32_t {
+      return chunked ? hash_vslot(num_probe_smem(keys, c, logT), logT) : num_probe(keys, c, logT);
+    };
     if (use_seq(flop[i], ae - as)) {
       // keys of a round are distinct: plain read-modify-write of the value
       for_row<true, true, 2>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
-        if (act) vals[num_probe(keys, c, logT)] += v;   // c_ij <- c_ij + value (l.8)
+        if (act) vals[wslot(c)] += v;   // c_ij <- c_ij + value (l.8)
         __syncwarp();
       });
     } else {
       for_row<false, true, 2>(A, B, as, ae, 0, 1, [&](bool act, uint32_t c, double v) {
         uint32_t slot = 0;
-        if (act) slot = num_probe(keys, c, logT);
+        if (act) slot = wslot(c);
         const unsigned grp = __match_any_sync(kFull, act ? c : (0x80000000u | lane));
         if (act) {
           if (__popc(grp) == 1) vals[slot] += v;   // c_ij <- c_ij + value (l.8)
@@ -344,7 +368,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_
       for (int s0 = 0; s0 < T; s0 += 32) nnz += __popc(__ballot_sync(kFull, keys[s0 + lane] != kEmpty));
       if (lane == 0) op.row_nnz[i] = nnz;
     }
-    warp_emit(keys, vals, cnt, T, logT, nnz, rp0, c_col, c_val, sorted);
+    warp_emit(keys, vals, cnt, T, logT, nnz, rp0, c_col, c_val, sorted, chunked ? logT : 0);
     __syncwarp();
   }
 }

@@ -99,6 +99,11 @@ __device__ __forceinline__ int sym_log2_gpu(int64_t flop, int64_t ncols) {
 // column space fits one (it also cuts the row into column-range parts for the
 // numeric phase); otherwise the larger smem hash tables / global hash.
 constexpr int64_t kBitmapMaxCols = int64_t(200 * 1024) * 8;  // 200 KB of bits
+// Warp tiers probe 4-slot chunks (one LDS.128 per probe; SPG_WARP_CHUNK=0:
+// scalar linear probing, the round-1 warp tiers)
+#ifndef SPG_WARP_CHUNK
+#define SPG_WARP_CHUNK 0
+#endif
 #ifndef SPG_MED_BM
 #define SPG_MED_BM 0
 #endif

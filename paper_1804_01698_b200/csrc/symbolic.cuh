@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
       if (BUCKET) cnt += warp_bucket_insert(tab, logT, act, c);
-      else if (act) cnt += sym_insert(tab, c, logT);
+      else if (act) cnt += SPG_WARP_CHUNK ? sym_insert_smem(tab, c, logT) : sym_insert(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, SPG_SYM_WARP_DEPTH>(A, B, as, ae, 0, 1, ins);
     else for_row<false, false, 2>(A, B, as, ae, 0, 1, ins);
@@ -567,7 +567,10 @@ __device__ __forceinline__ uint32_t bm_phys(uint32_t q) {
   return q ^ (((q >> 5) * 0x9E3779B1u) >> 27);
 }
 constexpr int kBmD = 4;        // short rounds resolved per batch
-constexpr int kBmLong = 32;    // B rows of >= kBmLong entries walk sequentially
+#ifndef SPG_BM_LONG
+#define SPG_BM_LONG 32
+#endif
+constexpr int kBmLong = SPG_BM_LONG;  // B rows of >= kBmLong entries walk sequentially
 constexpr size_t kBmStageBytes = size_t(kBmEnt) * 16 + 16;
 
 __device__ __forceinline__ void bm_set(uint32_t *bm, uint32_t c) {
