@@ -83,6 +83,48 @@ __device__ __forceinline__ void red_shared_f64(uint32_t saddr, double v) {
   asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(saddr), "d"(v) : "memory");
 }
 
+// Two independent fp64 adds into shared memory (SPG_ADD2 builds): both
+// current values are loaded and both CAS issued before either result is
+// tested, so the two read-modify-write round trips overlap (the lowered
+// red.shared.add.f64 is a serial LDS + CAS-spin loop per add).  A failed CAS
+// returns the slot's current bits, which seed the retry.
+#ifndef SPG_ADD2
+#define SPG_ADD2 0
+#endif
+__device__ __forceinline__ void add2_shared_f64(bool a0, uint32_t s0, double v0, bool a1, uint32_t s1,
+                                                double v1) {
+#if SPG_ADD2
+  unsigned long long x0 = 0, x1 = 0;
+  if (a0) asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x0) : "r"(s0) : "memory");
+  if (a1) asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x1) : "r"(s1) : "memory");
+  unsigned p0 = a0, p1 = a1;
+  while (p0 | p1) {
+    const unsigned long long n0 = (unsigned long long)__double_as_longlong(
+        __dadd_rn(__longlong_as_double((long long)x0), v0));
+    const unsigned long long n1 = (unsigned long long)__double_as_longlong(
+        __dadd_rn(__longlong_as_double((long long)x1), v1));
+    unsigned long long o0 = x0, o1 = x1;  // (an inactive side keeps x: done)
+    // both CAS predicated, no branch between them
+    asm volatile(
+        "{\n\t.reg .pred q0, q1;\n\t"
+        "setp.ne.u32 q0, %8, 0;\n\t"
+        "setp.ne.u32 q1, %9, 0;\n\t"
+        "@q0 atom.shared.cas.b64 %0, [%2], %4, %6;\n\t"
+        "@q1 atom.shared.cas.b64 %1, [%3], %5, %7;\n\t}"
+        : "+l"(o0), "+l"(o1)
+        : "r"(s0), "r"(s1), "l"(x0), "l"(x1), "l"(n0), "l"(n1), "r"(p0), "r"(p1)
+        : "memory");
+    p0 = p0 && o0 != x0;
+    p1 = p1 && o1 != x1;
+    x0 = o0;
+    x1 = o1;
+  }
+#else
+  if (a0) red_shared_f64(s0, v0);
+  if (a1) red_shared_f64(s1, v1);
+#endif
+}
+
 // Lanes of a round holding the same key c combine their values into the
 // lowest such lane; returns true for the lanes that then hold a key to apply
 // (active, first of their key).  Summation order inside a round is free
@@ -1026,8 +1068,8 @@ __device__ __forceinline__ void for_tpart_rounds(const DevCSR &B, const int32_t 
       c[d] = act[d] ? (uint32_t)__ldg(B.col + q[d]) : 0u;
       v[d] = act[d] ? __ldg(B.val + q[d]) : 0.0;
     }
-#pragma unroll
-    for (int d = 0; d < kD; ++d) f(act[d], c[d], a[d] * v[d]);  // a_ik * b_kj (Fig:code_spgemm l.5)
+    static_assert(kD == 2, "pairs of rounds");
+    f(act[0], c[0], a[0] * v[0], act[1], c[1], a[1] * v[1]);  // a_ik * b_kj (Fig:code_spgemm l.5)
   }
 }
 
@@ -1065,14 +1107,13 @@ __device__ __forceinline__ void for_long_rounds_entry(const DevCSR &B, const int
       const double v0 = act0 ? __ldg(pv + t) : 0.0;
       const uint32_t c1 = act1 ? (uint32_t)__ldg(pc + t + 32) : 0u;
       const double v1 = act1 ? __ldg(pv + t + 32) : 0.0;
-      f(act0, c0, a * v0);
-      f(act1, c1, a * v1);
+      f(act0, c0, a * v0, act1, c1, a * v1);
     }
     if (g < re) {
       const bool act0 = t < L;
       const uint32_t c0 = act0 ? (uint32_t)__ldg(pc + t) : 0u;
       const double v0 = act0 ? __ldg(pv + t) : 0.0;
-      f(act0, c0, a * v0);
+      f(act0, c0, a * v0, false, 0u, 0.0);
       ++g;
     }
     ++j;
@@ -1128,7 +1169,7 @@ __device__ __forceinline__ void for_long_rounds(const DevCSR &B, const int32_t *
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       if (g + d < g1) {
-        f(c[d] != kEmpty, c[d], la[jd[d]] * v[d]);  // a_ik * b_kj (Fig:code_spgemm l.5)
+        f(c[d] != kEmpty, c[d], la[jd[d]] * v[d], false, 0u, 0.0);  // a_ik * b_kj (Fig:code_spgemm l.5)
         if (gl < g1) load(d);
       }
     }
@@ -1189,6 +1230,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   __shared__ long long s_q;
   __shared__ int4 s_P, s_P1, s_P2, s_Pn[3];
   __shared__ int s_pn_ok;  // the next part exists (its records are in s_Pn once thread 0 waited)
+  // the dense window was used by a record / hash part (written by thread 0 at
+  // the publish step: a shared flag instead of a register kept across parts)
+  __shared__ int s_dirty;
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   char *base = reinterpret_cast<char *>(s_dyn_f64);
@@ -1217,8 +1261,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
   const uint32_t dv_sa = (uint32_t)__cvta_generic_to_shared(dv);
   for (int s = threadIdx.x; s < kTileCols; s += THREADS) dvb[s] = kNegZeroBits;
   long long q_next = 0;  // (thread 0) reserved part after the current one
-  bool dirty = false;    // the dense window was used by a record / hash part (block-uniform)
   if (threadIdx.x == 0) {
+    s_dirty = 0;
     s_res[0][0] = s_res[0][1] = s_res[1][0] = s_res[1][1] = 0ull;
     const long long q = (long long)atomicAdd(counter, 1ull);
     s_q = q;
@@ -1281,33 +1325,33 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       const uint4 *src = reinterpret_cast<const uint4 *>(pbits + koff * kTileRec);
       for (int q = threadIdx.x; q < nrec / 4; q += THREADS) reinterpret_cast<uint4 *>(rec)[q] = ld_once(src + q);
       for (int r = threadIdx.x; r < cnt; r += THREADS) rv[r] = 0.0;
-      dirty = true;
     } else if (!dense) {
       for (int s = threadIdx.x; s < T; s += THREADS) { hk[s] = kEmpty; hv[s] = 0.0; }
-      dirty = true;
-    } else if (dirty) {  // a dense window after parts that used the region otherwise
+    } else if (s_dirty) {  // a dense window after a part that used the region otherwise
       for (int s = threadIdx.x; s < kTileCols; s += THREADS) dvb[s] = kNegZeroBits;
-      dirty = false;
     }
     if (threadIdx.x == 0) s_cnt = 0;
     const int32_t *tk0 = toff + int64_t(t0) * nB, *tk1 = toff + int64_t(t1) * nB;
     const uint32_t lo32 = (uint32_t)lo;
-    auto acc_dense = [&](bool act, uint32_t c, double v) {
+    auto acc_dense = [&](bool a0, uint32_t c0, double v0, bool a1, uint32_t c1, double v1) {
       // c_ij <- c_ij + value (l.8), dense window (presence: the slot left -0.0)
-      if (act) red_shared_f64(dv_sa + 8u * dense_slot(c - lo32), nz_product(v));
+      add2_shared_f64(a0, dv_sa + 8u * dense_slot(c0 - lo32), nz_product(v0), a1,
+                      dv_sa + 8u * dense_slot(c1 - lo32), nz_product(v1));
     };
-    auto acc_known = [&](bool act, uint32_t c, double v) {  // rank of the column in the part
-      if (act) {
-        const uint32_t off = c - (uint32_t)lo, q = off >> 5;
-        const uint32_t *tr = rec + (q >> 8) * kTileRec;
-        const uint32_t wd = tr[q & 255u];
-        const int rank = (int)reinterpret_cast<const uint16_t *>(tr + 256)[q & 255u] +
-                         __popc(wd & ((1u << (off & 31u)) - 1u));
-        atomicAdd(rv + rank, v);  // c_ij <- c_ij + value (l.8)
-        rcol[rank] = (int32_t)c;  // (every product of the key stores the same column)
-      }
+    const uint32_t rv_sa = (uint32_t)__cvta_generic_to_shared(rv);
+    auto rank_of = [&](uint32_t c) {  // rank of the column in the part
+      const uint32_t off = c - (uint32_t)lo, q = off >> 5;
+      const uint32_t *tr = rec + (q >> 8) * kTileRec;
+      const uint32_t wd = tr[q & 255u];
+      return (int)reinterpret_cast<const uint16_t *>(tr + 256)[q & 255u] + __popc(wd & ((1u << (off & 31u)) - 1u));
     };
-    auto acc_hash = [&](bool act, uint32_t c, double v) {
+    auto acc_known = [&](bool a0, uint32_t c0, double v0, bool a1, uint32_t c1, double v1) {
+      const int r0 = a0 ? rank_of(c0) : 0, r1 = a1 ? rank_of(c1) : 0;
+      add2_shared_f64(a0, rv_sa + 8u * r0, v0, a1, rv_sa + 8u * r1, v1);  // c_ij <- c_ij + value (l.8)
+      if (a0) rcol[r0] = (int32_t)c0;  // (every product of the key stores the same column)
+      if (a1) rcol[r1] = (int32_t)c1;
+    };
+    auto acc_hash1 = [&](bool act, uint32_t c, double v) {
       bool isnew = false;
       uint32_t slot = 0;
       if (act) {
@@ -1322,6 +1366,10 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
         b0 = __shfl_sync(kFull, b0, leader);
         if (isnew) slot_of[b0 + __popc(m & ((1u << lane) - 1u))] = (uint16_t)slot;
       }
+    };
+    auto acc_hash = [&](bool a0, uint32_t c0, double v0, bool a1, uint32_t c1, double v1) {
+      acc_hash1(a0, c0, v0);
+      acc_hash1(a1, c1, v1);
     };
     for (int cb = 0; cb < na; cb += kTEnt) {
       const int n = min(kTEnt, na - cb);
@@ -1429,7 +1477,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       const int gl0 = (int)((int64_t)RL * w / NW), gl1 = (int)((int64_t)RL * (w + 1) / NW);
       if (tune & 32) {  // (measurement only: gathers without accumulation; C left unwritten)
         double sink = 0.0;
-        auto acc_none = [&](bool act, uint32_t c, double v) { sink += act ? v + (double)c : 0.0; };
+        auto acc_none = [&](bool a0, uint32_t c0, double v0, bool a1, uint32_t c1, double v1) {
+          sink += (a0 ? v0 + (double)c0 : 0.0) + (a1 ? v1 + (double)c1 : 0.0);
+        };
         for_long_rounds(B, ls, ll, la, lpre, nL, RL, gl0, gl1, acc_none);
         for_tpart_rounds<2>(B, es, ea, epre, nS, PS, gs0, gs1, acc_none);
         if (sink == 1.2345e300) dbg[13] = 1;
@@ -1477,24 +1527,34 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       const unsigned below = (1u << lane) - 1u;
       const int32_t cbase = (int32_t)lo + w * GPW * 32 + lane;
       int o = 0;
-#pragma unroll 4
-      for (int j = 0; j < GPW; ++j) {
-        const uint32_t ds = dense_slot(uint32_t(w * GPW + j) * 32u + lane);
-        const unsigned long long bits = dvb[ds];
-        const bool pres = bits != kNegZeroBits;
-        const unsigned m = __ballot_sync(kFull, pres);
-        if (pres) {
-          const int p = o + __popc(m & below);
-          if (tune & 16384) {  // (A/B: plain write-back stores)
-            cc[p] = cbase + j * 32;
-            cvp[p] = __longlong_as_double(bits);
-          } else if (!(tune & 8192)) {  // (measurement switch: 8192 skips the stores)
-            st_c(cc + p, cbase + j * 32);
-            st_c(cvp + p, __longlong_as_double(bits));
-          }
-          dvb[ds] = kNegZeroBits;
+      // batches of kEB groups: every slot value loaded first (no store
+      // between the loads, so they are all in flight at once), the batch's
+      // slots reset to -0.0 unconditionally, then ballots and coalesced
+      // stores from registers
+      constexpr int kEB = 8;
+      static_assert(GPW % kEB == 0, "emit batches");
+#pragma unroll
+      for (int j0 = 0; j0 < GPW; j0 += kEB) {
+        unsigned long long bits[kEB];
+        uint32_t ds[kEB];
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          ds[u] = dense_slot(uint32_t(w * GPW + j0 + u) * 32u + lane);
+          bits[u] = dvb[ds[u]];
         }
-        o += __popc(m);
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) dvb[ds[u]] = kNegZeroBits;
+#pragma unroll
+        for (int u = 0; u < kEB; ++u) {
+          const bool pres = bits[u] != kNegZeroBits;
+          const unsigned m = __ballot_sync(kFull, pres);
+          if (pres) {
+            const int p = o + __popc(m & below);
+            st_c(cc + p, cbase + (j0 + u) * 32);
+            st_c(cvp + p, __longlong_as_double(bits[u]));
+          }
+          o += __popc(m);
+        }
       }
     } else if (dense && !known) {
       // warp w owns the 32-column groups [GPW w, GPW (w + 1)) (ascending
@@ -1620,6 +1680,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_num_tpart(
       }
     }
     if (threadIdx.x == 0) {  // publish the next part (every thread has read this one)
+      s_dirty = known || !dense;  // (a dense part's emit leaves its window clean)
       s_q = q_next;
       s_P = s_Pn[0];
       s_P1 = s_Pn[1];
