@@ -650,12 +650,24 @@ __device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, in
           const int L = st_len[j];
           const int32_t *pc = B.col + st_bs[j];
           int t = (g - rb) * 32 + lane;
-          for (; g + 1 < re; g += 2, t += 64) {
+          // four rounds' column loads in flight per step (the walk waits on
+          // these gathers, not on the bitmap ORs)
+          for (; g + 3 < re; g += 4, t += 128) {
+            uint32_t c[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) c[d] = t + 32 * d < L ? (uint32_t)__ldg(pc + t + 32 * d) : kEmpty;
+#pragma unroll
+            for (int d = 0; d < 4; ++d)
+              if (c[d] != kEmpty) bm_set(bm, c[d]);
+          }
+          if (g + 1 < re) {
             const bool a0 = t < L, a1 = t + 32 < L;
             const uint32_t c0 = a0 ? (uint32_t)__ldg(pc + t) : 0u;
             const uint32_t c1 = a1 ? (uint32_t)__ldg(pc + t + 32) : 0u;
             if (a0) bm_set(bm, c0);
             if (a1) bm_set(bm, c1);
+            g += 2;
+            t += 64;
           }
           if (g < re) {
             if (t < L) bm_set(bm, (uint32_t)__ldg(pc + t));
