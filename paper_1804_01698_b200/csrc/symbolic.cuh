@@ -652,6 +652,14 @@ __device__ __forceinline__ void bm_walk_row(const DevCSR &A, const DevCSR &B, in
           int t = (g - rb) * 32 + lane;
           // four rounds' column loads in flight per step (the walk waits on
           // these gathers, not on the bitmap ORs)
+          for (; g + 7 < re; g += 8, t += 256) {
+            uint32_t c[8];
+#pragma unroll
+            for (int d = 0; d < 8; ++d) c[d] = t + 32 * d < L ? (uint32_t)__ldg(pc + t + 32 * d) : kEmpty;
+#pragma unroll
+            for (int d = 0; d < 8; ++d)
+              if (c[d] != kEmpty) bm_set(bm, c[d]);
+          }
           for (; g + 3 < re; g += 4, t += 128) {
             uint32_t c[4];
 #pragma unroll
