@@ -101,9 +101,16 @@ def _check(ctx, fn: str, status: int):
         raise SpgError(fn, status, msg)
 
 
-def spg_ctx_create() -> int:
+# spg_alloc_fn / spg_free_fn of include/spgemm.h
+ALLOC_FN = ct.CFUNCTYPE(ct.c_void_p, ct.c_size_t, ct.c_void_p, ct.c_void_p)
+FREE_FN = ct.CFUNCTYPE(None, ct.c_void_p, ct.c_void_p, ct.c_void_p)
+
+
+def spg_ctx_create(alloc=None, free_fn=None) -> int:
+    """alloc / free_fn: ALLOC_FN / FREE_FN instances (both or neither); the
+    caller keeps them alive for the lifetime of the ctx."""
     h = ct.c_void_p()
-    st = load().spg_ctx_create(ct.byref(h), None, None, None)
+    st = load().spg_ctx_create(ct.byref(h), alloc, free_fn, None)
     _check(None, "spg_ctx_create", st)
     return h.value
 

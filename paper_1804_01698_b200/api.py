@@ -64,11 +64,47 @@ class DeviceCSR:
 class Context:
     """One spg_ctx (plan + grow-only workspace) bound to a CUDA device."""
 
-    def __init__(self, device=None):
+    def __init__(self, device=None, allocator: str = "cuda"):
+        """allocator: where the grow-only ctx workspace comes from.
+        "cuda" (default) = cudaMalloc / cudaFree inside the library;
+        "torch" = the PyTorch caching allocator through the C ABI's
+        spg_alloc_fn / spg_free_fn callbacks (called only when the workspace
+        grows).  The free callback synchronises the device first, as cudaFree
+        does: a released buffer may still be read by kernels on the ctx's
+        internal streams."""
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None
                                    else torch.device(device).index or 0)
+        self.allocator = allocator
+        self._live = {}            # ptr -> bytes held through the callbacks ("torch" only)
+        self._cb = (None, None)
+        if allocator == "torch":
+            dev = self.device.index
+            live = self._live      # (the callbacks close over this dict, not over self)
+
+            def _alloc(nbytes, stream, _user):
+                try:
+                    p = torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0))
+                except Exception:   # (OOM: the library reports SPG_ERR_WORKSPACE)
+                    return None
+                live[p] = int(nbytes)
+                return p
+
+            def _free(ptr, _stream, _user):
+                if ptr:
+                    torch.cuda.synchronize(dev)
+                    live.pop(ptr, None)
+                    torch.cuda.caching_allocator_delete(ptr)
+
+            self._cb = (_lib.ALLOC_FN(_alloc), _lib.FREE_FN(_free))
+        elif allocator != "cuda":
+            raise ValueError("allocator must be 'cuda' or 'torch'")
         with torch.cuda.device(self.device):
-            self.handle = _lib.spg_ctx_create()
+            self.handle = _lib.spg_ctx_create(*self._cb)
+
+    @property
+    def workspace_bytes(self) -> int:
+        """Bytes of ctx workspace currently held through the allocator callbacks."""
+        return sum(self._live.values())
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -764,3 +764,29 @@ def test_block_tier_sorted_lists(spg, monkeypatch, sorted_out):
     for rep in range(2):
         C = spg.spgemm(dA, dA, sorted=sorted_out, ctx=ctx)
         compare(*C.to_host(), *o, sorted_out, f"sorted lists rep {rep}")
+
+
+def test_torch_allocator_callbacks(spg):
+    """The C ABI's spg_alloc_fn / spg_free_fn (include/spgemm.h): a ctx whose
+    workspace comes from the PyTorch caching allocator gives the oracle's
+    result, grows through the callbacks (a second, larger product) and hands
+    everything back on destroy."""
+    ctx = spg.Context(allocator="torch")
+    assert ctx.workspace_bytes == 0
+    for n, seed in ((3000, 11), (40000, 12)):
+        A = synth.er_poisson(n, 8.0, seed)
+        for sorted_out in (True, False):
+            gpu_vs_oracle(A, A, sorted_out, ctx=ctx, what=f"torch allocator n={n}")
+        held = ctx.workspace_bytes
+        assert held > 0 and len(ctx._live) > 0
+    small = held
+    A = synth.rmat(14, 16, seed=5)   # long rows: parts, tile offsets, slabs
+    gpu_vs_oracle(A, A, True, ctx=ctx, what="torch allocator rmat14")
+    assert ctx.workspace_bytes > small
+    live = ctx._live
+    del ctx
+    import gc
+    gc.collect()
+    assert len(live) == 0
+    with pytest.raises(ValueError):
+        spg.Context(allocator="nope")
