@@ -391,7 +391,7 @@ spg_status spg_ctx_destroy(spg_ctx *c) {
                  &c->toff,      &c->bnz,       &c->prune_cnt, &c->prune_rp,  &c->prune_col,
                  &c->prune_val, &c->prune_idx, &c->trow,      &c->rl_key,    &c->rl_rank,
                  &c->rl_tmp,    &c->rl_cub,    &c->mask_rows, &c->useful_bits, &c->one_fofs,
-                 &c->one_col,   &c->one_val};
+                 &c->one_col,   &c->one_val,   &c->dpfx,      &c->lists,     &c->list_off};
   for (Buf *b : bufs) buf_release(c, *b, nullptr);
   if (c->host_info) cudaFreeHost(c->host_info);
   for (int k = 0; k < kSubStreams; ++k) {

@@ -14,7 +14,7 @@ echo "c5 rc=$?" >> gpurun_out/fin2_rc.log
 SPG_SERIAL_BINS=1 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_num_tpart|k_sym_bitmap" -s 2 -c 2 \
     -o gpurun_out/fin_full_c3 -f python tools/profile_step.py --config c3_rmat20 --reps 2 --sorted 1 > gpurun_out/fin_ncu_full_c3.log 2>&1
 echo "full c3 rc=$?" >> gpurun_out/fin2_rc.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_num_warp|k_sym_warp" -s 2 -c 2 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_num_warp|k_sym_warp" -c 6 \
     -o gpurun_out/fin_full_c2 -f python tools/profile_step.py --reps 2 > gpurun_out/fin_ncu_full_c2.log 2>&1
 echo "full c2 rc=$?" >> gpurun_out/fin2_rc.log
 python tools/ncu_summary.py gpurun_out/fin_ncu_summary.md C3=gpurun_out/fin_full_c3.ncu-rep C2=gpurun_out/fin_full_c2.ncu-rep > gpurun_out/fin_ncu_summary.log 2>&1
