@@ -30,6 +30,35 @@ __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int lo
   }
 }
 
+// The same for the warp tier's warp-private shared tables.  SPG_NUM_PROBE
+// (A/B switch): 0 = num_probe; 1 = the slot's occupant after an attempted
+// insert decides (one exit test per step); 2 = CAS-first (no plain load).
+#ifndef SPG_NUM_PROBE
+#define SPG_NUM_PROBE 0
+#endif
+__device__ __forceinline__ uint32_t num_probe_w(uint32_t *keys, uint32_t c, int logT) {
+#if SPG_NUM_PROBE == 0
+  return num_probe(keys, c, logT);
+#else
+  const uint32_t mask = (1u << logT) - 1u;
+  uint32_t h = hash_slot(c, logT);
+  while (true) {
+#if SPG_NUM_PROBE == 1
+    uint32_t k = ((volatile uint32_t *)keys)[h];
+    if (k == kEmpty) {
+      k = atomicCAS(keys + h, kEmpty, c);
+      k = k == kEmpty ? c : k;
+    }
+    if (k == c) return h;
+#else
+    const uint32_t old = atomicCAS(keys + h, kEmpty, c);
+    if (old == kEmpty || old == c) return h;
+#endif
+    h = (h + 1u) & mask;
+  }
+#endif
+}
+
 // Bank spreading of the fp64 accumulators (shared-memory CAS adds serialise
 // per bank; measured 26 wavefronts per 32-lane ATOMS.CAST.64 on C3):
 //  * dense window: column offset -> slot off ^ (bits 4-7) ^ (bits 8-11) ^
@@ -386,7 +415,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SORTED ? 40 : 48) / WARPS) k_num_
     // (tables of <= 256 slots: the emit can hold a lane's values in registers)
     const bool chunked = SPG_WARP_CHUNK && T <= 256;
     auto wslot = [&](uint32_t c) -> uint32_t {
-      return chunked ? hash_vslot(num_probe_smem(keys, c, logT), logT) : num_probe(keys, c, logT);
+      return chunked ? hash_vslot(num_probe_smem(keys, c, logT), logT) : num_probe_w(keys, c, logT);
     };
     if (use_seq(flop[i], ae - as)) {
       // keys of a round are distinct: plain read-modify-write of the value

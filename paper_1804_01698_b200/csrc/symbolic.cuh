@@ -28,6 +28,24 @@ __device__ __forceinline__ int sym_insert(uint32_t *tab, uint32_t c, int logT) {
   }
 }
 
+// Warp-private shared-memory table, CAS-first probing (A/B switch
+// SPG_SYM_CASFIRST): one ATOMS.CAS per probe decides hit / inserted / occupied
+// (no load + compare + conditional CAS), so the divergent probe loop has one
+// exit test per step.
+#ifndef SPG_SYM_CASFIRST
+#define SPG_SYM_CASFIRST 0
+#endif
+__device__ __forceinline__ int sym_insert_cas(uint32_t *tab, uint32_t c, int logT) {
+  const uint32_t mask = (1u << logT) - 1u;
+  uint32_t h = hash_slot(c, logT);
+  while (true) {
+    const uint32_t old = atomicCAS(tab + h, kEmpty, c);
+    if (old == kEmpty) return 1;
+    if (old == c) return 0;
+    h = (h + 1u) & mask;  // linear probing
+  }
+}
+
 // Same, for a shared-memory table (chunked probing).
 __device__ __forceinline__ int sym_insert_smem(uint32_t *tab, uint32_t c, int logT) {
   bool isnew = false;
@@ -497,7 +515,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_sym_warp(const int32_t *__restri
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
       if (BUCKET) cnt += warp_bucket_insert(tab, logT, act, c);
-      else if (act) cnt += SPG_WARP_CHUNK ? sym_insert_smem(tab, c, logT) : sym_insert(tab, c, logT);
+      else if (act) cnt += SPG_WARP_CHUNK ? sym_insert_smem(tab, c, logT)
+                      : SPG_SYM_CASFIRST ? sym_insert_cas(tab, c, logT) : sym_insert(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, SPG_SYM_WARP_DEPTH>(A, B, as, ae, 0, 1, ins);
     else for_row<false, false, 2>(A, B, as, ae, 0, 1, ins);
