@@ -31,10 +31,12 @@ __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int lo
 }
 
 // The same for the warp tier's warp-private shared tables.  SPG_NUM_PROBE
-// (A/B switch): 0 = num_probe; 1 = the slot's occupant after an attempted
-// insert decides (one exit test per step); 2 = CAS-first (no plain load).
+// (switch): 0 = num_probe; 1 = the slot's occupant after an attempted
+// insert decides (one exit test per step); 2 = CAS-first (no plain load: one
+// ATOMS.CAS per probe decides hit / inserted / occupied).  Measured on C2
+// (k_num_warp<256>, sorted): 1.156 / 1.105 / 1.025 ms: 2 is the default.
 #ifndef SPG_NUM_PROBE
-#define SPG_NUM_PROBE 0
+#define SPG_NUM_PROBE 2
 #endif
 __device__ __forceinline__ uint32_t num_probe_w(uint32_t *keys, uint32_t c, int logT) {
 #if SPG_NUM_PROBE == 0
