@@ -30,6 +30,18 @@ __device__ __forceinline__ uint32_t num_probe(uint32_t *keys, uint32_t c, int lo
   }
 }
 
+// CAS-first linear probing of a shared table: one ATOMS.CAS per probe decides
+// hit / inserted / occupied.
+__device__ __forceinline__ uint32_t num_probe_cas(uint32_t *keys, uint32_t c, int logT) {
+  const uint32_t mask = (1u << logT) - 1u;
+  uint32_t h = hash_slot(c, logT);
+  while (true) {
+    const uint32_t old = atomicCAS(keys + h, kEmpty, c);
+    if (old == kEmpty || old == c) return h;
+    h = (h + 1u) & mask;
+  }
+}
+
 // The same for the warp tier's warp-private shared tables.  SPG_NUM_PROBE
 // (switch): 0 = num_probe; 1 = the slot's occupant after an attempted
 // insert decides (one exit test per step); 2 = CAS-first (no plain load: one
@@ -790,7 +802,8 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_num_block(const int
       const int64_t as = A.rp[i], ae = A.rp[i + 1];
       auto slot_of = [&](uint32_t c) -> double * {
         return lrow ? vals + rank[probe_find(keys, c, logT)]
-                    : vals + hash_vslot(num_probe_smem(keys, c, logT), logT);
+                    : vals + hash_vslot(SPG_BLOCK_CASFIRST ? num_probe_cas(keys, c, logT)
+                                                           : num_probe_smem(keys, c, logT), logT);
       };
       auto acc = [&](bool act, uint32_t c, double v) {  // c_ij <- c_ij + value (l.8)
         if (act) atomicAdd(slot_of(c), v);

@@ -46,6 +46,12 @@ __device__ __forceinline__ int sym_insert_cas(uint32_t *tab, uint32_t c, int log
   }
 }
 
+// Block tiers (block-shared tables): CAS-first single-slot probing instead of
+// the 4-slot chunks (A/B switch; also the numeric block tier's key probe).
+#ifndef SPG_BLOCK_CASFIRST
+#define SPG_BLOCK_CASFIRST 0
+#endif
+
 // Same, for a shared-memory table (chunked probing).
 __device__ __forceinline__ int sym_insert_smem(uint32_t *tab, uint32_t c, int logT) {
   bool isnew = false;
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(THREADS) k_sym_block(const int32_t *__restrict
     int cnt = 0;
     const int64_t as = A.rp[i], ae = A.rp[i + 1];
     auto ins = [&](bool act, uint32_t c, double) {
-      if (act) cnt += sym_insert_smem(tab, c, logT);
+      if (act) cnt += SPG_BLOCK_CASFIRST ? sym_insert_cas(tab, c, logT) : sym_insert_smem(tab, c, logT);
     };
     if (use_seq(flop[i], ae - as)) for_row<true, false, 8, true>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
     else for_row<false, false>(A, B, as, ae, w, NW, ins, &s_next, &s_dl);
