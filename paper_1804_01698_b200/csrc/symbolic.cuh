@@ -48,6 +48,8 @@ __device__ __forceinline__ int sym_insert_cas(uint32_t *tab, uint32_t c, int log
 
 // Block tiers (block-shared tables): CAS-first single-slot probing instead of
 // the 4-slot chunks (A/B switch; also the numeric block tier's key probe).
+// Measured on C3: numeric block tiers 27.4 -> 26.2 ms, symbolic block tiers
+// 11.3 -> 25.0 ms (hits on hot columns become same-word atomics): off.
 #ifndef SPG_BLOCK_CASFIRST
 #define SPG_BLOCK_CASFIRST 0
 #endif
