@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--config", default="c3_rmat20")
     ap.add_argument("--sorted", type=int, default=1)
     ap.add_argument("--block-entries", type=int, default=1 << 28)
+    ap.add_argument("--row-start", type=int, default=0, help="resume: compare rows [row-start, m) only")
     args = ap.parse_args()
     import torch
     import paper_1804_01698_b200 as spg
@@ -49,7 +50,7 @@ def main():
     rows_done = ents = 0
     worst = 0.0
     bad_struct = bad_vals = 0
-    r0 = 0
+    r0 = args.row_start
     t_oracle = 0.0
     while r0 < A.nrows:
         r1 = int(np.searchsorted(g_rp, g_rp[r0] + args.block_entries, side="right")) - 1
@@ -84,7 +85,8 @@ def main():
     out = {"config": args.config, "sorted": bool(args.sorted), "rows_checked": rows_done,
            "rows_total": A.nrows, "entries_checked": ents, "nnz_C": nnz, "structure_mismatches": bad_struct,
            "value_violations": bad_vals, "max_rel_err": worst, "tolerance": 1e-12,
-           "ok": bad_struct == 0 and bad_vals == 0 and ents == nnz,
+           "row_start": args.row_start,
+           "ok": bad_struct == 0 and bad_vals == 0 and ents == nnz - int(g_rp[args.row_start]),
            "oracle_seconds": round(t_oracle, 1), "wall_seconds": round(time.time() - t0, 1),
            "oracle_threads": os.cpu_count()}
     print(json.dumps(out), flush=True)
